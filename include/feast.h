@@ -1,0 +1,164 @@
+/*
+ * feast.h — C ABI of the B200-native non-Hermitian FEAST quadrature projector
+ * (Tang, Kestyn & Polizzi, arXiv 1404.2891).  Library: paper_1404_2891_b200/libfeast_b200.so
+ *
+ * Problem (§2): A x = lambda B x, A, B dense n x n complex128.
+ * The contour (eq. ellipses) is the ellipse
+ *     phi(t) = c + r ( cos(pi/2 (1+t)) + i * aspect * sin(pi/2 (1+t)) ),  t in [-1, 3]
+ * with real semi-axis r and imaginary semi-axis r*aspect (reading R2 in DESIGN.md).
+ * A quadrature rule on [-1,1], applied on both halves t and 2-t (eq. pi), gives
+ * q poles z_j = phi_k and weights w_j = sigma_k (eq. quadrature_for_pi), i.e. the
+ * rational filter rho(mu) = sum_j w_j / (z_j - mu).
+ *
+ * The hot path (eq. Rasp; eq. Lasp, P:424-439 read as R4):
+ *     Q  = sum_j      w_j  (z_j B - A)^{-1} (B X)
+ *     QL = sum_j conj(w_j) (z_j B - A)^{-H} (B^H V)
+ * computed as: shift C_j = z_j B - A, blocked LU with partial pivoting P_j C_j = L_j U_j,
+ * multi-RHS substitution, fused weighted accumulation — all in this library's sm_100a kernels.
+ *
+ * CONVENTIONS (every entry point)
+ *   - Matrices are COLUMN-MAJOR complex128, interleaved (re, im) — the bytes of
+ *     torch.complex128 / cuDoubleComplex / C99 double _Complex.  "ld" is the leading
+ *     dimension in complex elements, ld >= n (or >= m0 for m0 x m0 matrices).
+ *   - Matrix arguments are DEVICE pointers (16-byte aligned), unless marked (host).
+ *   - All device work is enqueued on the handle's CUDA stream; every call returns after
+ *     synchronising that stream (host outputs are valid on return).
+ *   - The caller owns every matrix and the workspace; the library never frees caller memory.
+ *   - Return value: 0 = ok, < 0 = error (result not valid), > 0 = warning (result valid).
+ *     No exception or exit() crosses the ABI; feast_last_error() has the message.
+ *   - A handle is not re-entrant; use one handle per stream.
+ *
+ * MULTI-GPU (§5.5: parallelism over the linear systems)
+ *   Rank r of `world` owns the contiguous node block [r q/world, (r+1) q/world) (reading R17);
+ *   q % world must be 0.  feast_project / feast_project_left return this rank's PARTIAL sum
+ *   over its own nodes.  The node sum across ranks is one all-reduce of n x m0 complex128,
+ *   which feast_iterate performs through the callback registered with feast_set_allreduce
+ *   (the Python binding registers torch.distributed.all_reduce over NCCL).
+ */
+#ifndef FEAST_B200_H
+#define FEAST_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct feast_ctx* feast_handle;
+
+/* Quadrature rules (readings R1, R3):
+ *  FEAST_RULE_TRAPEZOID           composite midpoint rule with K = n_e/2 points on [-1,1]:
+ *                                 q = n_e poles at theta_j = 2 pi (j + 1/2)/q on a circle,
+ *                                 rho = 1/(1 + x^q) (BASELINE.json closed form); n_e even >= 2.
+ *  FEAST_RULE_TRAPEZOID_ENDPOINT  the paper's trapezoid with both endpoints:
+ *                                 K = n_e/2 + 1 points, q = 2(K-1) = n_e poles, rho = 1/(1 - x^q).
+ *  FEAST_RULE_GAUSS_LEGENDRE      K = n_e Gauss-Legendre points per half, q = 2 n_e. */
+enum { FEAST_RULE_TRAPEZOID = 0, FEAST_RULE_TRAPEZOID_ENDPOINT = 1, FEAST_RULE_GAUSS_LEGENDRE = 2 };
+
+/* R-FEAST (right projector only) or Bi-FEAST (both projectors). */
+enum { FEAST_RIGHT = 0, FEAST_BI = 1 };
+
+enum {
+  FEAST_OK = 0,
+  FEAST_E_ARG = -1,       /* invalid argument (sizes, radii, rule, q % world, null pointer, ld) */
+  FEAST_E_NOMEM = -2,     /* workspace missing or too small */
+  FEAST_E_SINGULAR = -3,  /* some node's min|u_ii|/max|u_ii| < 1e-14 or an exact zero pivot;
+                             Q is still written; feast_node_stats names the node */
+  FEAST_E_CUDA = -4,      /* CUDA / cuSOLVER failure (message in feast_last_error) */
+  FEAST_E_COMM = -5,      /* the registered all-reduce callback failed, or world > 1 without one */
+  FEAST_E_STATE = -6,     /* call out of order (e.g. no workspace bound) */
+  FEAST_E_REDUCED = -7,   /* reduced eigenproblem failed (B^ singular / QR failure) */
+  FEAST_W_ILLCOND = 1     /* some node's pivot ratio < 1e-10 (near-singular shifted matrix) */
+};
+
+/* Create a handle.
+ *  n >= 1, 1 <= m0 <= n         problem size and subspace width (p in the paper)
+ *  c_re, c_im, r, aspect        contour centre, real semi-axis r > 0, aspect a > 0
+ *  n_e, rule                    quadrature (see FEAST_RULE_*)
+ *  mode                         FEAST_RIGHT or FEAST_BI
+ *  b_is_identity                non-zero when B = I (B pointers may then be NULL)
+ *  rank, world                  node sharding (world >= 1, 0 <= rank < world, q % world == 0)
+ *  max_batch                    nodes factored concurrently (0 = all owned nodes); bounds
+ *                               the workspace at max_batch * 16 n^2 bytes plus blocks
+ *  cuda_stream                  cudaStream_t the work is enqueued on (NULL = legacy stream)
+ * Errors: FEAST_E_ARG, FEAST_E_CUDA. */
+int feast_init(feast_handle* h, int64_t n, int64_t m0, double c_re, double c_im, double r,
+               double aspect, int32_t n_e, int32_t rule, int32_t mode, int32_t b_is_identity,
+               int32_t rank, int32_t world, int32_t max_batch, void* cuda_stream);
+
+/* Device workspace size in bytes for this handle (caller allocates, e.g. with torch). */
+int feast_workspace_bytes(feast_handle h, size_t* bytes);
+
+/* Bind caller-owned device memory (>= feast_workspace_bytes, 256-byte aligned). */
+int feast_bind_workspace(feast_handle h, void* dev_ptr, size_t bytes);
+
+/* Quadrature data (host outputs): *q; z, w = 2*q doubles each (complex interleaved poles
+ * z_j and weights w_j); *j0, *j1 = this rank's owned node range.  Any pointer may be NULL. */
+int feast_nodes(feast_handle h, int32_t* q, double* z, double* w, int32_t* j0, int32_t* j1);
+
+/* Right projector, this rank's partial sum (eq. Rasp):
+ *   Q = sum_{j owned} w_j (z_j B - A)^{-1} (B X)       (B = NULL when b_is_identity)
+ * A, B: n x n; X, Q: n x m0.  Q is overwritten (X and Q must not alias).
+ * Returns FEAST_OK, FEAST_W_ILLCOND, FEAST_E_SINGULAR, FEAST_E_ARG, FEAST_E_STATE, FEAST_E_CUDA. */
+int feast_project(feast_handle h, const void* A, int64_t lda, const void* B, int64_t ldb,
+                  const void* X, int64_t ldx, void* Q, int64_t ldq);
+
+/* Left projector, this rank's partial sum (eq. Lasp, P:424-439 read as R4):
+ *   QL = sum_{j owned} conj(w_j) (z_j B - A)^{-H} (B^H V)
+ * solved with the conjugate-transposed factors of the same LU. */
+int feast_project_left(feast_handle h, const void* A, int64_t lda, const void* B, int64_t ldb,
+                       const void* V, int64_t ldv, void* QL, int64_t ldql);
+
+/* Both projectors from ONE factorisation per node (Bi-FEAST steps 4-5):
+ * Q as feast_project (from X) and QL as feast_project_left (from V). */
+int feast_project_bi(feast_handle h, const void* A, int64_t lda, const void* B, int64_t ldb,
+                     const void* X, int64_t ldx, const void* V, int64_t ldv,
+                     void* Q, int64_t ldq, void* QL, int64_t ldql);
+
+/* Reduced matrices (R-FEAST step 4; Bi-FEAST step 6):
+ *   Ahat = QL^H A Q,  Bhat = QL^H B Q      (QL = Q in R-FEAST: pass QL = NULL)
+ * Ahat, Bhat: m0 x m0 device, ld >= m0.  B = NULL when b_is_identity. */
+int feast_reduce(feast_handle h, const void* A, int64_t lda, const void* B, int64_t ldb,
+                 const void* Q, int64_t ldq, const void* QL, int64_t ldql,
+                 void* Ahat, int64_t ldah, void* Bhat, int64_t ldbh);
+
+/* All-reduce callback for world > 1: sum `count` float64 values at device pointer `buf`
+ * across ranks, in place, ordered on `cuda_stream`; return 0 on success. */
+typedef int (*feast_allreduce_fn)(void* buf, int64_t count, void* cuda_stream, void* user);
+int feast_set_allreduce(feast_handle h, feast_allreduce_fn fn, void* user);
+
+/* One FEAST iteration (R-FEAST P:503-517 / Bi-FEAST P:520-537):
+ *   project (+ all-reduce), orthonormalise U^ (and V^) (reading R13), reduce, solve the
+ *   m0 x m0 eigenproblem (outside the hot path; cuSOLVER), X <- U^ W with unit columns,
+ *   Bi: V <- V^ Z with Z = (B^ W)^-H (reading R5).
+ * X (n x m0, device) in/out; V (bi only, else NULL) in/out.
+ * Host outputs (may be NULL): ritz (2*m0 doubles, complex interleaved), resid (m0) =
+ *   ||A x - l B x||_2 / (||A||_F ||x||_2) (reading R11), flags (m0): bit0 = Ritz value
+ *   inside the contour, bit1 = candidate (inside and ||A x - l B x||/||x|| <= 1e-4).
+ * Returns as feast_project, plus FEAST_E_REDUCED, FEAST_E_COMM. */
+int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int64_t ldb,
+                  void* X, int64_t ldx, void* V, int64_t ldv,
+                  double* ritz, double* resid, int32_t* flags);
+
+/* Pivot diagnostics of the last projection (host outputs): min_rel_pivot[q] =
+ * min|u_ii| / max|u_ii| per node (owned nodes only; others are set to -1), *worst_node =
+ * index of the smallest ratio.  Either pointer may be NULL. */
+int feast_node_stats(feast_handle h, double* min_rel_pivot, int32_t* worst_node);
+
+/* Number of this library's kernels launched by the last call (for bench accounting). */
+int64_t feast_last_launch_count(feast_handle h);
+
+/* Message for the last error on this handle ("" if none).  Valid until the next call. */
+const char* feast_last_error(feast_handle h);
+
+/* Library version string. */
+const char* feast_version(void);
+
+/* Free the handle (not the caller's memory). */
+void feast_destroy(feast_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FEAST_B200_H */

@@ -1,0 +1,79 @@
+// kernels.h — internal launcher interfaces of the B200 FEAST library (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace feast {
+
+// ---------------------------------------------------------------- ZGEMM (DMMA)
+enum { ZG_SUB = 0,   // C -= op(A) B
+       ZG_GEN = 1 }; // C = alpha op(A) B + beta C
+struct ZgemmArgs {
+  int64_t M, N, K;
+  const double2* A; int64_t lda, sA;  // op(A) is M x K; A is M x K (N) or K x M (conj-transpose)
+  const double2* B; int64_t ldb, sB;  // K x N
+  double2* C; int64_t ldc, sC;        // M x N
+  double2 alpha, beta;
+  int batch;                          // batch index z adds z*sA, z*sB, z*sC
+};
+void zgemm_launch(const ZgemmArgs& p, bool conjA, int mode, cudaStream_t s);
+
+// ---------------------------------------------------------------- LU pieces
+// Batched matrices: matrix b at base + b*stride (complex elements), column-major, ld.
+struct Batched {
+  double2* p;
+  int64_t ld, stride;
+};
+
+// C_b = z_b B - A   (B == nullptr: B = I).  z: device array of batch poles.
+void shift_launch(Batched C, const double2* A, int64_t lda, const double2* B, int64_t ldb,
+                  const double2* z, int64_t n, int batch, cudaStream_t s);
+
+// Panel factorisation with partial pivoting of columns [k, k+w) (rows k..n-1) of each matrix.
+// ipiv: batch x n int32 (absolute row index swapped with row k+i), stats: batch x 2 doubles
+// (running min / max |u_ii|), info: batch int32 (first exact zero pivot, 1-based; 0 none).
+struct PanelCfg { int cluster; int W; int S; };
+PanelCfg panel_config(int64_t n);
+void panel_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info,
+                  int batch, const PanelCfg& cfg, cudaStream_t s);
+
+// Apply row swaps ipiv[k..k+w) to columns [c0, c1) of every matrix.
+void laswp_launch(Batched C, int64_t n, int64_t k, int w, const int32_t* ipiv, int64_t c0, int64_t c1,
+                  int batch, cudaStream_t s);
+
+// Triangular solve op(T) X = X in place, T = nb x nb diagonal block (nb <= 64),
+// X = nb x ncols.  lower_op: op(T) lower (forward); unit: unit diagonal; conjT: op = ^H.
+void trsm_launch(Batched T, Batched X, int nb, int64_t ncols, bool lower_op, bool unit, bool conjT,
+                 int batch, cudaStream_t s);
+
+void stats_init_launch(double* stats, int32_t* info, int batch, cudaStream_t s);
+// perm_b from ipiv_b (sequential swaps of rows 0..n-1); iperm (optional) = inverse permutation
+void perm_launch(const int32_t* ipiv, int32_t* perm, int32_t* iperm, int64_t n, int batch, cudaStream_t s);
+// gather: Y_b[i][c] = R[perm_b[i]][c]   (R shared by the batch: sR = 0 allowed)
+void gather_rows_launch(Batched Y, const double2* R, int64_t ldr, int64_t sR, const int32_t* perm,
+                        int64_t n, int64_t m, int batch, cudaStream_t s);
+// scatter: Out_b[perm_b[i]][c] = Y_b[i][c]
+void scatter_rows_launch(Batched Out, const double2* Y, int64_t ldy, int64_t sY, const int32_t* perm,
+                         int64_t n, int64_t m, int batch, cudaStream_t s);
+// copy R (shared) into every Y_b
+void broadcast_copy_launch(Batched Y, const double2* R, int64_t ldr, int64_t n, int64_t m, int batch,
+                           cudaStream_t s);
+
+// Q (+)= sum_b w_b Y_b[iperm_b[i]] (conj(w_b) if conjw; iperm null = identity), b increasing;
+// accumulate=false overwrites Q.
+void accum_launch(double2* Q, int64_t ldq, Batched Y, const double2* w, const int32_t* iperm, int64_t n, int64_t m,
+                  int batch, bool conjw, bool accumulate, cudaStream_t s);
+// C = alpha * sum_s P_s + beta C, P_s = M x N (ld M) partials at P + s*M*N
+void splitk_reduce_launch(double2* C, int64_t ldc, const double2* P, int64_t M, int64_t N, int splits,
+                          double2 alpha, double2 beta, cudaStream_t s);
+
+// Column residual norms: out[c] = || AX[:,c] - lam_c BX[:,c] ||_2 and xn[c] = || X[:,c] ||_2.
+void resid_launch(const double2* AX, const double2* BX, const double2* X, int64_t ld, const double2* lam,
+                  int64_t n, int64_t m, double* out, double* xn, cudaStream_t s);
+// || A ||_F^2 partial sums into out (one double, must be zeroed) — deterministic two-pass.
+void frob2_launch(const double2* A, int64_t lda, int64_t n, double* partial, int nparts, cudaStream_t s);
+// Scale columns of X by 1/xn[c] and rows of W by same: X[:,c] /= xn[c], W[:,c] /= xn[c]
+void colscale_launch(double2* X, int64_t ldx, int64_t n, double2* W, int64_t ldw, int64_t m,
+                     const double* xn, cudaStream_t s);
+
+}  // namespace feast

@@ -1,0 +1,255 @@
+"""Thin Python binding of the C ABI in include/feast.h (argument marshalling only).
+
+Every step of the FEAST hot path runs in libfeast_b200.so's sm_100a kernels; PyTorch only
+provides device memory, the CUDA stream and torch.distributed (the cross-rank node sum,
+P:910-913).  There is no CPU fallback: if the library is missing this module raises.
+
+Matrices are complex128 COLUMN-MAJOR CUDA tensors (stride(0) == 1, stride(1) = ld >= rows),
+e.g. ``colmajor(torch.from_numpy(np.asfortranarray(a)))`` or ``empty_colmajor(n, m)``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfeast_b200.so")
+
+RULE_TRAPEZOID = 0
+RULE_TRAPEZOID_ENDPOINT = 1
+RULE_GAUSS_LEGENDRE = 2
+RIGHT = 0
+BI = 1
+
+OK, E_ARG, E_NOMEM, E_SINGULAR, E_CUDA, E_COMM, E_STATE, E_REDUCED, W_ILLCOND = 0, -1, -2, -3, -4, -5, -6, -7, 1
+_NAMES = {E_ARG: "FEAST_E_ARG", E_NOMEM: "FEAST_E_NOMEM", E_SINGULAR: "FEAST_E_SINGULAR", E_CUDA: "FEAST_E_CUDA",
+          E_COMM: "FEAST_E_COMM", E_STATE: "FEAST_E_STATE", E_REDUCED: "FEAST_E_REDUCED"}
+
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p)
+
+# every symbol include/feast.h declares (checked by tests/test_abi.py)
+EXPORTS = ["feast_init", "feast_workspace_bytes", "feast_bind_workspace", "feast_nodes", "feast_project",
+           "feast_project_left", "feast_project_bi", "feast_reduce", "feast_set_allreduce", "feast_iterate",
+           "feast_node_stats", "feast_last_launch_count", "feast_last_error", "feast_version", "feast_destroy"]
+
+
+class FeastError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libfeast_b200.so (raises if it was not built: no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built; run `python -m paper_1404_2891_b200.build` (no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    P, I64, I32, D, SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_size_t
+    lib.feast_init.argtypes = [ctypes.POINTER(P), I64, I64, D, D, D, D, I32, I32, I32, I32, I32, I32, I32, P]
+    lib.feast_workspace_bytes.argtypes = [P, ctypes.POINTER(SZ)]
+    lib.feast_bind_workspace.argtypes = [P, P, SZ]
+    lib.feast_nodes.argtypes = [P, P, P, P, P, P]
+    lib.feast_project.argtypes = [P, P, I64, P, I64, P, I64, P, I64]
+    lib.feast_project_left.argtypes = [P, P, I64, P, I64, P, I64, P, I64]
+    lib.feast_project_bi.argtypes = [P, P, I64, P, I64, P, I64, P, I64, P, I64, P, I64]
+    lib.feast_reduce.argtypes = [P, P, I64, P, I64, P, I64, P, I64, P, I64, P, I64]
+    lib.feast_set_allreduce.argtypes = [P, ALLREDUCE_FN, P]
+    lib.feast_iterate.argtypes = [P, P, I64, P, I64, P, I64, P, I64, P, P, P]
+    lib.feast_node_stats.argtypes = [P, P, P]
+    lib.feast_last_launch_count.argtypes = [P]
+    lib.feast_last_launch_count.restype = I64
+    lib.feast_last_error.argtypes = [P]
+    lib.feast_last_error.restype = ctypes.c_char_p
+    lib.feast_version.restype = ctypes.c_char_p
+    lib.feast_destroy.argtypes = [P]
+    lib.feast_destroy.restype = None
+    _lib = lib
+    return lib
+
+
+def colmajor(t: torch.Tensor) -> torch.Tensor:
+    """Column-major copy of a 2-D tensor (complex128 kept)."""
+    return t.t().contiguous().t()
+
+
+def empty_colmajor(rows: int, cols: int, device="cuda", dtype=torch.complex128) -> torch.Tensor:
+    return torch.empty((cols, rows), dtype=dtype, device=device).t()
+
+
+def _ptr_ld(t, rows, name):
+    if t is None:
+        return None, 0
+    if t.dtype != torch.complex128 or not t.is_cuda or t.dim() != 2:
+        raise FeastError(E_ARG, f"{name} must be a 2-D complex128 CUDA tensor")
+    if t.shape[0] != rows or (t.shape[1] > 1 and t.stride(0) != 1):
+        raise FeastError(E_ARG, f"{name} must be column-major with {rows} rows")
+    ld = t.stride(1) if t.shape[1] > 1 else max(rows, 1)
+    return ctypes.c_void_p(t.data_ptr()), ld
+
+
+class _CudaPtr:
+    """__cuda_array_interface__ shim so the all-reduce callback can wrap a raw buffer."""
+
+    def __init__(self, ptr, count):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class Feast:
+    """One handle of the C ABI: contour, quadrature, node ownership and workspace."""
+
+    def __init__(self, n, m0, center=0j, r=1.0, aspect=1.0, n_e=8, rule=RULE_TRAPEZOID, mode=RIGHT,
+                 b_is_identity=True, rank=0, world=1, max_batch=0, device=None, group=None):
+        self.lib = load_library()
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.stream = torch.cuda.current_stream(self.device)
+        self.n, self.m0, self.mode, self.b_is_identity = int(n), int(m0), int(mode), bool(b_is_identity)
+        self.rank, self.world, self.group = int(rank), int(world), group
+        self.center, self.r, self.aspect = complex(center), float(r), float(aspect)
+        h = ctypes.c_void_p()
+        rc = self.lib.feast_init(ctypes.byref(h), self.n, self.m0, self.center.real, self.center.imag, self.r,
+                                 self.aspect, int(n_e), int(rule), self.mode, int(self.b_is_identity), self.rank,
+                                 self.world, int(max_batch), ctypes.c_void_p(self.stream.cuda_stream))
+        if rc != OK:
+            raise FeastError(rc, "feast_init rejected the arguments")
+        self.h = h
+        nbytes = ctypes.c_size_t()
+        self._check(self.lib.feast_workspace_bytes(self.h, ctypes.byref(nbytes)))
+        self.workspace = torch.empty(int(nbytes.value) + 256, dtype=torch.uint8, device=self.device)
+        base = self.workspace.data_ptr()
+        aligned = (base + 255) // 256 * 256
+        self._check(self.lib.feast_bind_workspace(self.h, ctypes.c_void_p(aligned), int(nbytes.value)))
+        self._ar = None
+        if self.world > 1:
+            self._ar = ALLREDUCE_FN(self._allreduce_cb)
+            self._check(self.lib.feast_set_allreduce(self.h, self._ar, None))
+
+    # ------------------------------------------------------------------ helpers
+    def _check(self, rc, allow_warn=True):
+        if rc < 0 or (rc > 0 and not allow_warn):
+            raise FeastError(rc, self.lib.feast_last_error(self.h).decode())
+        return rc
+
+    def _allreduce_cb(self, buf, count, stream, user):
+        try:
+            import torch.distributed as dist
+            t = torch.as_tensor(_CudaPtr(buf, count), device=self.device)
+            dist.all_reduce(t, group=self.group)
+            return 0
+        except Exception:  # noqa: BLE001 — reported as FEAST_E_COMM by the library
+            return 1
+
+    def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+        """Node sum across ranks: in-place all-reduce of a partial Q."""
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(t, group=self.group)
+        return t
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.feast_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    # ------------------------------------------------------------------ API
+    def nodes(self):
+        q = ctypes.c_int32()
+        self._check(self.lib.feast_nodes(self.h, ctypes.byref(q), None, None, None, None))
+        z = (ctypes.c_double * (2 * q.value))()
+        w = (ctypes.c_double * (2 * q.value))()
+        j0, j1 = ctypes.c_int32(), ctypes.c_int32()
+        self._check(self.lib.feast_nodes(self.h, None, z, w, ctypes.byref(j0), ctypes.byref(j1)))
+        zz = [complex(z[2 * i], z[2 * i + 1]) for i in range(q.value)]
+        ww = [complex(w[2 * i], w[2 * i + 1]) for i in range(q.value)]
+        return zz, ww, j0.value, j1.value
+
+    def project(self, A, B, X, Q=None, allreduce=True):
+        """Q = sum_j w_j (z_j B - A)^-1 (B X); this rank's nodes, then the cross-rank sum."""
+        Q = empty_colmajor(self.n, self.m0, self.device) if Q is None else Q
+        pa, lda = _ptr_ld(A, self.n, "A")
+        pb, ldb = _ptr_ld(B, self.n, "B")
+        px, ldx = _ptr_ld(X, self.n, "X")
+        pq, ldq = _ptr_ld(Q, self.n, "Q")
+        self.status = self._check(self.lib.feast_project(self.h, pa, lda, pb, ldb, px, ldx, pq, ldq))
+        if allreduce:
+            self.allreduce_(Q)
+        return Q
+
+    def project_left(self, A, B, V, QL=None, allreduce=True):
+        QL = empty_colmajor(self.n, self.m0, self.device) if QL is None else QL
+        pa, lda = _ptr_ld(A, self.n, "A")
+        pb, ldb = _ptr_ld(B, self.n, "B")
+        pv, ldv = _ptr_ld(V, self.n, "V")
+        pq, ldq = _ptr_ld(QL, self.n, "QL")
+        self.status = self._check(self.lib.feast_project_left(self.h, pa, lda, pb, ldb, pv, ldv, pq, ldq))
+        if allreduce:
+            self.allreduce_(QL)
+        return QL
+
+    def project_bi(self, A, B, X, V, Q=None, QL=None, allreduce=True):
+        Q = empty_colmajor(self.n, self.m0, self.device) if Q is None else Q
+        QL = empty_colmajor(self.n, self.m0, self.device) if QL is None else QL
+        pa, lda = _ptr_ld(A, self.n, "A")
+        pb, ldb = _ptr_ld(B, self.n, "B")
+        px, ldx = _ptr_ld(X, self.n, "X")
+        pv, ldv = _ptr_ld(V, self.n, "V")
+        pq, ldq = _ptr_ld(Q, self.n, "Q")
+        pl, ldl = _ptr_ld(QL, self.n, "QL")
+        self.status = self._check(self.lib.feast_project_bi(self.h, pa, lda, pb, ldb, px, ldx, pv, ldv, pq, ldq,
+                                                            pl, ldl))
+        if allreduce:
+            self.allreduce_(Q)
+            self.allreduce_(QL)
+        return Q, QL
+
+    def reduce(self, A, B, Q, QL=None, Ahat=None, Bhat=None):
+        Ahat = empty_colmajor(self.m0, self.m0, self.device) if Ahat is None else Ahat
+        Bhat = empty_colmajor(self.m0, self.m0, self.device) if Bhat is None else Bhat
+        pa, lda = _ptr_ld(A, self.n, "A")
+        pb, ldb = _ptr_ld(B, self.n, "B")
+        pq, ldq = _ptr_ld(Q, self.n, "Q")
+        pl, ldl = _ptr_ld(QL, self.n, "QL")
+        p1, ld1 = _ptr_ld(Ahat, self.m0, "Ahat")
+        p2, ld2 = _ptr_ld(Bhat, self.m0, "Bhat")
+        self._check(self.lib.feast_reduce(self.h, pa, lda, pb, ldb, pq, ldq, pl, ldl, p1, ld1, p2, ld2))
+        return Ahat, Bhat
+
+    def iterate(self, A, B, X, V=None):
+        """One R-FEAST / Bi-FEAST iteration; X (and V) updated in place."""
+        m = self.m0
+        ritz = (ctypes.c_double * (2 * m))()
+        res = (ctypes.c_double * m)()
+        flags = (ctypes.c_int32 * m)()
+        pa, lda = _ptr_ld(A, self.n, "A")
+        pb, ldb = _ptr_ld(B, self.n, "B")
+        px, ldx = _ptr_ld(X, self.n, "X")
+        pv, ldv = _ptr_ld(V, self.n, "V")
+        self.status = self._check(self.lib.feast_iterate(self.h, pa, lda, pb, ldb, px, ldx, pv, ldv, ritz, res,
+                                                         flags))
+        lam = [complex(ritz[2 * i], ritz[2 * i + 1]) for i in range(m)]
+        return {"lam": lam, "resid": list(res), "flags": list(flags)}
+
+    def node_stats(self):
+        zz, _, _, _ = self.nodes()
+        arr = (ctypes.c_double * len(zz))()
+        worst = ctypes.c_int32()
+        self._check(self.lib.feast_node_stats(self.h, arr, ctypes.byref(worst)))
+        return list(arr), worst.value
+
+    @property
+    def last_launch_count(self) -> int:
+        return int(self.lib.feast_last_launch_count(self.h))

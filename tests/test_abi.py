@@ -1,0 +1,97 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol include/feast.h
+declares, validates arguments (FEAST_E_ARG) and generates the same poles/weights as the
+oracle (node generation is host code in the library, written independently)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1404_2891_b200 import feast as fb
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "feast.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(feast_[a-z_]+)\s*\(", src)) - {"feast_allreduce_fn"})
+
+
+def test_exports_every_declared_symbol():
+    lib = fb.load_library()
+    decl = _declared()
+    assert set(decl) == set(fb.EXPORTS)
+    for name in decl:
+        assert hasattr(lib, name), name
+    assert b"sm_100a" in lib.feast_version()
+
+
+def _init(n=64, m0=8, c=0j, r=1.0, a=1.0, n_e=8, rule=0, mode=0, bid=1, rank=0, world=1, batch=0):
+    lib = fb.load_library()
+    h = ctypes.c_void_p()
+    rc = lib.feast_init(ctypes.byref(h), n, m0, c.real, c.imag, r, a, n_e, rule, mode, bid, rank, world, batch, None)
+    return rc, h
+
+
+@pytest.mark.parametrize("kw", [dict(n=0), dict(m0=0), dict(m0=65), dict(r=0.0), dict(r=-1.0), dict(a=0.0),
+                                dict(n_e=7), dict(n_e=0, rule=2), dict(rule=3), dict(mode=2), dict(world=3),
+                                dict(rank=1), dict(world=0), dict(n_e=6, rule=1, world=4), dict(n=40000)])
+def test_init_rejects_bad_arguments(kw):
+    rc, h = _init(**kw)
+    assert rc == fb.E_ARG and not h.value
+
+
+def _nodes(h):
+    lib = fb.load_library()
+    q = ctypes.c_int32()
+    lib.feast_nodes(h, ctypes.byref(q), None, None, None, None)
+    z = np.zeros(2 * q.value)
+    w = np.zeros(2 * q.value)
+    j0, j1 = ctypes.c_int32(), ctypes.c_int32()
+    lib.feast_nodes(h, None, z.ctypes.data_as(ctypes.c_void_p), w.ctypes.data_as(ctypes.c_void_p),
+                    ctypes.byref(j0), ctypes.byref(j1))
+    return z.view(np.complex128), w.view(np.complex128), j0.value, j1.value
+
+
+@pytest.mark.parametrize("c,r,a,n_e,rule", [(0j, 0.5, 1.0, 8, 0), (0.2 + 0.1j, 0.3, 1.0, 16, 0), (0j, 0.4, 0.15, 16, 2),
+                                            (0.5, 0.25, 1.0, 32, 0), (0j, 1.0, 1.0, 4, 1), (0j, 1.0, 1.0, 16, 1),
+                                            (1 - 1j, 2.0, 0.5, 5, 2)])
+def test_library_nodes_match_oracle(c, r, a, n_e, rule):
+    rc, h = _init(c=c, r=r, a=a, n_e=n_e, rule=rule)
+    assert rc == 0
+    z, w, j0, j1 = _nodes(h)
+    zo, wo = oracle.nodes(c, r, a, n_e, rule)
+    assert len(z) == len(zo) and (j0, j1) == (0, len(z))
+    for zi, wi in zip(zo, wo):
+        k = np.argmin(np.abs(z - zi))
+        assert abs(z[k] - zi) < 1e-14 * max(1, r) and abs(w[k] - wi) < 1e-14 * max(1, r)
+    fb.load_library().feast_destroy(h)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_node_ownership_partition(world):
+    import synth
+    owned = []
+    for rank in range(world):
+        rc, h = _init(n_e=16, rank=rank, world=world)
+        assert rc == 0
+        _, _, j0, j1 = _nodes(h)
+        assert (j0, j1) == synth.node_owner_range(16, rank, world)
+        owned += list(range(j0, j1))
+        fb.load_library().feast_destroy(h)
+    assert owned == list(range(16))
+
+
+def test_workspace_size_scales_with_batch():
+    lib = fb.load_library()
+    sizes = []
+    for batch in (1, 4):
+        rc, h = _init(n=512, m0=32, batch=batch)
+        b = ctypes.c_size_t()
+        assert lib.feast_workspace_bytes(h, ctypes.byref(b)) == 0
+        sizes.append(b.value)
+        lib.feast_destroy(h)
+    assert sizes[1] - sizes[0] >= 3 * 16 * 512 * 512

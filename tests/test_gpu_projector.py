@@ -1,0 +1,132 @@
+"""GPU parity of the projector hot path (eq. Rasp, eq. Lasp): the CUDA
+path through the C ABI vs the plain-C oracle on the same seeded inputs.  Bar (BASELINE
+north_star): relative Frobenius error <= 1e-10 in complex128."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_1404_2891_b200 import Feast, FeastError, feast as fb
+from gpu_util import dev, host, rel
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def _handle(P, mode=fb.RIGHT, **kw):
+    s = P.spec
+    return Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, mode, P.B is None, **kw)
+
+
+def _oracle_nodes(P):
+    s = P.spec
+    return oracle.nodes(s.c, s.r, s.aspect, s.n_e, s.rule)
+
+
+@pytest.mark.parametrize("key,n,m0", [("C1", None, None), ("C2", 300, 40), ("C2", 129, 7), ("C1", 64, 64),
+                                      ("C3", 384, 32), ("C4", 256, 48), ("C5", 200, 33)])
+def test_right_projector_parity(key, n, m0):
+    P = synth.make_pencil(key, n=n, m0=m0)
+    f = _handle(P)
+    Q = host(f.project(dev(P.A), dev(P.B), dev(P.X0)))
+    z, w = _oracle_nodes(P)
+    Qo = oracle.project(P.A, P.B, P.X0, z, w)
+    assert rel(Q, Qo) <= TOL
+    if P.V is not None:   # spectral pin as a second reference (eq. quadf_surM)
+        x = (P.lam - P.spec.c) / P.spec.r
+        Qs = P.V @ ((1 / (1 + x ** P.spec.q))[:, None] * np.linalg.solve(P.V, P.X0))
+        assert rel(Q, Qs) <= TOL
+
+
+def test_c2_full_size_parity():
+    P = synth.make_pencil("C2")
+    f = _handle(P)
+    Q = host(f.project(dev(P.A), dev(P.B), dev(P.X0)))
+    z, w = _oracle_nodes(P)
+    Qo = oracle.project(P.A, P.B, P.X0, z, w)
+    assert rel(Q, Qo) <= TOL
+
+
+@pytest.mark.parametrize("key,n,m0", [("C4", 256, 48), ("C2", 200, 24), ("C3", 130, 16)])
+def test_left_and_bi_projector_parity(key, n, m0):
+    P = synth.make_pencil(key, n=n, m0=m0)
+    Vin = synth.random_block(P.n, P.m0, 11)
+    z, w = _oracle_nodes(P)
+    f = _handle(P, mode=fb.BI)
+    QL = host(f.project_left(dev(P.A), dev(P.B), dev(Vin)))
+    QLo = oracle.project(P.A, P.B, Vin, z, w, left=True)
+    assert rel(QL, QLo) <= TOL
+    Qb, QLb = f.project_bi(dev(P.A), dev(P.B), dev(P.X0), dev(Vin))
+    assert rel(host(Qb), oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
+    assert rel(host(QLb), QLo) <= TOL
+
+
+@pytest.mark.parametrize("rule,n_e", [(fb.RULE_TRAPEZOID_ENDPOINT, 8), (fb.RULE_GAUSS_LEGENDRE, 4)])
+def test_rules(rule, n_e):
+    P = synth.make_pencil("C1", n=150, m0=20)
+    f = Feast(P.n, P.m0, 0j, 0.5, 1.0, n_e, rule, fb.RIGHT, True)
+    z, w = oracle.nodes(0j, 0.5, 1.0, n_e, rule)
+    assert rel(host(f.project(dev(P.A), None, dev(P.X0))), oracle.project(P.A, None, P.X0, z, w)) <= TOL
+
+
+@pytest.mark.parametrize("n,m0", [(1, 1), (2, 1), (63, 1), (64, 5), (65, 65), (130, 3)])
+def test_edge_sizes(n, m0):
+    P = synth.make_pencil("C2", n=n, m0=m0)
+    f = _handle(P)
+    z, w = _oracle_nodes(P)
+    assert rel(host(f.project(dev(P.A), dev(P.B), dev(P.X0))), oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
+
+
+def test_zero_block_and_batching():
+    P = synth.make_pencil("C2", n=160, m0=12)
+    z, w = _oracle_nodes(P)
+    Qo = oracle.project(P.A, P.B, P.X0, z, w)
+    for batch in (1, 3, 16):   # nodes factored concurrently; ragged last batch for 3
+        f = _handle(P, max_batch=batch)
+        assert rel(host(f.project(dev(P.A), dev(P.B), dev(P.X0))), Qo) <= TOL
+    f = _handle(P)
+    Z = f.project(dev(P.A), dev(P.B), dev(np.zeros((160, 12))))
+    assert torch.count_nonzero(Z).item() == 0
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_virtual_ranks_partition(world):
+    """Rank r's partial over its nodes (reading R17), summed over r, equals the full Q
+    (the node sum the NCCL all-reduce performs)."""
+    P = synth.make_pencil("C2", n=200, m0=16)
+    z, w = _oracle_nodes(P)
+    Qo = oracle.project(P.A, P.B, P.X0, z, w)
+    tot = 0
+    for r in range(world):
+        f = _handle(P, rank=r, world=world)
+        part = host(f.project(dev(P.A), dev(P.B), dev(P.X0), allreduce=False))
+        j0, j1 = synth.node_owner_range(P.q, r, world)
+        assert rel(part, oracle.project(P.A, P.B, P.X0, z, w, j0, j1)) <= TOL
+        tot = tot + part
+    assert rel(tot, Qo) <= TOL
+
+
+def test_singular_node_reported():
+    # pole exactly on an eigenvalue: midpoint rule on the unit circle with q = 4 has a pole at
+    # exp(i pi/4); make it an eigenvalue of a diagonal A
+    p = np.exp(1j * np.pi / 4)
+    A = np.diag([p, 0.1, 3.0, -0.2 + 0.1j]).astype(complex)
+    f = Feast(4, 2, 0j, 1.0, 1.0, 4, fb.RULE_TRAPEZOID, fb.RIGHT, True)
+    zz, _, _, _ = f.nodes()
+    A[0, 0] = zz[0]
+    with pytest.raises(FeastError) as e:
+        f.project(dev(A), None, dev(np.eye(4)[:, :2]))
+    assert e.value.code == fb.E_SINGULAR
+    stats, worst = f.node_stats()
+    assert worst == 0 and stats[0] == 0.0
+
+
+def test_reduce_parity():
+    P = synth.make_pencil("C2", n=300, m0=40)
+    f = _handle(P)
+    Qd = f.project(dev(P.A), dev(P.B), dev(P.X0))
+    Ah, Bh = f.reduce(dev(P.A), dev(P.B), Qd)
+    Q = host(Qd)
+    assert rel(host(Ah), oracle.gemm(Q, oracle.gemm(P.A, Q), opa=2)) <= 1e-12
+    assert rel(host(Bh), oracle.gemm(Q, oracle.gemm(P.B, Q), opa=2)) <= 1e-12
