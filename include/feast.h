@@ -149,6 +149,17 @@ int feast_node_stats(feast_handle h, double* min_rel_pivot, int32_t* worst_node)
 /* Number of this library's kernels launched by the last call (for bench accounting). */
 int64_t feast_last_launch_count(feast_handle h);
 
+/* Per-kernel-class timing (bench roofline accounting).  feast_profile(h, 1) starts recording
+ * a CUDA-event pair around every launch of this library on the launching stream (and clears
+ * earlier records); feast_profile(h, 0) stops.  feast_profile_summary aggregates the records of
+ * one class: launches, summed event time (ms), algorithmic flops and algorithmic bytes
+ * (DESIGN.md "Roofline" defines them per class).  Classes: */
+enum { FEAST_K_SHIFT = 0, FEAST_K_PANEL = 1, FEAST_K_LASWP = 2, FEAST_K_TRSM = 3, FEAST_K_ZGEMM = 4,
+       FEAST_K_PERM = 5, FEAST_K_ACCUM = 6, FEAST_K_OTHER = 7 };
+int feast_profile(feast_handle h, int32_t enable);
+int feast_profile_summary(feast_handle h, int32_t kclass, int64_t* launches, double* ms, double* flops,
+                          double* bytes);
+
 /* Message for the last error on this handle ("" if none).  Valid until the next call. */
 const char* feast_last_error(feast_handle h);
 

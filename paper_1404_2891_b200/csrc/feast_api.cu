@@ -18,6 +18,7 @@
 #include "../../include/feast.h"
 #include "common.cuh"
 #include "kernels.h"
+#include "prof.h"
 
 using feast::Batched;
 using feast::ZgemmArgs;
@@ -679,6 +680,35 @@ int feast_node_stats(feast_handle h, double* min_rel_pivot, int32_t* worst_node)
 }
 
 int64_t feast_last_launch_count(feast_handle h) { return h ? h->launches : 0; }
+
+int feast_profile(feast_handle h, int32_t enable) {
+  if (!h) return FEAST_E_ARG;
+  feast::Prof& p = feast::prof();
+  p.on = enable != 0;
+  p.recs.clear();
+  p.used = 0;
+  return FEAST_OK;
+}
+
+int feast_profile_summary(feast_handle h, int32_t kclass, int64_t* launches, double* ms, double* flops,
+                          double* bytes) {
+  if (!h || kclass < 0 || kclass >= feast::K_NCLASS) return FEAST_E_ARG;
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  CUDA_TRY(h, cudaDeviceSynchronize());
+  int64_t c = 0;
+  double t = 0, f = 0, b = 0;
+  for (const auto& r : feast::prof().recs) {
+    if (r.cls != kclass) continue;
+    float e = 0.f;
+    CUDA_TRY(h, cudaEventElapsedTime(&e, r.a, r.b));
+    ++c; t += e; f += r.flops; b += r.bytes;
+  }
+  if (launches) *launches = c;
+  if (ms) *ms = t;
+  if (flops) *flops = f;
+  if (bytes) *bytes = b;
+  return FEAST_OK;
+}
 
 const char* feast_last_error(feast_handle h) { return h ? h->err.c_str() : "null handle"; }
 

@@ -12,11 +12,16 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "prof.h"
 
 namespace cg = cooperative_groups;
 
 namespace feast {
 thread_local int64_t g_launches = 0;
+Prof& prof() {
+  static thread_local Prof p;
+  return p;
+}
 
 // ============================================================================ shift
 // C_b = z_b B - A  (HBM-bound: reads A (+B), writes C_b).
@@ -39,6 +44,7 @@ __global__ void shift_kernel(Batched C, const double2* __restrict__ A, int64_t l
 
 void shift_launch(Batched C, const double2* A, int64_t lda, const double2* B, int64_t ldb,
                   const double2* z, int64_t n, int batch, cudaStream_t s) {
+  ProfScope ps_(K_SHIFT, 0.0, (double)batch * n * n * 16.0 * (B ? 3 : 2), s);
   const int threads = 256;
   unsigned gx = (unsigned)((n + threads - 1) / threads);
   if (gx > 8) gx = 8;
@@ -330,6 +336,7 @@ PanelCfg panel_config(int64_t n) {
 
 void panel_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info,
                   int batch, const PanelCfg& cfg, cudaStream_t s) {
+  const double L_ = (double)(n - k); ProfScope ps_(K_PANEL, (double)batch * (4.0 * L_ * w * w - 4.0 * w * (double)w * w / 3.0), 0.0, s);
   if (cfg.W == 8 && cfg.S == 1) panel_launch_t<8, 1>(C, n, k, w, ipiv, stats, info, batch, cfg.cluster, s);
   else if (cfg.W == 8 && cfg.S == 2) panel_launch_t<8, 2>(C, n, k, w, ipiv, stats, info, batch, cfg.cluster, s);
   else if (cfg.W == 8 && cfg.S == 4) panel_launch_t<8, 4>(C, n, k, w, ipiv, stats, info, batch, cfg.cluster, s);
@@ -342,6 +349,7 @@ __global__ void stats_init_kernel(double* stats, int32_t* info, int batch) {
 }
 
 void stats_init_launch(double* stats, int32_t* info, int batch, cudaStream_t s) {
+  ProfScope ps_(K_OTHER, 0.0, 0.0, s);
   stats_init_kernel<<<(batch + 127) / 128, 128, 0, s>>>(stats, info, batch);
   count_launch();
 }
@@ -374,6 +382,7 @@ __global__ void laswp_kernel(Batched C, int64_t n, int64_t k, int w, const int32
 
 void laswp_launch(Batched C, int64_t n, int64_t k, int w, const int32_t* ipiv, int64_t c0, int64_t c1,
                   int batch, cudaStream_t s) {
+  ProfScope ps_(K_LASWP, 0.0, (double)batch * (c1 - c0) * w * 64.0, s);
   // here [c0, c1) indexes the n - w columns outside the panel
   if (c1 <= c0) return;
   const int threads = 128;
@@ -453,6 +462,7 @@ void trsm_t(Batched T, Batched X, int nb, int64_t ncols, int batch, cudaStream_t
 
 void trsm_launch(Batched T, Batched X, int nb, int64_t ncols, bool lower_op, bool unit, bool conjT, int batch,
                  cudaStream_t s) {
+  ProfScope ps_(K_TRSM, (double)batch * 4.0 * nb * nb * ncols, 0.0, s);
   if (ncols <= 0 || nb <= 0) return;
 #define TR_CASE(L, U, C) \
   if (lower_op == L && unit == U && conjT == C) { trsm_t<L, U, C>(T, X, nb, ncols, batch, s); return; }
@@ -492,6 +502,7 @@ __global__ void perm_kernel(const int32_t* __restrict__ ipiv_all, int32_t* __res
 }
 
 void perm_launch(const int32_t* ipiv, int32_t* perm, int32_t* iperm, int64_t n, int batch, cudaStream_t s) {
+  ProfScope ps_(K_PERM, 0.0, (double)batch * n * 12.0, s);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -514,6 +525,7 @@ __global__ void gather_rows_kernel(Batched Y, const double2* __restrict__ R, int
 
 void gather_rows_launch(Batched Y, const double2* R, int64_t ldr, int64_t sR, const int32_t* perm, int64_t n,
                         int64_t m, int batch, cudaStream_t s) {
+  ProfScope ps_(K_PERM, 0.0, (double)batch * n * m * 36.0, s);
   unsigned gx = (unsigned)((n + 255) / 256);
   if (gx > 16) gx = 16;
   gather_rows_kernel<<<dim3(gx, (unsigned)m, (unsigned)batch), 256, 0, s>>>(Y, R, ldr, sR, perm, n);
@@ -533,6 +545,7 @@ __global__ void scatter_rows_kernel(Batched Out, const double2* __restrict__ Y, 
 
 void scatter_rows_launch(Batched Out, const double2* Y, int64_t ldy, int64_t sY, const int32_t* perm, int64_t n,
                          int64_t m, int batch, cudaStream_t s) {
+  ProfScope ps_(K_PERM, 0.0, (double)batch * n * m * 36.0, s);
   unsigned gx = (unsigned)((n + 255) / 256);
   if (gx > 16) gx = 16;
   scatter_rows_kernel<<<dim3(gx, (unsigned)m, (unsigned)batch), 256, 0, s>>>(Out, Y, ldy, sY, perm, n);
@@ -550,6 +563,7 @@ __global__ void broadcast_copy_kernel(Batched Y, const double2* __restrict__ R, 
 
 void broadcast_copy_launch(Batched Y, const double2* R, int64_t ldr, int64_t n, int64_t m, int batch,
                            cudaStream_t s) {
+  ProfScope ps_(K_PERM, 0.0, (double)batch * n * m * 32.0, s);
   unsigned gx = (unsigned)((n + 255) / 256);
   if (gx > 16) gx = 16;
   broadcast_copy_kernel<<<dim3(gx, (unsigned)m, (unsigned)batch), 256, 0, s>>>(Y, R, ldr, n);
@@ -576,6 +590,7 @@ __global__ void accum_kernel(double2* __restrict__ Q, int64_t ldq, Batched Y, co
 
 void accum_launch(double2* Q, int64_t ldq, Batched Y, const double2* w, const int32_t* iperm, int64_t n, int64_t m,
                   int batch, bool conjw, bool accumulate, cudaStream_t s) {
+  ProfScope ps_(K_ACCUM, (double)batch * n * m * 8.0, (double)(batch + (accumulate ? 2 : 1)) * n * m * 16.0, s);
   unsigned gx = (unsigned)((n + 255) / 256);
   if (gx > 16) gx = 16;
   accum_kernel<<<dim3(gx, (unsigned)m), 256, 0, s>>>(Q, ldq, Y, w, iperm, n, batch, conjw, accumulate);
@@ -597,6 +612,7 @@ __global__ void splitk_reduce_kernel(double2* C, int64_t ldc, const double2* P, 
 
 void splitk_reduce_launch(double2* C, int64_t ldc, const double2* P, int64_t M, int64_t N, int splits,
                           double2 alpha, double2 beta, cudaStream_t s) {
+  ProfScope ps_(K_OTHER, 0.0, (double)(splits + 1) * M * N * 16.0, s);
   unsigned gx = (unsigned)((M + 255) / 256);
   if (gx > 16) gx = 16;
   splitk_reduce_kernel<<<dim3(gx, (unsigned)N), 256, 0, s>>>(C, ldc, P, M, N, splits, alpha, beta);
@@ -638,6 +654,7 @@ __global__ void resid_kernel(const double2* AX, const double2* BX, const double2
 
 void resid_launch(const double2* AX, const double2* BX, const double2* X, int64_t ld, const double2* lam,
                   int64_t n, int64_t m, double* out, double* xn, cudaStream_t s) {
+  ProfScope ps_(K_OTHER, 0.0, 0.0, s);
   resid_kernel<<<(unsigned)m, 256, 0, s>>>(AX, BX, X, ld, lam, n, out, xn);
   count_launch();
 }
@@ -654,6 +671,7 @@ __global__ void frob2_kernel(const double2* A, int64_t lda, int64_t n, double* p
 }
 
 void frob2_launch(const double2* A, int64_t lda, int64_t n, double* partial, int nparts, cudaStream_t s) {
+  ProfScope ps_(K_OTHER, 0.0, 0.0, s);
   frob2_kernel<<<nparts, 256, 0, s>>>(A, lda, n, partial);
   count_launch();
 }
@@ -675,6 +693,7 @@ __global__ void colscale_kernel(double2* X, int64_t ldx, int64_t n, double2* W, 
 
 void colscale_launch(double2* X, int64_t ldx, int64_t n, double2* W, int64_t ldw, int64_t m, const double* xn,
                      cudaStream_t s) {
+  ProfScope ps_(K_OTHER, 0.0, 0.0, s);
   unsigned gx = (unsigned)((n + 255) / 256);
   if (gx > 16) gx = 16;
   colscale_kernel<<<dim3(gx, (unsigned)m), 256, 0, s>>>(X, ldx, n, W, ldw, m, xn);

@@ -22,6 +22,7 @@
 // fragment load bank-conflict free (A: ld 68 complex, B: ld 18 complex).
 #include "common.cuh"
 #include "kernels.h"
+#include "prof.h"
 
 namespace feast {
 namespace {
@@ -175,6 +176,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_kernel(ZgemmArgs p) {
 
 template <bool CONJA, int MODE>
 void launch_t(const ZgemmArgs& p, cudaStream_t s) {
+  ProfScope ps_(K_ZGEMM, 8.0 * (double)p.M * (double)p.N * (double)p.K * p.batch, 0.0, s);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(zgemm_dmma_kernel<CONJA, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -32,7 +32,9 @@ ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, c
 # every symbol include/feast.h declares (checked by tests/test_abi.py)
 EXPORTS = ["feast_init", "feast_workspace_bytes", "feast_bind_workspace", "feast_nodes", "feast_project",
            "feast_project_left", "feast_project_bi", "feast_reduce", "feast_set_allreduce", "feast_iterate",
-           "feast_node_stats", "feast_last_launch_count", "feast_last_error", "feast_version", "feast_destroy"]
+           "feast_node_stats", "feast_last_launch_count", "feast_profile", "feast_profile_summary", "feast_last_error",
+           "feast_version", "feast_destroy"]
+K_CLASSES = ["shift", "panel", "laswp", "trsm", "zgemm", "perm", "accum", "other"]
 
 
 class FeastError(RuntimeError):
@@ -66,6 +68,8 @@ def load_library(path: str = LIB_PATH):
     lib.feast_node_stats.argtypes = [P, P, P]
     lib.feast_last_launch_count.argtypes = [P]
     lib.feast_last_launch_count.restype = I64
+    lib.feast_profile.argtypes = [P, I32]
+    lib.feast_profile_summary.argtypes = [P, I32, P, P, P, P]
     lib.feast_last_error.argtypes = [P]
     lib.feast_last_error.restype = ctypes.c_char_p
     lib.feast_version.restype = ctypes.c_char_p
@@ -249,6 +253,20 @@ class Feast:
         worst = ctypes.c_int32()
         self._check(self.lib.feast_node_stats(self.h, arr, ctypes.byref(worst)))
         return list(arr), worst.value
+
+    def profile(self, enable: bool):
+        """Start (clears) / stop per-kernel-class CUDA-event timing of this library's launches."""
+        self._check(self.lib.feast_profile(self.h, int(bool(enable))))
+
+    def profile_summary(self):
+        """{class: {launches, ms, flops, bytes}} of the launches recorded since profile(True)."""
+        out = {}
+        for i, name in enumerate(K_CLASSES):
+            c, ms, fl, by = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+            self._check(self.lib.feast_profile_summary(self.h, i, ctypes.byref(c), ctypes.byref(ms), ctypes.byref(fl),
+                                                       ctypes.byref(by)))
+            out[name] = {"launches": c.value, "ms": ms.value, "flops": fl.value, "bytes": by.value}
+        return out
 
     @property
     def last_launch_count(self) -> int:
