@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -33,12 +34,15 @@ struct feast_ctx {
   cudaStream_t stream = nullptr;
   int nb = 64;
   feast::PanelCfg pcfg{};
+  int smem_cs = 0;   // cluster size of the shared-memory panel kernel (0: register-chunk kernel)
   int64_t ldc = 0;
   // workspace
   void* ws = nullptr;
   size_t ws_bytes = 0;
   double2 *Cw = nullptr, *Y = nullptr, *YL = nullptr, *R = nullptr, *RL = nullptr, *zd = nullptr, *wd = nullptr;
   double2 *AQ = nullptr, *BQ = nullptr, *SK = nullptr;
+  double2* Inv = nullptr;          // batch x nblk x {L^-1, U^-1} 64x64 diagonal-block inverses
+  int64_t inv_stride = 0, nblk = 0;
   int64_t sk_elems = 0;
   int32_t *ipiv = nullptr, *perm = nullptr, *iperm = nullptr, *info = nullptr;
   double* stats = nullptr;
@@ -177,6 +181,7 @@ int make_nodes(feast_ctx* h) {
 }
 
 Batched bat(double2* p, int64_t ld, int64_t stride) { return Batched{p, ld, stride}; }
+const double2* inv_ptr(feast_ctx* h, int64_t kb, int which) { return h->Inv + (kb * 2 + which) * 4096; }
 
 // ---------------------------------------------------------------- GEMM helpers
 // C = alpha op(A) B + beta C (single), with split-K when the output tile grid is too small
@@ -219,17 +224,36 @@ void lu_batched(feast_ctx* h, int nbat) {
   double2* C = h->Cw;
   for (int64_t k = 0; k < n; k += h->nb) {
     const int w = (int)std::min<int64_t>(h->nb, n - k);
-    feast::panel_launch(bat(C, ld, st), n, k, w, h->ipiv, h->stats_cur, h->info_cur, nbat, h->pcfg, h->stream);
-    if (n - w > 0) feast::laswp_launch(bat(C, ld, st), n, k, w, h->ipiv, 0, n - w, nbat, h->stream);
+    if (h->smem_cs) {
+      feast::panel_smem_launch(bat(C, ld, st), n, k, w, h->ipiv, h->stats_cur, h->info_cur, nbat, h->smem_cs,
+                               h->stream);
+      feast::laswp_launch(bat(C, ld, st), n, k, w, h->ipiv, 0, n, nbat, h->stream, false);
+    } else {
+      feast::panel_launch(bat(C, ld, st), n, k, w, h->ipiv, h->stats_cur, h->info_cur, nbat, h->pcfg, h->stream);
+      if (n - w > 0) feast::laswp_launch(bat(C, ld, st), n, k, w, h->ipiv, 0, n - w, nbat, h->stream);
+    }
+    // L_kk^-1 and U_kk^-1 (the latter for the substitutions)
+    feast::trtri_launch(bat(C, ld, st), n, k / 64, 1, h->Inv, h->inv_stride, 2, nbat, h->stream);
     const int64_t rest = n - k - w;
     if (rest > 0) {
-      feast::trsm_launch(bat(C + k + k * ld, ld, st), bat(C + k + (k + w) * ld, ld, st), w, rest, true, true, false,
-                         nbat, h->stream);
+      // U12 = L11^-1 A12  (in-place DMMA GEMM, M = w <= 64)
+      ZgemmArgs u{w, rest, w, inv_ptr(h, k / 64, 0), 64, h->inv_stride, C + k + (k + w) * ld, ld, st,
+                  C + k + (k + w) * ld, ld, st, make_double2(1, 0), make_double2(0, 0), nbat};
+      feast::zgemm_launch(u, false, feast::ZG_GEN, h->stream);
+      // A22 -= L21 U12
       ZgemmArgs p{rest, rest, w, C + (k + w) + k * ld, ld, st, C + k + (k + w) * ld, ld, st,
                   C + (k + w) + (k + w) * ld, ld, st, make_double2(-1, 0), make_double2(1, 0), nbat};
       feast::zgemm_launch(p, false, feast::ZG_SUB, h->stream);
     }
   }
+}
+
+// Y_k <- op(T_kk^-1) Y_k in place (M = w <= 64): which 0 = L^-1, 1 = U^-1; conj: (.)^H
+void diag_apply(feast_ctx* h, double2* Y, int64_t k, int w, int which, bool conj, int nbat) {
+  const int64_t ld = h->ldc, sy = ld * h->m0;
+  ZgemmArgs p{w, h->m0, w, inv_ptr(h, k / 64, which), 64, h->inv_stride, Y + k, ld, sy, Y + k, ld, sy,
+              make_double2(1, 0), make_double2(0, 0), nbat};
+  feast::zgemm_launch(p, conj, feast::ZG_GEN, h->stream);
 }
 
 // Y <- U^-1 L^-1 Y  (Y already row-permuted)
@@ -238,7 +262,7 @@ void solve_right(feast_ctx* h, double2* Y, int nbat) {
   double2* C = h->Cw;
   for (int64_t k = 0; k < n; k += h->nb) {
     const int w = (int)std::min<int64_t>(h->nb, n - k);
-    feast::trsm_launch(bat(C + k + k * ld, ld, st), bat(Y + k, ld, sy), w, m, true, true, false, nbat, h->stream);
+    diag_apply(h, Y, k, w, 0, false, nbat);
     const int64_t rest = n - k - w;
     if (rest > 0) {
       ZgemmArgs p{rest, m, w, C + (k + w) + k * ld, ld, st, Y + k, ld, sy, Y + k + w, ld, sy,
@@ -249,7 +273,7 @@ void solve_right(feast_ctx* h, double2* Y, int nbat) {
   const int64_t last = ((n - 1) / h->nb) * h->nb;
   for (int64_t k = last; k >= 0; k -= h->nb) {
     const int w = (int)std::min<int64_t>(h->nb, n - k);
-    feast::trsm_launch(bat(C + k + k * ld, ld, st), bat(Y + k, ld, sy), w, m, false, false, false, nbat, h->stream);
+    diag_apply(h, Y, k, w, 1, false, nbat);
     if (k > 0) {
       ZgemmArgs p{k, m, w, C + k * ld, ld, st, Y + k, ld, sy, Y, ld, sy, make_double2(-1, 0), make_double2(1, 0), nbat};
       feast::zgemm_launch(p, false, feast::ZG_SUB, h->stream);
@@ -263,7 +287,7 @@ void solve_left(feast_ctx* h, double2* Y, int nbat) {
   double2* C = h->Cw;
   for (int64_t k = 0; k < n; k += h->nb) {  // U^H: lower, non-unit
     const int w = (int)std::min<int64_t>(h->nb, n - k);
-    feast::trsm_launch(bat(C + k + k * ld, ld, st), bat(Y + k, ld, sy), w, m, true, false, true, nbat, h->stream);
+    diag_apply(h, Y, k, w, 1, true, nbat);      // (U_kk^H)^-1 = (U_kk^-1)^H
     const int64_t rest = n - k - w;
     if (rest > 0) {
       // Y[k+w:] -= (U[k:k+w, k+w:])^H Y[k:k+w]
@@ -275,7 +299,7 @@ void solve_left(feast_ctx* h, double2* Y, int nbat) {
   const int64_t last = ((n - 1) / h->nb) * h->nb;
   for (int64_t k = last; k >= 0; k -= h->nb) {  // L^H: upper, unit
     const int w = (int)std::min<int64_t>(h->nb, n - k);
-    feast::trsm_launch(bat(C + k + k * ld, ld, st), bat(Y + k, ld, sy), w, m, false, true, true, nbat, h->stream);
+    diag_apply(h, Y, k, w, 0, true, nbat);      // (L_kk^H)^-1 = (L_kk^-1)^H
     if (k > 0) {
       // Y[0:k] -= (L[k:k+w, 0:k])^H Y[k:k+w]
       ZgemmArgs p{k, m, w, C + k, ld, st, Y + k, ld, sy, Y, ld, sy, make_double2(-1, 0), make_double2(1, 0), nbat};
@@ -448,6 +472,14 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   h->batch = std::max(1, max_batch == 0 ? owned : std::min<int>(max_batch, owned));
   h->pcfg = feast::panel_config(n);
   if (h->pcfg.cluster == 0) { delete h; return FEAST_E_ARG; }
+  // panel strategy: shared-memory cluster panel when the n x nb panel fits in <= 16 CTAs
+  h->smem_cs = 0;
+  h->nb = 64;   // the diagonal-block inverses (trtri) use 64-row blocks
+  for (int cs = 1; cs <= 16; cs *= 2)
+    if (feast::panel_smem_fits(n, 64, cs)) { h->smem_cs = cs; break; }
+  if (const char* e = getenv("FEAST_PANEL")) {   // debugging override: "reg" = register-chunk kernel
+    if (e[0] == 'r') { h->smem_cs = 0; h->nb = 64; }
+  }
   h->ldc = (n + 7) / 8 * 8;
   *out = h;
   return FEAST_OK;
@@ -466,6 +498,9 @@ static size_t layout(feast_ctx* h, char* base) {
   h->BQ = !h->b_id ? (double2*)take((size_t)ld * m * 16) : nullptr;
   h->sk_elems = std::max<int64_t>(8 * m * m, (int64_t)4 * ld * m);
   h->SK = (double2*)take((size_t)h->sk_elems * 16);
+  h->nblk = (n + 63) / 64;
+  h->inv_stride = h->nblk * 2 * 4096;
+  h->Inv = (double2*)take((size_t)h->batch * h->inv_stride * 16);
   h->ipiv = (int32_t*)take((size_t)h->batch * n * 4);
   h->perm = (int32_t*)take((size_t)h->batch * n * 4);
   h->iperm = (int32_t*)take((size_t)h->batch * n * 4);

@@ -38,14 +38,25 @@ void panel_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double*
                   int batch, const PanelCfg& cfg, cudaStream_t s);
 
 // Apply row swaps ipiv[k..k+w) to columns [c0, c1) of every matrix.
+// skip_panel: [c0, c1) indexes the n - w columns outside the panel; else all columns.
 void laswp_launch(Batched C, int64_t n, int64_t k, int w, const int32_t* ipiv, int64_t c0, int64_t c1,
-                  int batch, cudaStream_t s);
+                  int batch, cudaStream_t s, bool skip_panel = true);
+// Cluster panel with the panel resident in shared memory (rows never moved; see panel_smem.cu).
+bool panel_smem_fits(int64_t n, int w, int cs);
+void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info, int batch,
+                       int cs, cudaStream_t s);
 
 // Triangular solve op(T) X = X in place, T = nb x nb diagonal block (nb <= 64),
 // X = nb x ncols.  lower_op: op(T) lower (forward); unit: unit diagonal; conjT: op = ^H.
 void trsm_launch(Batched T, Batched X, int nb, int64_t ncols, bool lower_op, bool unit, bool conjT,
                  int batch, cudaStream_t s);
 
+// Inverses of the 64x64 diagonal blocks kb0 .. kb0+nblocks-1 of every factored node:
+// inv + b*inv_node_stride + (kb*2 + 0) * 4096 = L_kk^-1 (unit lower), (kb*2 + 1) * 4096 = U_kk^-1,
+// each 64 x 64 column-major (ld 64), identity-padded for a partial last block.
+// which: 0 = L only, 1 = U only, 2 = both.
+void trtri_launch(Batched C, int64_t n, int64_t kb0, int64_t nblocks, double2* inv, int64_t inv_node_stride, int which,
+                  int batch, cudaStream_t s);
 void stats_init_launch(double* stats, int32_t* info, int batch, cudaStream_t s);
 // perm_b from ipiv_b (sequential swaps of rows 0..n-1); iperm (optional) = inverse permutation
 void perm_launch(const int32_t* ipiv, int32_t* perm, int32_t* iperm, int64_t n, int batch, cudaStream_t s);

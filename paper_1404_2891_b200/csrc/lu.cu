@@ -358,7 +358,7 @@ void stats_init_launch(double* stats, int32_t* info, int batch, cudaStream_t s) 
 // Apply the w swaps of panel k to every column outside the panel.
 // Thread per column; each swap exchanges two 16-byte complex entries of that column.
 __global__ void laswp_kernel(Batched C, int64_t n, int64_t k, int w, const int32_t* __restrict__ ipiv_all,
-                             int64_t c0, int64_t c1) {
+                             int64_t c0, int64_t c1, bool skip_panel) {
   __shared__ int32_t pv[NB_MAX];
   const int b = blockIdx.y;
   const int32_t* ipiv = ipiv_all + (int64_t)b * n;
@@ -367,7 +367,7 @@ __global__ void laswp_kernel(Batched C, int64_t n, int64_t k, int w, const int32
   const int64_t cc = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (cc >= c1) return;
   // columns [c0, c1) excluding the panel [k, k+w)
-  const int64_t col = cc < k ? cc : cc + w;
+  const int64_t col = (!skip_panel || cc < k) ? cc : cc + w;
   if (col >= n) return;
   double2* Cc = C.p + (int64_t)b * C.stride + col * C.ld;
   for (int i = 0; i < w; ++i) {
@@ -381,81 +381,100 @@ __global__ void laswp_kernel(Batched C, int64_t n, int64_t k, int w, const int32
 }
 
 void laswp_launch(Batched C, int64_t n, int64_t k, int w, const int32_t* ipiv, int64_t c0, int64_t c1,
-                  int batch, cudaStream_t s) {
+                  int batch, cudaStream_t s, bool skip_panel) {
   ProfScope ps_(K_LASWP, 0.0, (double)batch * (c1 - c0) * w * 64.0, s);
   // here [c0, c1) indexes the n - w columns outside the panel
   if (c1 <= c0) return;
   const int threads = 128;
   dim3 grid((unsigned)((c1 - c0 + threads - 1) / threads), (unsigned)batch);
-  laswp_kernel<<<grid, threads, 0, s>>>(C, n, k, w, ipiv, c0, c1);
+  laswp_kernel<<<grid, threads, 0, s>>>(C, n, k, w, ipiv, c0, c1, skip_panel);
   count_launch();
 }
 
 // ============================================================================ trsm
-// op(T) X = X for an nb x nb (nb <= 64) diagonal block, 32 right-hand sides per CTA.
-// Used for U12 = L11^-1 A12 in the LU, and for the diagonal blocks of the blocked
-// substitutions (L, U; and U^H, L^H for the conjugate-transposed left solves).
+// op(T) X = X for an nb x nb (nb <= 64) diagonal block; one thread per right-hand side column,
+// the column held in registers in two 32-row halves (no barriers, no shared memory):
+//   forward (op(T) lower): solve rows 0..31, update rows 32..63 with them, solve rows 32..63;
+//   backward (op(T) upper): mirror image.
+// T entries are read through the read-only path (all threads of a warp read the same
+// address: broadcast).  Used for U12 = L11^-1 A12 in the LU and for the diagonal blocks of
+// the blocked substitutions (L, U; U^H, L^H for the conjugate-transposed left solves).
 namespace {
-constexpr int TR_NB = 64, TR_TN = 32, TR_T = 256, TR_LD = TR_NB + 1;
-constexpr size_t TR_SMEM = (size_t)(TR_NB * TR_LD + TR_TN * TR_LD) * sizeof(double2);
+constexpr int TR_T = 128, TR_H = 32;
 
+template <bool CONJT>
+__device__ __forceinline__ double2 tget(const double2* __restrict__ T, int64_t ld, int r, int i) {
+  // op(T)[r][i]
+  if (!CONJT) return __ldg(T + r + (int64_t)i * ld);
+  const double2 v = __ldg(T + i + (int64_t)r * ld);
+  return make_double2(v.x, -v.y);
+}
+
+// solve the h x h triangular block at rows/cols [o, o+h) of op(T), in place on x
 template <bool LOWER, bool UNIT, bool CONJT>
-__global__ void __launch_bounds__(TR_T) trsm_kernel(Batched T, Batched X, int nb, int64_t ncols) {
-  extern __shared__ __align__(16) double2 sm[];
-  double2* Ts = sm;                 // Ts[r * TR_LD + i] = op(T)[r][i]
-  double2* Xs = sm + TR_NB * TR_LD; // Xs[c * TR_LD + r]
-  const int b = blockIdx.y;
-  const double2* Tb = T.p + (int64_t)b * T.stride;
-  double2* Xb = X.p + (int64_t)b * X.stride;
-  const int64_t col0 = (int64_t)blockIdx.x * TR_TN;
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < nb * nb; idx += TR_T) {
-    const int r = idx % nb, i = idx / nb;
-    double2 v;
-    if (!CONJT) v = Tb[r + (int64_t)i * T.ld];
-    else v = cconj(Tb[i + (int64_t)r * T.ld]);
-    Ts[r * TR_LD + i] = v;
-  }
-  for (int idx = tid; idx < nb * TR_TN; idx += TR_T) {
-    const int r = idx % nb, c = idx / nb;
-    Xs[c * TR_LD + r] = (col0 + c < ncols) ? Xb[r + (col0 + c) * X.ld] : make_double2(0.0, 0.0);
-  }
-  __syncthreads();
-  const int c = tid & 31, rg = tid >> 5;
-  double2* xc = Xs + c * TR_LD;
+__device__ __forceinline__ void tri_solve(const double2* __restrict__ T, int64_t ld, int o, int h, double2 (&x)[TR_H]) {
   if (LOWER) {
-    for (int i = 0; i < nb; ++i) {
-      if (rg == (i & 7) && !UNIT) xc[i] = cdiv(xc[i], Ts[i * TR_LD + i]);
-      __syncthreads();
-      const double2 x = xc[i];
-      for (int r = rg; r < nb; r += 8)
-        if (r > i) xc[r] = cfms(xc[r], Ts[r * TR_LD + i], x);
+#pragma unroll
+    for (int i = 0; i < TR_H; ++i) {
+      if (i < h) {
+        if (!UNIT) x[i] = cdiv(x[i], tget<CONJT>(T, ld, o + i, o + i));
+#pragma unroll
+        for (int r = i + 1; r < TR_H; ++r)
+          if (r < h) x[r] = cfms(x[r], tget<CONJT>(T, ld, o + r, o + i), x[i]);
+      }
     }
   } else {
-    for (int i = nb - 1; i >= 0; --i) {
-      if (rg == (i & 7) && !UNIT) xc[i] = cdiv(xc[i], Ts[i * TR_LD + i]);
-      __syncthreads();
-      const double2 x = xc[i];
-      for (int r = rg; r < nb; r += 8)
-        if (r < i) xc[r] = cfms(xc[r], Ts[r * TR_LD + i], x);
+#pragma unroll
+    for (int i = TR_H - 1; i >= 0; --i) {
+      if (i < h) {
+        if (!UNIT) x[i] = cdiv(x[i], tget<CONJT>(T, ld, o + i, o + i));
+#pragma unroll
+        for (int r = 0; r < i; ++r) x[r] = cfms(x[r], tget<CONJT>(T, ld, o + r, o + i), x[i]);
+      }
     }
   }
-  __syncthreads();
-  for (int idx = tid; idx < nb * TR_TN; idx += TR_T) {
-    const int r = idx % nb, cc = idx / nb;
-    if (col0 + cc < ncols) Xb[r + (col0 + cc) * X.ld] = Xs[cc * TR_LD + r];
+}
+
+template <bool LOWER, bool UNIT, bool CONJT>
+__global__ void __launch_bounds__(TR_T) trsm_kernel(Batched Tb, Batched Xb, int nb, int64_t ncols) {
+  const int b = blockIdx.y;
+  const double2* __restrict__ T = Tb.p + (int64_t)b * Tb.stride;
+  const int64_t c = (int64_t)blockIdx.x * TR_T + threadIdx.x;
+  if (c >= ncols) return;
+  double2* __restrict__ X = Xb.p + (int64_t)b * Xb.stride + c * Xb.ld;
+  const int64_t ld = Tb.ld;
+  const int h0 = min(nb, TR_H), h1 = nb - h0;
+  double2 x[TR_H];
+  // first half to solve: rows [0,h0) for forward, rows [h0,nb) for backward
+  const int oa = LOWER ? 0 : h0, ha = LOWER ? h0 : h1;
+  const int ob = LOWER ? h0 : 0, hb = LOWER ? h1 : h0;
+  if (ha > 0) {
+#pragma unroll
+    for (int r = 0; r < TR_H; ++r) if (r < ha) x[r] = X[oa + r];
+    tri_solve<LOWER, UNIT, CONJT>(T, ld, oa, ha, x);
+#pragma unroll
+    for (int r = 0; r < TR_H; ++r) if (r < ha) X[oa + r] = x[r];
+  }
+  if (hb > 0) {
+    // second half: x <- rows [ob, ob+hb) - op(T)[ob.., oa..] * (first-half solution, re-read)
+#pragma unroll
+    for (int r = 0; r < TR_H; ++r) if (r < hb) x[r] = X[ob + r];
+    for (int t = 0; t < ha; ++t) {
+      const double2 xt = X[oa + t];
+#pragma unroll
+      for (int r = 0; r < TR_H; ++r)
+        if (r < hb) x[r] = cfms(x[r], tget<CONJT>(T, ld, ob + r, oa + t), xt);
+    }
+    tri_solve<LOWER, UNIT, CONJT>(T, ld, ob, hb, x);
+#pragma unroll
+    for (int r = 0; r < TR_H; ++r) if (r < hb) X[ob + r] = x[r];
   }
 }
 
 template <bool LOWER, bool UNIT, bool CONJT>
 void trsm_t(Batched T, Batched X, int nb, int64_t ncols, int batch, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(trsm_kernel<LOWER, UNIT, CONJT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TR_SMEM);
-    configured = true;
-  }
-  dim3 grid((unsigned)((ncols + TR_TN - 1) / TR_TN), (unsigned)batch);
-  trsm_kernel<LOWER, UNIT, CONJT><<<grid, TR_T, TR_SMEM, s>>>(T, X, nb, ncols);
+  dim3 grid((unsigned)((ncols + TR_T - 1) / TR_T), (unsigned)batch);
+  trsm_kernel<LOWER, UNIT, CONJT><<<grid, TR_T, 0, s>>>(T, X, nb, ncols);
   count_launch();
 }
 }  // namespace

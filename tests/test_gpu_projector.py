@@ -130,3 +130,16 @@ def test_reduce_parity():
     Q = host(Qd)
     assert rel(host(Ah), oracle.gemm(Q, oracle.gemm(P.A, Q), opa=2)) <= 1e-12
     assert rel(host(Bh), oracle.gemm(Q, oracle.gemm(P.B, Q), opa=2)) <= 1e-12
+
+
+@pytest.mark.parametrize("key,n,m0", [("C2", 300, 40), ("C4", 200, 24)])
+def test_register_panel_variant(monkeypatch, key, n, m0):
+    """The register-chunk panel kernel (used when the panel does not fit the cluster's shared
+    memory, n > 4096) forced on small sizes: same parity bar."""
+    monkeypatch.setenv("FEAST_PANEL", "reg")
+    P = synth.make_pencil(key, n=n, m0=m0)
+    z, w = _oracle_nodes(P)
+    f = _handle(P, mode=fb.BI)
+    Q, QL = f.project_bi(dev(P.A), dev(P.B), dev(P.X0), dev(P.X0))
+    assert rel(host(Q), oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
+    assert rel(host(QL), oracle.project(P.A, P.B, P.X0, z, w, left=True)) <= TOL

@@ -19,3 +19,11 @@ for it in range(3):
     n, m, q = P.n, P.m0, P.q
     fl = q * (8 / 3 * n ** 3 + 8 * n * n * m)
     print(f"{key} project {ms:.2f} ms  LU+solve {fl / ms / 1e9:.2f} TF/s  launches {f.last_launch_count}", flush=True)
+f.profile(True)
+f.project(A, B, X, Q)
+torch.cuda.synchronize()
+for k, v in f.profile_summary().items():
+    if v["launches"]:
+        extra = f"{v['flops'] / (v['ms'] * 1e-3) / 1e12:6.2f} TF/s" if v["flops"] else ""
+        print(f"  {k:6s} n={v['launches']:4d} {v['ms']:8.3f} ms  {1e3 * v['ms'] / v['launches']:8.1f} us/launch {extra}")
+f.profile(False)
