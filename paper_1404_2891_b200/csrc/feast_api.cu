@@ -35,6 +35,9 @@ struct feast_ctx {
   int nb = 64;
   feast::PanelCfg pcfg{};
   int smem_cs = 0;   // cluster size of the shared-memory panel kernel (0: register-chunk kernel)
+  bool lookahead = true;
+  cudaStream_t side = nullptr;        // high-priority stream for the lookahead panel
+  cudaEvent_t ev_a = nullptr, ev_p = nullptr;
   int64_t ldc = 0;
   // workspace
   void* ws = nullptr;
@@ -219,31 +222,53 @@ void gemm_gen(feast_ctx* h, int64_t M, int64_t N, int64_t K, bool conjA, const d
 }
 
 // ---------------------------------------------------------------- blocked LU (batched)
+void panel_at(feast_ctx* h, int64_t k, int w, int nbat, cudaStream_t s) {
+  const int64_t n = h->n, ld = h->ldc, st = ld * n;
+  if (h->smem_cs)
+    feast::panel_smem_launch(bat(h->Cw, ld, st), n, k, w, h->ipiv, h->stats_cur, h->info_cur, nbat, h->smem_cs, s);
+  else
+    feast::panel_launch(bat(h->Cw, ld, st), n, k, w, h->ipiv, h->stats_cur, h->info_cur, nbat, h->pcfg, s);
+}
+
+// Right-looking blocked LU of the batch with one-step LOOKAHEAD: at step k the trailing update
+// first refreshes the next panel's columns, then the next panel is factored on a high-priority
+// side stream while the rest of the trailing update runs on the main stream (disjoint
+// columns).  The serial, latency-bound panel thus hides behind the DMMA trailing GEMM.
 void lu_batched(feast_ctx* h, int nbat) {
   const int64_t n = h->n, ld = h->ldc, st = ld * n;
   double2* C = h->Cw;
+  cudaStream_t sm = h->stream, sp = h->side;
+  panel_at(h, 0, (int)std::min<int64_t>(h->nb, n), nbat, sm);
   for (int64_t k = 0; k < n; k += h->nb) {
     const int w = (int)std::min<int64_t>(h->nb, n - k);
-    if (h->smem_cs) {
-      feast::panel_smem_launch(bat(C, ld, st), n, k, w, h->ipiv, h->stats_cur, h->info_cur, nbat, h->smem_cs,
-                               h->stream);
-      feast::laswp_launch(bat(C, ld, st), n, k, w, h->ipiv, 0, n, nbat, h->stream, false);
-    } else {
-      feast::panel_launch(bat(C, ld, st), n, k, w, h->ipiv, h->stats_cur, h->info_cur, nbat, h->pcfg, h->stream);
-      if (n - w > 0) feast::laswp_launch(bat(C, ld, st), n, k, w, h->ipiv, 0, n - w, nbat, h->stream);
-    }
+    if (h->smem_cs) feast::laswp_launch(bat(C, ld, st), n, k, w, h->ipiv, 0, n, nbat, sm, false);
+    else if (n - w > 0) feast::laswp_launch(bat(C, ld, st), n, k, w, h->ipiv, 0, n - w, nbat, sm);
     // L_kk^-1 and U_kk^-1 (the latter for the substitutions)
-    feast::trtri_launch(bat(C, ld, st), n, k / 64, 1, h->Inv, h->inv_stride, 2, nbat, h->stream);
-    const int64_t rest = n - k - w;
-    if (rest > 0) {
-      // U12 = L11^-1 A12  (in-place DMMA GEMM, M = w <= 64)
-      ZgemmArgs u{w, rest, w, inv_ptr(h, k / 64, 0), 64, h->inv_stride, C + k + (k + w) * ld, ld, st,
-                  C + k + (k + w) * ld, ld, st, make_double2(1, 0), make_double2(0, 0), nbat};
-      feast::zgemm_launch(u, false, feast::ZG_GEN, h->stream);
-      // A22 -= L21 U12
-      ZgemmArgs p{rest, rest, w, C + (k + w) + k * ld, ld, st, C + k + (k + w) * ld, ld, st,
-                  C + (k + w) + (k + w) * ld, ld, st, make_double2(-1, 0), make_double2(1, 0), nbat};
-      feast::zgemm_launch(p, false, feast::ZG_SUB, h->stream);
+    feast::trtri_launch(bat(C, ld, st), n, k / 64, 1, h->Inv, h->inv_stride, 2, nbat, sm);
+    const int64_t k1 = k + w, rest = n - k1;
+    if (rest <= 0) break;
+    const int w1 = (int)std::min<int64_t>(h->nb, rest);
+    // columns [c0, c0 + nc): U12 = L11^-1 A12 (in-place DMMA GEMM, M = w), then A22 -= L21 U12
+    auto update = [&](int64_t c0, int64_t nc) {
+      if (nc <= 0) return;
+      ZgemmArgs u{w, nc, w, inv_ptr(h, k / 64, 0), 64, h->inv_stride, C + k + c0 * ld, ld, st, C + k + c0 * ld, ld, st,
+                  make_double2(1, 0), make_double2(0, 0), nbat};
+      feast::zgemm_launch(u, false, feast::ZG_GEN, sm);
+      ZgemmArgs p{rest, nc, w, C + k1 + k * ld, ld, st, C + k + c0 * ld, ld, st, C + k1 + c0 * ld, ld, st,
+                  make_double2(-1, 0), make_double2(1, 0), nbat};
+      feast::zgemm_launch(p, false, feast::ZG_SUB, sm);
+    };
+    update(k1, w1);                                   // next panel's columns first
+    if (h->lookahead) {
+      cudaEventRecord(h->ev_a, sm);
+      cudaStreamWaitEvent(sp, h->ev_a, 0);
+      panel_at(h, k1, w1, nbat, sp);                  // overlaps the rest of the update
+      cudaEventRecord(h->ev_p, sp);
+      update(k1 + w1, rest - w1);
+      cudaStreamWaitEvent(sm, h->ev_p, 0);
+    } else {
+      update(k1 + w1, rest - w1);
+      panel_at(h, k1, w1, nbat, sm);
     }
   }
 }
@@ -479,6 +504,17 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
     if (feast::panel_smem_fits(n, 64, cs)) { h->smem_cs = cs; break; }
   if (const char* e = getenv("FEAST_PANEL")) {   // debugging override: "reg" = register-chunk kernel
     if (e[0] == 'r') { h->smem_cs = 0; h->nb = 64; }
+  }
+  if (const char* e = getenv("FEAST_LOOKAHEAD")) h->lookahead = e[0] != '0';
+  {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_p, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      h->lookahead = false;   // no CUDA context (CPU-only validation): launches never happen
+    }
   }
   h->ldc = (n + 7) / 8 * 8;
   *out = h;
@@ -749,6 +785,9 @@ const char* feast_last_error(feast_handle h) { return h ? h->err.c_str() : "null
 
 void feast_destroy(feast_handle h) {
   if (!h) return;
+  if (h->ev_a) cudaEventDestroy(h->ev_a);
+  if (h->ev_p) cudaEventDestroy(h->ev_p);
+  if (h->side) cudaStreamDestroy(h->side);
   if (h->itmem) cudaFree(h->itmem);
   if (h->solp) cusolverDnDestroyParams(h->solp);
   if (h->sol) cusolverDnDestroy(h->sol);

@@ -10,13 +10,15 @@
 // from the pivot sequence; the row-swap kernel then applies ipiv to ALL n columns (panel
 // included), which yields exactly the LAPACK getrf layout.
 //
-// Per column: warp-shuffle argmax -> CTA argmax -> the candidate's owner pushes its chunk row
-// (W complex) + |pivot| + row id into every CTA's slot (DSMEM) -> ONE cluster barrier ->
-// identical global decision everywhere -> in-register rank-1 update of the W-column chunk.
-// Per chunk of W columns: the chunk's W pivot rows push their remaining-panel values to every
-// CTA, one more barrier, every CTA forms U12 = L11^-1 (pivot rows) and applies the rank-W
-// update to its own non-pivot rows in shared memory (one smem read-modify-write per element
-// per chunk, not per column).
+// Per column: warp-shuffle argmax -> CTA argmax -> the CTA candidate (chunk row of W complex,
+// |pivot|, row id) is pushed into every CTA's slot with st.async, whose bytes complete a
+// transaction mbarrier in the receiving CTA -> each CTA waits on its OWN mbarrier (no
+// cluster-wide barrier, no memory fence) -> identical global decision everywhere -> in-register
+// rank-1 update of the W-column chunk.  Slots are double-buffered by column parity: a CTA can
+// only push column c+2 after every CTA pushed column c+1, i.e. after every CTA consumed c.
+// Per chunk of W columns: the chunk's W pivot rows push their remaining-panel values the same
+// way, every CTA forms U12 = L11^-1 (pivot rows) and applies the rank-W update to its own
+// non-pivot rows in shared memory (one smem read-modify-write per element per chunk).
 #include <cooperative_groups.h>
 #include <float.h>
 #include <limits.h>
@@ -34,17 +36,49 @@ constexpr int PT = 128;          // threads per CTA (one panel row each, S rows)
 constexpr int CSM = 16;          // max cluster size
 constexpr int WC = 8;            // chunk width (columns held in registers)
 constexpr int WMAX = 64;         // max panel width
+constexpr int SLOT_BYTES = (WC + 2) * 16;
 
 struct __align__(16) Slot {
   double2 row[WC];
   double val;
-  int idx;
-  int pad;
+  long long idx;
+  double2 pinv;      // 1 / pivot, computed by the candidate's owner before the exchange
 };
 
 __device__ __forceinline__ bool better(double v, int i, double bv, int bi) {
   return v > bv || (v == bv && i < bi);
 }
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async16(uint32_t raddr, double2 v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];"
+               ::"r"(raddr), "l"(__double_as_longlong(v.x)), "l"(__double_as_longlong(v.y)), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arm(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+  }
+}
+
+#ifdef FEAST_PANEL_TRACE
+__device__ unsigned long long g_ptrace[512];
+#define PTRACE(i) do { if (blockIdx.x == 0 && threadIdx.x == 0 && k == 0) { unsigned long long t_; \
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_ptrace[(i)] = t_; } } while (0)
+#else
+#define PTRACE(i) do {} while (0)
+#endif
 
 template <int S>
 __global__ void __launch_bounds__(PT, 1)
@@ -61,21 +95,44 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
   const int Lc = (L + CS - 1) / CS;
   const int rbeg = crank * Lc;
   const int nrow = max(0, min(L, rbeg + Lc) - rbeg);
-  const int PLD = w + 1;   // smem row stride (complex) -> conflict-free column access
+  const int PLD = Lc;   // column-major smem panel: P[c * PLD + r] (consecutive rows -> conflict-free)
 
-  extern __shared__ __align__(16) double2 P[];  // [Lc][PLD]
+  extern __shared__ __align__(128) double2 P[];  // [w][PLD]
   __shared__ Slot slots[2][CSM];
   __shared__ double2 L11s[WC][WC];               // chunk pivot rows' chunk values
-  __shared__ double2 U12s[WC][WMAX];             // chunk pivot rows' rest-of-panel values
+  __shared__ __align__(16) double2 U12s[WC][WMAX];   // chunk pivot rows' rest-of-panel values
   __shared__ int pvt[WMAX];                      // pivot (panel row index) per column
   __shared__ double wv[PT / 32];
   __shared__ int wi[PT / 32];
-  __shared__ double2 cand[WC];
+  __shared__ double2 wrow[PT / 32][WC + 1];
+  __shared__ __align__(8) unsigned long long mbar[4];   // slots[0], slots[1], U12s, load
+  __shared__ int pos2row[WMAX], cur[WMAX];
 
-  // ---- load own rows of the panel (coalesced: consecutive threads = consecutive rows)
-  for (int c = 0; c < w; ++c)
-    for (int r = tid; r < nrow; r += PT) P[r * PLD + c] = C[(rbeg + r) + c * ld];
+  PTRACE(0);
+  if (tid == 0) {
+    mbar_init(saddr(&mbar[0]), 1);
+    mbar_init(saddr(&mbar[1]), 1);
+    mbar_init(saddr(&mbar[2]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // ---- load own rows of the panel: one bulk (TMA) copy per column segment into the
+  // column-major shared layout P[c][r], completing a local transaction mbarrier
+  const uint32_t lbar = saddr(&mbar[3]);
+  if (tid == 0) {
+    mbar_init(lbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
+  if (nrow > 0) {
+    if (tid == 0) mbar_arm(lbar, (uint32_t)(w * nrow * 16));
+    for (int c = tid; c < w; c += PT) {
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(saddr(P + c * PLD)), "l"(C + rbeg + c * ld), "r"(nrow * 16), "r"(lbar) : "memory");
+    }
+  }
+  cluster.sync();   // mbarrier inits visible cluster-wide before any remote st.async
+  if (nrow > 0) mbar_wait(lbar, 0);
+  PTRACE(1);
 
   bool used[S];
 #pragma unroll
@@ -83,77 +140,99 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
   double2 a[S][WC];
   double pmin = DBL_MAX, pmax = 0.0;
   int info = 0;
+  int chunk = 0;
 
-  for (int j0 = 0; j0 < w; j0 += WC) {
+  for (int j0 = 0; j0 < w; j0 += WC, ++chunk) {
     const int wc = min(WC, w - j0);
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int r = tid + s * PT;
 #pragma unroll
       for (int jj = 0; jj < WC; ++jj)
-        a[s][jj] = (r < nrow && jj < wc) ? P[r * PLD + j0 + jj] : make_double2(0.0, 0.0);
+        a[s][jj] = (r < nrow && jj < wc) ? P[(j0 + jj) * PLD + r] : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int jj = 0; jj < WC; ++jj) {
       if (jj >= wc) break;
       const int col = j0 + jj;
       const int buf = col & 1;
+      const uint32_t bar = saddr(&mbar[buf]);
+      PTRACE(8 + 4 * col);
+      if (tid == 0) mbar_arm(bar, (uint32_t)(CS * SLOT_BYTES));
       double bv = -1.0;
-      int bi = INT_MAX;
+      int bi = INT_MAX, bs = -1;
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const int r = tid + s * PT;
         if (r < nrow && !used[s]) {
           const double v = cabs1(a[s][jj]);
-          if (better(v, rbeg + r, bv, bi)) { bv = v; bi = rbeg + r; }
+          if (better(v, rbeg + r, bv, bi)) { bv = v; bi = rbeg + r; bs = s; }
         }
       }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-        if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
-      }
-      if (lane == 0) { wv[warp] = bv; wi[warp] = bi; }
-      __syncthreads();
-      double cv = wv[0];
-      int ci = wi[0];
-#pragma unroll
-      for (int q = 1; q < PT / 32; ++q)
-        if (better(wv[q], wi[q], cv, ci)) { cv = wv[q]; ci = wi[q]; }
-      // the owner stages its chunk row locally, then CS*(WC+1) threads push it in parallel
+      // every thread inverts its own candidate now, overlapping the division with the shuffles
+      double2 myrcp = make_double2(0.0, 0.0);
 #pragma unroll
       for (int s = 0; s < S; ++s)
-        if (cv >= 0.0 && rbeg + tid + s * PT == ci) {
+        if (s == bs) {
+          const double2 pv = a[s][jj];
+          if (pv.x != 0.0 || pv.y != 0.0) myrcp = crcp(pv);
+        }
+      double wbv = bv;
+      int wbi = bi;
 #pragma unroll
-          for (int q = 0; q < WC; ++q) cand[q] = a[s][q];
-        }
-      __syncthreads();
-      for (int t = tid; t < CS * (WC + 1); t += PT) {
-        const int dcta = t / (WC + 1), e = t % (WC + 1);
-        Slot* d = cluster.map_shared_rank(&slots[buf][crank], dcta);
-        if (e < WC) {
-          if (cv >= 0.0) d->row[e] = cand[e];
-        } else {
-          d->val = cv;
-          d->idx = cv >= 0.0 ? ci : INT_MAX;
-        }
+      for (int off = 16; off > 0; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, wbv, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, wbi, off);
+        if (better(ov, oi, wbv, wbi)) { wbv = ov; wbi = oi; }
       }
-      cluster.sync();
-      int gb = 0;
-      double gv = slots[buf][0].val;
-      int gi = slots[buf][0].idx;
-      for (int c = 1; c < CS; ++c) {
-        const double v = slots[buf][c].val;
-        const int i = slots[buf][c].idx;
-        if (better(v, i, gv, gi)) { gv = v; gi = i; gb = c; }
+      // the warp's winning lane stages its chunk row and 1/pivot; one barrier for the CTA step
+      if (wbv >= 0.0 && bi == wbi) {
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+          if (s == bs) {
+#pragma unroll
+            for (int q = 0; q < WC; ++q) wrow[warp][q] = a[s][q];
+            wrow[warp][WC] = myrcp;
+          }
+      }
+      if (lane == 0) { wv[warp] = wbv; wi[warp] = wbi; }
+      __syncthreads();
+      double cv = wv[0];
+      int ci = wi[0], cw = 0;
+#pragma unroll
+      for (int q = 1; q < PT / 32; ++q)
+        if (better(wv[q], wi[q], cv, ci)) { cv = wv[q]; ci = wi[q]; cw = q; }
+      // push {row[WC], (val, idx)} into slot [buf][crank] of every CTA (st.async -> its mbarrier)
+      for (int t = tid; t < CS * (WC + 2); t += PT) {
+        const int dcta = t / (WC + 2), e = t % (WC + 2);
+        const uint32_t rslot = mapa(saddr(&slots[buf][crank]), dcta);
+        const uint32_t rbar = mapa(bar, dcta);
+        double2 v;
+        if (e < WC) v = cv >= 0.0 ? wrow[cw][e] : make_double2(0.0, 0.0);
+        else if (e == WC) v = make_double2(cv, __longlong_as_double((long long)(cv >= 0.0 ? ci : INT_MAX)));
+        else v = cv >= 0.0 ? wrow[cw][WC] : make_double2(0.0, 0.0);
+        st_async16(rslot + e * 16, v, rbar);
+      }
+      PTRACE(9 + 4 * col);
+      mbar_wait(bar, (uint32_t)((col >> 1) & 1));
+      PTRACE(10 + 4 * col);
+      // global pivot: lanes scan the CS slots, warp-shuffle argmax (every warp, same result)
+      double gv = -2.0;
+      int gi = INT_MAX, gb = 0;
+      if (lane < CS) { gv = slots[buf][lane].val; gi = (int)slots[buf][lane].idx; gb = lane; }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, gv, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, gi, off);
+        const int ob = __shfl_xor_sync(0xffffffffu, gb, off);
+        if (better(ov, oi, gv, gi)) { gv = ov; gi = oi; gb = ob; }
       }
       const double2* prow = slots[buf][gb].row;
       if (tid < WC) L11s[jj][tid] = prow[tid];
       if (tid == 0) pvt[col] = gi;
       const double2 p = prow[jj];
       const bool pzero = (p.x == 0.0 && p.y == 0.0);
-      const double2 pinv = pzero ? make_double2(0.0, 0.0) : crcp(p);
+      const double2 pinv = slots[buf][gb].pinv;
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const int r = tid + s * PT;
@@ -182,12 +261,14 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
       if (r < nrow) {
 #pragma unroll
         for (int jj = 0; jj < WC; ++jj)
-          if (jj < wc) P[r * PLD + j0 + jj] = a[s][jj];
+          if (jj < wc) P[(j0 + jj) * PLD + r] = a[s][jj];
       }
     }
     const int c1 = j0 + wc;
     if (c1 < w) {
       const int rem = w - c1;
+      const uint32_t ubar = saddr(&mbar[2]);
+      if (tid == 0) mbar_arm(ubar, (uint32_t)(wc * rem * 16));
       __syncthreads();
       // owners push the chunk pivot rows' rest-of-panel values to every CTA
       for (int jj = 0; jj < wc; ++jj) {
@@ -195,12 +276,13 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
         if (pr >= 0 && pr < nrow) {
           for (int idx = tid; idx < rem * CS; idx += PT) {
             const int c = idx % rem, dcta = idx / rem;
-            double2* d = cluster.map_shared_rank(&U12s[jj][c], dcta);
-            *d = P[pr * PLD + c1 + c];
+            st_async16(mapa(saddr(&U12s[jj][c]), dcta), P[(c1 + c) * PLD + pr], mapa(ubar, dcta));
           }
         }
       }
-      cluster.sync();
+      PTRACE(300 + 4 * chunk);
+      mbar_wait(ubar, (uint32_t)(chunk & 1));
+      PTRACE(301 + 4 * chunk);
       // U12 = L11^-1 (pivot rows), unit lower L11 (chunk multipliers of the pivot rows)
       for (int c = tid; c < rem; c += PT) {
         double2 u[WC];
@@ -215,38 +297,58 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
           }
         }
       }
+      PTRACE(303 + 4 * chunk);
       __syncthreads();
       // pivot rows of this chunk take their U12 values; other rows get the rank-wc update
       for (int jj = 0; jj < wc; ++jj) {
         const int pr = pvt[j0 + jj] - rbeg;
         if (pr >= 0 && pr < nrow)
-          for (int c = tid; c < rem; c += PT) P[pr * PLD + c1 + c] = U12s[jj][c];
+          for (int c = tid; c < rem; c += PT) P[(c1 + c) * PLD + pr] = U12s[jj][c];
       }
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const int r = tid + s * PT;
         if (r < nrow && !used[s]) {
-          double2* row = P + r * PLD + c1;
-          for (int c = 0; c < rem; ++c) {
-            double2 v = row[c];
+          double2* colp = P + c1 * PLD + r;
+          int c = 0;
+          for (; c + 4 <= rem; c += 4) {
+            double2 v0 = colp[(c + 0) * PLD], v1 = colp[(c + 1) * PLD], v2 = colp[(c + 2) * PLD], v3 = colp[(c + 3) * PLD];
+#pragma unroll
+            for (int jj = 0; jj < WC; ++jj)
+              if (jj < wc) {
+                v0 = cfms(v0, a[s][jj], U12s[jj][c + 0]);
+                v1 = cfms(v1, a[s][jj], U12s[jj][c + 1]);
+                v2 = cfms(v2, a[s][jj], U12s[jj][c + 2]);
+                v3 = cfms(v3, a[s][jj], U12s[jj][c + 3]);
+              }
+            colp[(c + 0) * PLD] = v0; colp[(c + 1) * PLD] = v1; colp[(c + 2) * PLD] = v2; colp[(c + 3) * PLD] = v3;
+          }
+          for (; c < rem; ++c) {
+            double2 v = colp[c * PLD];
 #pragma unroll
             for (int jj = 0; jj < WC; ++jj)
               if (jj < wc) v = cfms(v, a[s][jj], U12s[jj][c]);
-            row[c] = v;
+            colp[c * PLD] = v;
           }
         }
       }
-      // the next chunk's slots/U12s writes by other CTAs happen after the next cluster barrier
-      cluster.sync();
+      __syncthreads();
+      PTRACE(302 + 4 * chunk);
+      if (chunk == 0) PTRACE(400);
     }
   }
+  PTRACE(2);
+  // ---- store own rows back (physical order): bulk (TMA) shared -> global per column
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
-  // ---- store own rows back (physical order)
-  for (int c = 0; c < w; ++c)
-    for (int r = tid; r < nrow; r += PT) C[(rbeg + r) + c * ld] = P[r * PLD + c];
+  if (nrow > 0) {
+    for (int c = tid; c < w; c += PT)
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                   ::"l"(C + rbeg + c * ld), "r"(saddr(P + c * PLD)), "r"(nrow * 16) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
   // ---- LAPACK ipiv from the pivot sequence (rows / positions relative to k)
   if (crank == 0 && tid == 0) {
-    int pos2row[WMAX], cur[WMAX];
     for (int i = 0; i < w; ++i) { pos2row[i] = i; cur[i] = i; }
     int32_t* ipiv = ipiv_all + (int64_t)b * n + k;
     for (int col = 0; col < w; ++col) {
@@ -263,8 +365,10 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
     stats_all[2 * b + 1] = fmax(stats_all[2 * b + 1], pmax);
     if (info && !info_all[b]) info_all[b] = info;
   }
-  // keep every CTA's shared memory alive until remote writes into it are complete
-  cluster.sync();
+  if (nrow > 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  PTRACE(3);
+  // No trailing cluster barrier: every remote write into this CTA's shared memory was a
+  // st.async that this CTA waited for (the last column's slots), so it may exit.
 }
 
 template <int S>
@@ -272,7 +376,7 @@ void launch_s(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* sta
               cudaStream_t s) {
   const int64_t L = n - k;
   const int Lc = (int)((L + cs - 1) / cs);
-  const size_t smem = (size_t)Lc * (w + 1) * sizeof(double2);
+  const size_t smem = (size_t)Lc * w * sizeof(double2);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(panel_smem_kernel<S>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -297,9 +401,13 @@ void launch_s(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* sta
 
 }  // namespace
 
+#ifdef FEAST_PANEL_TRACE
+void panel_trace_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_ptrace, sizeof(g_ptrace)); }
+#endif
+
 bool panel_smem_fits(int64_t n, int w, int cs) {
   const int64_t Lc = (n + cs - 1) / cs;
-  return w <= WMAX && (size_t)Lc * (w + 1) * sizeof(double2) <= 190 * 1024 && Lc <= 2 * PT;
+  return w <= WMAX && (size_t)Lc * w * sizeof(double2) <= 190 * 1024 && Lc <= 2 * PT;
 }
 
 void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info, int batch,
