@@ -36,6 +36,8 @@ struct feast_ctx {
   feast::PanelCfg pcfg{};
   int smem_cs = 0;   // cluster size of the shared-memory panel kernel (0: register-chunk kernel)
   bool lookahead = true;
+  int64_t nbo = 256;                  // outer block (trailing-update K); multiple of 64
+  int64_t wp = 32;                    // cluster-panel width (divides 64)
   cudaStream_t side = nullptr;        // high-priority stream for the lookahead panel
   cudaEvent_t ev_a = nullptr, ev_p = nullptr;
   int64_t ldc = 0;
@@ -223,82 +225,135 @@ void gemm_gen(feast_ctx* h, int64_t M, int64_t N, int64_t K, bool conjA, const d
 
 // ---------------------------------------------------------------- blocked LU (batched)
 void panel_at(feast_ctx* h, int64_t k, int w, int nbat, cudaStream_t s) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * n;
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0);
   if (h->smem_cs)
     feast::panel_smem_launch(bat(h->Cw, ld, st), n, k, w, h->ipiv, h->stats_cur, h->info_cur, nbat, h->smem_cs, s);
   else
     feast::panel_launch(bat(h->Cw, ld, st), n, k, w, h->ipiv, h->stats_cur, h->info_cur, nbat, h->pcfg, s);
 }
 
-// Right-looking blocked LU of the batch with one-step LOOKAHEAD: at step k the trailing update
-// first refreshes the next panel's columns, then the next panel is factored on a high-priority
-// side stream while the rest of the trailing update runs on the main stream (disjoint
-// columns).  The serial, latency-bound panel thus hides behind the DMMA trailing GEMM.
-void lu_batched(feast_ctx* h, int nbat) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * n;
+// Two-level right-looking blocked LU of the batch with one-step LOOKAHEAD.
+//   inner: 64-wide panels (cluster kernel) inside an outer block of NBO columns, each followed
+//          by its row swaps on the block's columns, the 64x64 diagonal inverses and the
+//          in-block U12 / update (K = 64);
+//   outer: the block's swaps on all other columns, U12 = L11^-1 A12 as a blocked in-place DMMA
+//          TRSM with the 64x64 inverses, then the trailing update A22 -= L21 U12 with K = NBO.
+// Lookahead: the outer update first refreshes the next block's columns, then the next block is
+// factored on a high-priority side stream while the rest of the outer update runs on the main
+// stream (disjoint columns; the next block's swaps reach the other columns afterwards).
+// aug > 0: columns [n, n + aug) hold R, so swaps, U12 and updates also perform the forward
+// substitution L^-1 P R.
+void factor_block(feast_ctx* h, int64_t K0, int64_t Wo, int nbat, cudaStream_t s) {
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0);
   double2* C = h->Cw;
-  cudaStream_t sm = h->stream, sp = h->side;
-  panel_at(h, 0, (int)std::min<int64_t>(h->nb, n), nbat, sm);
-  for (int64_t k = 0; k < n; k += h->nb) {
-    const int w = (int)std::min<int64_t>(h->nb, n - k);
-    if (h->smem_cs) feast::laswp_launch(bat(C, ld, st), n, k, w, h->ipiv, 0, n, nbat, sm, false);
-    else if (n - w > 0) feast::laswp_launch(bat(C, ld, st), n, k, w, h->ipiv, 0, n - w, nbat, sm);
-    // L_kk^-1 and U_kk^-1 (the latter for the substitutions)
-    feast::trtri_launch(bat(C, ld, st), n, k / 64, 1, h->Inv, h->inv_stride, 2, nbat, sm);
-    const int64_t k1 = k + w, rest = n - k1;
-    if (rest <= 0) break;
-    const int w1 = (int)std::min<int64_t>(h->nb, rest);
-    // columns [c0, c0 + nc): U12 = L11^-1 A12 (in-place DMMA GEMM, M = w), then A22 -= L21 U12
-    auto update = [&](int64_t c0, int64_t nc) {
-      if (nc <= 0) return;
-      ZgemmArgs u{w, nc, w, inv_ptr(h, k / 64, 0), 64, h->inv_stride, C + k + c0 * ld, ld, st, C + k + c0 * ld, ld, st,
-                  make_double2(1, 0), make_double2(0, 0), nbat};
-      feast::zgemm_launch(u, false, feast::ZG_GEN, sm);
-      ZgemmArgs p{rest, nc, w, C + k1 + k * ld, ld, st, C + k + c0 * ld, ld, st, C + k1 + c0 * ld, ld, st,
+  const int64_t wp = h->smem_cs ? h->wp : 64;
+  for (int64_t ki = K0; ki < K0 + Wo; ki += 64) {
+    const int wi = (int)std::min<int64_t>(64, K0 + Wo - ki);
+    // the 64-block is factored as narrow cluster panels of wp columns (small SM footprint), with
+    // the in-block U12 (register TRSM) and update (DMMA) between them
+    for (int64_t kp = ki; kp < ki + wi; kp += wp) {
+      const int wpp = (int)std::min<int64_t>(wp, ki + wi - kp);
+      panel_at(h, kp, wpp, nbat, s);
+      if (h->smem_cs) {
+        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, h->ipiv, K0, K0 + Wo, nbat, s);
+      } else {   // the register-chunk panel already swapped its own columns
+        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, h->ipiv, K0, kp, nbat, s);
+        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, h->ipiv, kp + wpp, K0 + Wo, nbat, s);
+      }
+      const int64_t cp = kp + wpp, remb = ki + wi - cp;
+      if (remb > 0) {
+        feast::trsm_launch(bat(C + kp + kp * ld, ld, st), bat(C + kp + cp * ld, ld, st), wpp, remb, true, true, false,
+                           nbat, s);
+        ZgemmArgs p{n - cp, remb, wpp, C + cp + kp * ld, ld, st, C + kp + cp * ld, ld, st, C + cp + cp * ld, ld, st,
+                    make_double2(-1, 0), make_double2(1, 0), nbat};
+        feast::zgemm_launch(p, false, feast::ZG_SUB, s);
+      }
+    }
+    feast::trtri_launch(bat(C, ld, st), n, ki / 64, 1, h->Inv, h->inv_stride, 2, nbat, s);
+    const int64_t c1 = ki + wi, rem = K0 + Wo - c1;
+    if (rem > 0) {
+      ZgemmArgs u{wi, rem, wi, inv_ptr(h, ki / 64, 0), 64, h->inv_stride, C + ki + c1 * ld, ld, st, C + ki + c1 * ld,
+                  ld, st, make_double2(1, 0), make_double2(0, 0), nbat};
+      feast::zgemm_launch(u, false, feast::ZG_GEN, s);
+      ZgemmArgs p{n - c1, rem, wi, C + c1 + ki * ld, ld, st, C + ki + c1 * ld, ld, st, C + c1 + c1 * ld, ld, st,
                   make_double2(-1, 0), make_double2(1, 0), nbat};
-      feast::zgemm_launch(p, false, feast::ZG_SUB, sm);
-    };
-    update(k1, w1);                                   // next panel's columns first
-    if (h->lookahead) {
-      cudaEventRecord(h->ev_a, sm);
-      cudaStreamWaitEvent(sp, h->ev_a, 0);
-      panel_at(h, k1, w1, nbat, sp);                  // overlaps the rest of the update
-      cudaEventRecord(h->ev_p, sp);
-      update(k1 + w1, rest - w1);
-      cudaStreamWaitEvent(sm, h->ev_p, 0);
-    } else {
-      update(k1 + w1, rest - w1);
-      panel_at(h, k1, w1, nbat, sm);
+      feast::zgemm_launch(p, false, feast::ZG_SUB, s);
     }
   }
 }
 
+// U12 = L11^-1 A12 and A22 -= L21 U12 for the columns [c0, c0 + nc) of outer block (K0, Wo).
+void outer_update(feast_ctx* h, int64_t K0, int64_t Wo, int64_t c0, int64_t nc, int nbat, cudaStream_t s) {
+  if (nc <= 0) return;
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0), K1 = K0 + Wo;
+  double2* C = h->Cw;
+  for (int64_t ki = K0; ki < K1; ki += 64) {
+    const int wi = (int)std::min<int64_t>(64, K1 - ki);
+    ZgemmArgs u{wi, nc, wi, inv_ptr(h, ki / 64, 0), 64, h->inv_stride, C + ki + c0 * ld, ld, st, C + ki + c0 * ld, ld,
+                st, make_double2(1, 0), make_double2(0, 0), nbat};
+    feast::zgemm_launch(u, false, feast::ZG_GEN, s);
+    if (ki + wi < K1) {
+      ZgemmArgs p{K1 - ki - wi, nc, wi, C + (ki + wi) + ki * ld, ld, st, C + ki + c0 * ld, ld, st,
+                  C + (ki + wi) + c0 * ld, ld, st, make_double2(-1, 0), make_double2(1, 0), nbat};
+      feast::zgemm_launch(p, false, feast::ZG_SUB, s);
+    }
+  }
+  if (K1 < n) {
+    ZgemmArgs p{n - K1, nc, Wo, C + K1 + K0 * ld, ld, st, C + K0 + c0 * ld, ld, st, C + K1 + c0 * ld, ld, st,
+                make_double2(-1, 0), make_double2(1, 0), nbat};
+    feast::zgemm_launch(p, false, feast::ZG_SUB, s);
+  }
+}
+
+void lu_batched(feast_ctx* h, int nbat, int64_t aug) {
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0), ntot = n + aug;
+  double2* C = h->Cw;
+  cudaStream_t sm = h->stream, sp = h->side;
+  const int64_t NBO = h->nbo;
+  int64_t Wo = std::min<int64_t>(NBO, n);
+  factor_block(h, 0, Wo, nbat, sm);
+  feast::laswp_launch(bat(C, ld, st), n, 0, (int)Wo, h->ipiv, Wo, ntot, nbat, sm);
+  for (int64_t K0 = 0; K0 < n; K0 += Wo, Wo = std::min<int64_t>(NBO, n - K0)) {
+    const int64_t K1 = K0 + Wo;
+    if (K1 >= n) {
+      outer_update(h, K0, Wo, n, aug, nbat, sm);      // last block: augmented columns only
+      break;
+    }
+    const int64_t Wo1 = std::min<int64_t>(NBO, n - K1);
+    outer_update(h, K0, Wo, K1, Wo1, nbat, sm);       // next block's columns first
+    if (h->lookahead) {
+      cudaEventRecord(h->ev_a, sm);
+      cudaStreamWaitEvent(sp, h->ev_a, 0);
+      factor_block(h, K1, Wo1, nbat, sp);             // overlaps the rest of the outer update
+      cudaEventRecord(h->ev_p, sp);
+      outer_update(h, K0, Wo, K1 + Wo1, ntot - K1 - Wo1, nbat, sm);
+      cudaStreamWaitEvent(sm, h->ev_p, 0);
+    } else {
+      outer_update(h, K0, Wo, K1 + Wo1, ntot - K1 - Wo1, nbat, sm);
+      factor_block(h, K1, Wo1, nbat, sm);
+    }
+    // block K1's swaps on every column outside it
+    feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, h->ipiv, 0, K1, nbat, sm);
+    feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, h->ipiv, K1 + Wo1, ntot, nbat, sm);
+  }
+}
+
 // Y_k <- op(T_kk^-1) Y_k in place (M = w <= 64): which 0 = L^-1, 1 = U^-1; conj: (.)^H
-void diag_apply(feast_ctx* h, double2* Y, int64_t k, int w, int which, bool conj, int nbat) {
-  const int64_t ld = h->ldc, sy = ld * h->m0;
+void diag_apply(feast_ctx* h, double2* Y, int64_t sy, int64_t k, int w, int which, bool conj, int nbat) {
+  const int64_t ld = h->ldc;
   ZgemmArgs p{w, h->m0, w, inv_ptr(h, k / 64, which), 64, h->inv_stride, Y + k, ld, sy, Y + k, ld, sy,
               make_double2(1, 0), make_double2(0, 0), nbat};
   feast::zgemm_launch(p, conj, feast::ZG_GEN, h->stream);
 }
 
-// Y <- U^-1 L^-1 Y  (Y already row-permuted)
-void solve_right(feast_ctx* h, double2* Y, int nbat) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * n, m = h->m0, sy = ld * m;
+// Y <- U^-1 Y  (Y = L^-1 P R already: the forward substitution ran inside the augmented LU)
+void solve_right_back(feast_ctx* h, double2* Y, int64_t sy, int nbat) {
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0), m = h->m0;
   double2* C = h->Cw;
-  for (int64_t k = 0; k < n; k += h->nb) {
-    const int w = (int)std::min<int64_t>(h->nb, n - k);
-    diag_apply(h, Y, k, w, 0, false, nbat);
-    const int64_t rest = n - k - w;
-    if (rest > 0) {
-      ZgemmArgs p{rest, m, w, C + (k + w) + k * ld, ld, st, Y + k, ld, sy, Y + k + w, ld, sy,
-                  make_double2(-1, 0), make_double2(1, 0), nbat};
-      feast::zgemm_launch(p, false, feast::ZG_SUB, h->stream);
-    }
-  }
   const int64_t last = ((n - 1) / h->nb) * h->nb;
   for (int64_t k = last; k >= 0; k -= h->nb) {
     const int w = (int)std::min<int64_t>(h->nb, n - k);
-    diag_apply(h, Y, k, w, 1, false, nbat);
+    diag_apply(h, Y, sy, k, w, 1, false, nbat);
     if (k > 0) {
       ZgemmArgs p{k, m, w, C + k * ld, ld, st, Y + k, ld, sy, Y, ld, sy, make_double2(-1, 0), make_double2(1, 0), nbat};
       feast::zgemm_launch(p, false, feast::ZG_SUB, h->stream);
@@ -308,11 +363,11 @@ void solve_right(feast_ctx* h, double2* Y, int nbat) {
 
 // Y <- L^-H U^-H Y   (then the caller applies P^T): M^H = U^H L^H P  (P:438-439 same factors)
 void solve_left(feast_ctx* h, double2* Y, int nbat) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * n, m = h->m0, sy = ld * m;
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0), m = h->m0, sy = ld * m;
   double2* C = h->Cw;
   for (int64_t k = 0; k < n; k += h->nb) {  // U^H: lower, non-unit
     const int w = (int)std::min<int64_t>(h->nb, n - k);
-    diag_apply(h, Y, k, w, 1, true, nbat);      // (U_kk^H)^-1 = (U_kk^-1)^H
+    diag_apply(h, Y, sy, k, w, 1, true, nbat);      // (U_kk^H)^-1 = (U_kk^-1)^H
     const int64_t rest = n - k - w;
     if (rest > 0) {
       // Y[k+w:] -= (U[k:k+w, k+w:])^H Y[k:k+w]
@@ -324,7 +379,7 @@ void solve_left(feast_ctx* h, double2* Y, int nbat) {
   const int64_t last = ((n - 1) / h->nb) * h->nb;
   for (int64_t k = last; k >= 0; k -= h->nb) {  // L^H: upper, unit
     const int w = (int)std::min<int64_t>(h->nb, n - k);
-    diag_apply(h, Y, k, w, 0, true, nbat);      // (L_kk^H)^-1 = (L_kk^-1)^H
+    diag_apply(h, Y, sy, k, w, 0, true, nbat);      // (L_kk^H)^-1 = (L_kk^-1)^H
     if (k > 0) {
       // Y[0:k] -= (L[k:k+w, 0:k])^H Y[k:k+w]
       ZgemmArgs p{k, m, w, C + k, ld, st, Y + k, ld, sy, Y, ld, sy, make_double2(-1, 0), make_double2(1, 0), nbat};
@@ -364,16 +419,18 @@ int project_impl(feast_ctx* h, const double2* A, int64_t lda, const double2* B, 
     h->stats_cur = h->stats + 2 * j;
     h->info_cur = h->info + j;
     feast::stats_init_launch(h->stats_cur, h->info_cur, nbat, h->stream);
-    // a2: C_j = z_j B - A
-    feast::shift_launch(bat(h->Cw, ld, ld * n), A, lda, B, ldb, h->zd + j, n, nbat, h->stream);
-    // a3: P_j C_j = L_j U_j
-    lu_batched(h, nbat);
-    feast::perm_launch(h->ipiv, h->perm, doL ? h->iperm : nullptr, n, nbat, h->stream);
+    // a2: C_j = z_j B - A ; R appended as extra columns (augmented system [C_j | R])
+    const int64_t st = ld * (n + m);
+    feast::shift_launch(bat(h->Cw, ld, st), A, lda, B, ldb, h->zd + j, n, nbat, h->stream);
+    if (doR) feast::broadcast_copy_launch(bat(h->Cw + n * ld, ld, st), Rr, ldr, n, m, nbat, h->stream);
+    // a3 (+ forward substitution of a4): P_j [C_j | R] -> [U_j | L_j^-1 P_j R]
+    lu_batched(h, nbat, doR ? m : 0);
+    if (doL) feast::perm_launch(h->ipiv, h->perm, h->iperm, n, nbat, h->stream);
     if (doR) {
-      // a4: Y_j = U^-1 L^-1 P R ;  a5: Q (+)= sum w_j Y_j
-      feast::gather_rows_launch(bat(h->Y, ld, ld * m), Rr, ldr, 0, h->perm, n, m, nbat, h->stream);
-      solve_right(h, h->Y, nbat);
-      feast::accum_launch(Q, ldq, bat(h->Y, ld, ld * m), h->wd + j, nullptr, n, m, nbat, false, jb > 0, h->stream);
+      // a4: Y_j = U_j^-1 (L_j^-1 P_j R) ;  a5: Q (+)= sum w_j Y_j
+      solve_right_back(h, h->Cw + n * ld, st, nbat);
+      feast::accum_launch(Q, ldq, bat(h->Cw + n * ld, ld, st), h->wd + j, nullptr, n, m, nbat, false, jb > 0,
+                          h->stream);
     }
     if (doL) {
       // Z_j = P^T L^-H U^-H RL ;  QL (+)= sum conj(w_j) Z_j  (P^T folded into the accumulate)
@@ -500,12 +557,20 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   // panel strategy: shared-memory cluster panel when the n x nb panel fits in <= 16 CTAs
   h->smem_cs = 0;
   h->nb = 64;   // the diagonal-block inverses (trtri) use 64-row blocks
+  if (const char* e = getenv("FEAST_WP")) {
+    const long v = atol(e);
+    if (v == 8 || v == 16 || v == 32 || v == 64) h->wp = v;
+  }
   for (int cs = 1; cs <= 16; cs *= 2)
-    if (feast::panel_smem_fits(n, 64, cs)) { h->smem_cs = cs; break; }
+    if (feast::panel_smem_fits(n, (int)h->wp, cs)) { h->smem_cs = cs; break; }
   if (const char* e = getenv("FEAST_PANEL")) {   // debugging override: "reg" = register-chunk kernel
     if (e[0] == 'r') { h->smem_cs = 0; h->nb = 64; }
   }
   if (const char* e = getenv("FEAST_LOOKAHEAD")) h->lookahead = e[0] != '0';
+  if (const char* e = getenv("FEAST_NBO")) {
+    const long v = atol(e);
+    if (v >= 64 && v <= 256 && v % 64 == 0) h->nbo = v;
+  }
   {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -525,8 +590,8 @@ static size_t layout(feast_ctx* h, char* base) {
   const int64_t n = h->n, m = h->m0, ld = h->ldc;
   size_t off = 0;
   auto take = [&](size_t b) { size_t o = off; off += align256(b); return base ? (void*)(base + o) : nullptr; };
-  h->Cw = (double2*)take((size_t)h->batch * ld * n * 16);
-  h->Y = (double2*)take((size_t)h->batch * ld * m * 16);
+  h->Cw = (double2*)take((size_t)h->batch * ld * (n + m) * 16);   // [C_j | R] (augmented)
+  h->Y = nullptr;                                                     // right solutions live in Cw
   h->YL = h->mode == FEAST_BI ? (double2*)take((size_t)h->batch * ld * m * 16) : nullptr;
   h->R = !h->b_id ? (double2*)take((size_t)ld * m * 16) : nullptr;
   h->RL = (!h->b_id && h->mode == FEAST_BI) ? (double2*)take((size_t)ld * m * 16) : nullptr;

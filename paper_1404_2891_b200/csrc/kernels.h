@@ -37,10 +37,9 @@ PanelCfg panel_config(int64_t n);
 void panel_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info,
                   int batch, const PanelCfg& cfg, cudaStream_t s);
 
-// Apply row swaps ipiv[k..k+w) to columns [c0, c1) of every matrix.
-// skip_panel: [c0, c1) indexes the n - w columns outside the panel; else all columns.
-void laswp_launch(Batched C, int64_t n, int64_t k, int w, const int32_t* ipiv, int64_t c0, int64_t c1,
-                  int batch, cudaStream_t s, bool skip_panel = true);
+// Apply the cnt (<= 256) sequential swaps ipiv[k..k+cnt) to the columns [c0, c1).
+void laswp_launch(Batched C, int64_t n, int64_t k, int cnt, const int32_t* ipiv, int64_t c0, int64_t c1, int batch,
+                  cudaStream_t s);
 // Cluster panel with the panel resident in shared memory (rows never moved; see panel_smem.cu).
 bool panel_smem_fits(int64_t n, int w, int cs);
 void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info, int batch,

@@ -355,22 +355,19 @@ void stats_init_launch(double* stats, int32_t* info, int batch, cudaStream_t s) 
 }
 
 // ============================================================================ laswp
-// Apply the w swaps of panel k to every column outside the panel.
-// Thread per column; each swap exchanges two 16-byte complex entries of that column.
-__global__ void laswp_kernel(Batched C, int64_t n, int64_t k, int w, const int32_t* __restrict__ ipiv_all,
-                             int64_t c0, int64_t c1, bool skip_panel) {
-  __shared__ int32_t pv[NB_MAX];
+// Apply the cnt (<= 256) sequential swaps ipiv[k..k+cnt) to the columns [c0, c1) of every
+// matrix.  Thread per column; each swap exchanges two 16-byte complex entries.
+__global__ void laswp_kernel(Batched C, int64_t n, int64_t k, int cnt, const int32_t* __restrict__ ipiv_all,
+                             int64_t c0, int64_t c1) {
+  __shared__ int32_t pv[256];
   const int b = blockIdx.y;
   const int32_t* ipiv = ipiv_all + (int64_t)b * n;
-  if (threadIdx.x < w) pv[threadIdx.x] = ipiv[k + threadIdx.x];
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) pv[i] = ipiv[k + i];
   __syncthreads();
-  const int64_t cc = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (cc >= c1) return;
-  // columns [c0, c1) excluding the panel [k, k+w)
-  const int64_t col = (!skip_panel || cc < k) ? cc : cc + w;
-  if (col >= n) return;
+  const int64_t col = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= c1) return;
   double2* Cc = C.p + (int64_t)b * C.stride + col * C.ld;
-  for (int i = 0; i < w; ++i) {
+  for (int i = 0; i < cnt; ++i) {
     const int64_t r1 = k + i, r2 = pv[i];
     if (r1 != r2) {
       const double2 t = Cc[r1];
@@ -380,14 +377,13 @@ __global__ void laswp_kernel(Batched C, int64_t n, int64_t k, int w, const int32
   }
 }
 
-void laswp_launch(Batched C, int64_t n, int64_t k, int w, const int32_t* ipiv, int64_t c0, int64_t c1,
-                  int batch, cudaStream_t s, bool skip_panel) {
-  ProfScope ps_(K_LASWP, 0.0, (double)batch * (c1 - c0) * w * 64.0, s);
-  // here [c0, c1) indexes the n - w columns outside the panel
-  if (c1 <= c0) return;
+void laswp_launch(Batched C, int64_t n, int64_t k, int cnt, const int32_t* ipiv, int64_t c0, int64_t c1, int batch,
+                  cudaStream_t s) {
+  if (c1 <= c0 || cnt <= 0) return;
+  ProfScope ps_(K_LASWP, 0.0, (double)batch * (c1 - c0) * cnt * 64.0, s);
   const int threads = 128;
   dim3 grid((unsigned)((c1 - c0 + threads - 1) / threads), (unsigned)batch);
-  laswp_kernel<<<grid, threads, 0, s>>>(C, n, k, w, ipiv, c0, c1, skip_panel);
+  laswp_kernel<<<grid, threads, 0, s>>>(C, n, k, cnt, ipiv, c0, c1);
   count_launch();
 }
 
@@ -403,33 +399,33 @@ namespace {
 constexpr int TR_T = 128, TR_H = 32;
 
 template <bool CONJT>
-__device__ __forceinline__ double2 tget(const double2* __restrict__ T, int64_t ld, int r, int i) {
-  // op(T)[r][i]
-  if (!CONJT) return __ldg(T + r + (int64_t)i * ld);
-  const double2 v = __ldg(T + i + (int64_t)r * ld);
+__device__ __forceinline__ double2 tget(const double2* __restrict__ Ts, int r, int i) {
+  // op(T)[r][i] from the shared-memory copy Ts[c * 65 + r] = T[r][c]
+  if (!CONJT) return Ts[i * (TR_H * 2 + 1) + r];
+  const double2 v = Ts[r * (TR_H * 2 + 1) + i];
   return make_double2(v.x, -v.y);
 }
 
 // solve the h x h triangular block at rows/cols [o, o+h) of op(T), in place on x
 template <bool LOWER, bool UNIT, bool CONJT>
-__device__ __forceinline__ void tri_solve(const double2* __restrict__ T, int64_t ld, int o, int h, double2 (&x)[TR_H]) {
+__device__ __forceinline__ void tri_solve(const double2* __restrict__ Ts, int o, int h, double2 (&x)[TR_H]) {
   if (LOWER) {
 #pragma unroll
     for (int i = 0; i < TR_H; ++i) {
       if (i < h) {
-        if (!UNIT) x[i] = cdiv(x[i], tget<CONJT>(T, ld, o + i, o + i));
+        if (!UNIT) x[i] = cdiv(x[i], tget<CONJT>(Ts, o + i, o + i));
 #pragma unroll
         for (int r = i + 1; r < TR_H; ++r)
-          if (r < h) x[r] = cfms(x[r], tget<CONJT>(T, ld, o + r, o + i), x[i]);
+          if (r < h) x[r] = cfms(x[r], tget<CONJT>(Ts, o + r, o + i), x[i]);
       }
     }
   } else {
 #pragma unroll
     for (int i = TR_H - 1; i >= 0; --i) {
       if (i < h) {
-        if (!UNIT) x[i] = cdiv(x[i], tget<CONJT>(T, ld, o + i, o + i));
+        if (!UNIT) x[i] = cdiv(x[i], tget<CONJT>(Ts, o + i, o + i));
 #pragma unroll
-        for (int r = 0; r < i; ++r) x[r] = cfms(x[r], tget<CONJT>(T, ld, o + r, o + i), x[i]);
+        for (int r = 0; r < i; ++r) x[r] = cfms(x[r], tget<CONJT>(Ts, o + r, o + i), x[i]);
       }
     }
   }
@@ -437,12 +433,17 @@ __device__ __forceinline__ void tri_solve(const double2* __restrict__ T, int64_t
 
 template <bool LOWER, bool UNIT, bool CONJT>
 __global__ void __launch_bounds__(TR_T) trsm_kernel(Batched Tb, Batched Xb, int nb, int64_t ncols) {
+  extern __shared__ __align__(16) double2 Ts[];   // T[r][c] at Ts[c * 65 + r] (nb <= 64)
   const int b = blockIdx.y;
   const double2* __restrict__ T = Tb.p + (int64_t)b * Tb.stride;
+  for (int idx = threadIdx.x; idx < nb * nb; idx += TR_T) {
+    const int r = idx % nb, c = idx / nb;
+    Ts[c * (TR_H * 2 + 1) + r] = T[r + (int64_t)c * Tb.ld];
+  }
+  __syncthreads();
   const int64_t c = (int64_t)blockIdx.x * TR_T + threadIdx.x;
   if (c >= ncols) return;
   double2* __restrict__ X = Xb.p + (int64_t)b * Xb.stride + c * Xb.ld;
-  const int64_t ld = Tb.ld;
   const int h0 = min(nb, TR_H), h1 = nb - h0;
   double2 x[TR_H];
   // first half to solve: rows [0,h0) for forward, rows [h0,nb) for backward
@@ -451,7 +452,7 @@ __global__ void __launch_bounds__(TR_T) trsm_kernel(Batched Tb, Batched Xb, int 
   if (ha > 0) {
 #pragma unroll
     for (int r = 0; r < TR_H; ++r) if (r < ha) x[r] = X[oa + r];
-    tri_solve<LOWER, UNIT, CONJT>(T, ld, oa, ha, x);
+    tri_solve<LOWER, UNIT, CONJT>(Ts, oa, ha, x);
 #pragma unroll
     for (int r = 0; r < TR_H; ++r) if (r < ha) X[oa + r] = x[r];
   }
@@ -463,9 +464,9 @@ __global__ void __launch_bounds__(TR_T) trsm_kernel(Batched Tb, Batched Xb, int 
       const double2 xt = X[oa + t];
 #pragma unroll
       for (int r = 0; r < TR_H; ++r)
-        if (r < hb) x[r] = cfms(x[r], tget<CONJT>(T, ld, ob + r, oa + t), xt);
+        if (r < hb) x[r] = cfms(x[r], tget<CONJT>(Ts, ob + r, oa + t), xt);
     }
-    tri_solve<LOWER, UNIT, CONJT>(T, ld, ob, hb, x);
+    tri_solve<LOWER, UNIT, CONJT>(Ts, ob, hb, x);
 #pragma unroll
     for (int r = 0; r < TR_H; ++r) if (r < hb) X[ob + r] = x[r];
   }
@@ -473,8 +474,14 @@ __global__ void __launch_bounds__(TR_T) trsm_kernel(Batched Tb, Batched Xb, int 
 
 template <bool LOWER, bool UNIT, bool CONJT>
 void trsm_t(Batched T, Batched X, int nb, int64_t ncols, int batch, cudaStream_t s) {
+  static bool configured = false;
+  const size_t smem = (size_t)(TR_H * 2 + 1) * 64 * sizeof(double2);
+  if (!configured) {
+    cudaFuncSetAttribute(trsm_kernel<LOWER, UNIT, CONJT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
   dim3 grid((unsigned)((ncols + TR_T - 1) / TR_T), (unsigned)batch);
-  trsm_kernel<LOWER, UNIT, CONJT><<<grid, TR_T, 0, s>>>(T, X, nb, ncols);
+  trsm_kernel<LOWER, UNIT, CONJT><<<grid, TR_T, smem, s>>>(T, X, nb, ncols);
   count_launch();
 }
 }  // namespace

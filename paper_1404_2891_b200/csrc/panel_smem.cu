@@ -175,7 +175,15 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
       for (int s = 0; s < S; ++s)
         if (s == bs) {
           const double2 pv = a[s][jj];
-          if (pv.x != 0.0 || pv.y != 0.0) myrcp = crcp(pv);
+          if (pv.x != 0.0 || pv.y != 0.0) {
+            const double m2 = fma(pv.x, pv.x, pv.y * pv.y);
+            if (m2 > 1e-300 && m2 < 1e300) {       // 1/p = conj(p) / |p|^2, one reciprocal
+              const double d = __drcp_rn(m2);
+              myrcp = make_double2(pv.x * d, -pv.y * d);
+            } else {
+              myrcp = crcp(pv);                     // Smith's division at extreme magnitudes
+            }
+          }
         }
       double wbv = bv;
       int wbi = bi;
@@ -248,9 +256,9 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
         }
       }
       if (crank == 0 && tid == 0) {
-        const double ap = hypot(p.x, p.y);
-        pmin = fmin(pmin, ap);
-        pmax = fmax(pmax, ap);
+        const double ap2 = fma(p.x, p.x, p.y * p.y);   // |p|^2; sqrt taken once at the end
+        pmin = fmin(pmin, ap2);
+        pmax = fmax(pmax, ap2);
         if (pzero && !info) info = (int)(k + col + 1);
       }
     }
@@ -361,8 +369,8 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
       pos2row[col] = p;
       if (p < w) cur[p] = col;
     }
-    stats_all[2 * b] = fmin(stats_all[2 * b], pmin);
-    stats_all[2 * b + 1] = fmax(stats_all[2 * b + 1], pmax);
+    stats_all[2 * b] = fmin(stats_all[2 * b], sqrt(pmin));
+    stats_all[2 * b + 1] = fmax(stats_all[2 * b + 1], sqrt(pmax));
     if (info && !info_all[b]) info_all[b] = info;
   }
   if (nrow > 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -407,7 +415,7 @@ void panel_trace_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_ptr
 
 bool panel_smem_fits(int64_t n, int w, int cs) {
   const int64_t Lc = (n + cs - 1) / cs;
-  return w <= WMAX && (size_t)Lc * w * sizeof(double2) <= 190 * 1024 && Lc <= 2 * PT;
+  return w <= WMAX && (size_t)Lc * w * sizeof(double2) <= 190 * 1024 && Lc <= 4 * PT;
 }
 
 void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info, int batch,
@@ -416,7 +424,8 @@ void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, do
   ProfScope ps_(K_PANEL, (double)batch * (4.0 * L_ * w * w - 4.0 * w * (double)w * w / 3.0), 0.0, s);
   const int64_t Lc = (n + cs - 1) / cs;
   if (Lc <= PT) launch_s<1>(C, n, k, w, ipiv, stats, info, batch, cs, s);
-  else launch_s<2>(C, n, k, w, ipiv, stats, info, batch, cs, s);
+  else if (Lc <= 2 * PT) launch_s<2>(C, n, k, w, ipiv, stats, info, batch, cs, s);
+  else launch_s<4>(C, n, k, w, ipiv, stats, info, batch, cs, s);
 }
 
 }  // namespace feast

@@ -99,6 +99,15 @@ def _ptr_ld(t, rows, name):
     return ctypes.c_void_p(t.data_ptr()), ld
 
 
+def allreduce_node_sum(t: torch.Tensor, group=None) -> torch.Tensor:
+    """The cross-rank node sum of the projector: in-place SUM all-reduce of a rank's
+    partial Q (complex128 is reduced as its float64 view).  No-op without a process group."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(torch.view_as_real(t) if t.is_complex() else t, group=group)
+    return t
+
+
 class _CudaPtr:
     """__cuda_array_interface__ shim so the all-reduce callback can wrap a raw buffer."""
 
@@ -154,8 +163,7 @@ class Feast:
     def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
         """Node sum across ranks: in-place all-reduce of a partial Q."""
         if self.world > 1:
-            import torch.distributed as dist
-            dist.all_reduce(t, group=self.group)
+            allreduce_node_sum(t, self.group)
         return t
 
     def close(self):

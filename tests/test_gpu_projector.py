@@ -143,3 +143,17 @@ def test_register_panel_variant(monkeypatch, key, n, m0):
     Q, QL = f.project_bi(dev(P.A), dev(P.B), dev(P.X0), dev(P.X0))
     assert rel(host(Q), oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
     assert rel(host(QL), oracle.project(P.A, P.B, P.X0, z, w, left=True)) <= TOL
+
+
+@pytest.mark.parametrize("nbo,lookahead", [("64", "1"), ("128", "1"), ("256", "0"), ("192", "1")])
+def test_blocking_variants(monkeypatch, nbo, lookahead):
+    """Outer block (trailing-update K) and lookahead variants of the two-level LU: same bar,
+    on a ragged size spanning several outer blocks."""
+    monkeypatch.setenv("FEAST_NBO", nbo)
+    monkeypatch.setenv("FEAST_LOOKAHEAD", lookahead)
+    P = synth.make_pencil("C2", n=700, m0=37)
+    z, w = _oracle_nodes(P)
+    f = _handle(P, mode=fb.BI)
+    Q, QL = f.project_bi(dev(P.A), dev(P.B), dev(P.X0), dev(P.X0))
+    assert rel(host(Q), oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
+    assert rel(host(QL), oracle.project(P.A, P.B, P.X0, z, w, left=True)) <= TOL

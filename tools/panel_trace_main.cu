@@ -5,7 +5,8 @@
 #include <cuda_runtime.h>
 #include "kernels.h"
 namespace feast { void panel_trace_read(unsigned long long* out); }
-int main() {
+int main(int argc, char** argv) {
+  int W = argc > 1 ? atoi(argv[1]) : 64, CS = argc > 2 ? atoi(argv[2]) : 16;
   int n = 2048; int64_t ld = n;
   std::vector<double2> h((size_t)n * n);
   srand(1);
@@ -15,7 +16,7 @@ int main() {
   feast::stats_init_launch(st, inf, 1, 0);
   for (int rep = 0; rep < 3; ++rep) {
     cudaMemcpy(d, h.data(), h.size() * 16, cudaMemcpyHostToDevice);
-    feast::panel_smem_launch(feast::Batched{d, ld, ld * n}, n, 0, 64, ipiv, st, inf, 1, 16, 0);
+    feast::panel_smem_launch(feast::Batched{d, ld, ld * n}, n, 0, W, ipiv, st, inf, 1, CS, 0);
     cudaDeviceSynchronize();
   }
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
@@ -23,7 +24,7 @@ int main() {
   feast::panel_trace_read(t);
   auto us = [&](int i) { return (t[i] - t[0]) / 1000.0; };
   printf("start->loaded %.2f us\n", us(1));
-  for (int col = 0; col < 64; ++col) {
+  for (int col = 0; col < W; ++col) {
     printf("col %2d: begin %.2f  pushed %.2f  arrived %.2f", col, us(8+4*col), us(9+4*col), us(10+4*col));
     if (col % 8 == 7 && col < 63) printf("   | chunk end wait %.2f -> %.2f, done %.2f", us(300+4*(col/8)), us(301+4*(col/8)), us(302+4*(col/8)));
     if (col % 8 == 7 && col < 63) printf("  solve-done %.2f", us(303+4*(col/8)));
