@@ -273,7 +273,7 @@ void factor_block(feast_ctx* h, int64_t K0, int64_t Wo, int nbat, cudaStream_t s
     const int64_t c1 = ki + wi, rem = K0 + Wo - c1;
     if (rem > 0) {
       ZgemmArgs u{wi, rem, wi, inv_ptr(h, ki / 64, 0), 64, h->inv_stride, C + ki + c1 * ld, ld, st, C + ki + c1 * ld,
-                  ld, st, make_double2(1, 0), make_double2(0, 0), nbat};
+                  ld, st, make_double2(1, 0), make_double2(0, 0), nbat, 1};
       feast::zgemm_launch(u, false, feast::ZG_GEN, s);
       ZgemmArgs p{n - c1, rem, wi, C + c1 + ki * ld, ld, st, C + ki + c1 * ld, ld, st, C + c1 + c1 * ld, ld, st,
                   make_double2(-1, 0), make_double2(1, 0), nbat};
@@ -290,7 +290,7 @@ void outer_update(feast_ctx* h, int64_t K0, int64_t Wo, int64_t c0, int64_t nc, 
   for (int64_t ki = K0; ki < K1; ki += 64) {
     const int wi = (int)std::min<int64_t>(64, K1 - ki);
     ZgemmArgs u{wi, nc, wi, inv_ptr(h, ki / 64, 0), 64, h->inv_stride, C + ki + c0 * ld, ld, st, C + ki + c0 * ld, ld,
-                st, make_double2(1, 0), make_double2(0, 0), nbat};
+                st, make_double2(1, 0), make_double2(0, 0), nbat, 1};
     feast::zgemm_launch(u, false, feast::ZG_GEN, s);
     if (ki + wi < K1) {
       ZgemmArgs p{K1 - ki - wi, nc, wi, C + (ki + wi) + ki * ld, ld, st, C + ki + c0 * ld, ld, st,
@@ -342,7 +342,7 @@ void lu_batched(feast_ctx* h, int nbat, int64_t aug) {
 void diag_apply(feast_ctx* h, double2* Y, int64_t sy, int64_t k, int w, int which, bool conj, int nbat) {
   const int64_t ld = h->ldc;
   ZgemmArgs p{w, h->m0, w, inv_ptr(h, k / 64, which), 64, h->inv_stride, Y + k, ld, sy, Y + k, ld, sy,
-              make_double2(1, 0), make_double2(0, 0), nbat};
+              make_double2(1, 0), make_double2(0, 0), nbat, 1};
   feast::zgemm_launch(p, conj, feast::ZG_GEN, h->stream);
 }
 

@@ -15,6 +15,7 @@ struct ZgemmArgs {
   double2* C; int64_t ldc, sC;        // M x N
   double2 alpha, beta;
   int batch;                          // batch index z adds z*sA, z*sB, z*sC
+  int inplace = 0;                    // 1: C aliases B (requires M <= 64: one CTA row of tiles)
 };
 void zgemm_launch(const ZgemmArgs& p, bool conjA, int mode, cudaStream_t s);
 

@@ -27,12 +27,16 @@
 namespace feast {
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, THREADS = 128;
-constexpr int LDA_S = BM + 4;   // As[k][m]
+constexpr int BK = 16, STAGES = 3;
 constexpr int LDB_S = BK + 2;   // Bs[n][k]
-constexpr int A_STAGE = BK * LDA_S;
-constexpr int B_STAGE = BN * LDB_S;
-constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double2);
+template <int BM, int BN>
+struct Tile {
+  static constexpr int THREADS = 32 * (BM / 32) * (BN / 32);
+  static constexpr int LDA_S = BM + 4;   // As[k][m]
+  static constexpr int A_STAGE = BK * LDA_S;
+  static constexpr int B_STAGE = BN * LDB_S;
+  static constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double2);
+};
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -53,8 +57,11 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <bool CONJA, int MODE>
-__global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_kernel(ZgemmArgs p) {
+template <int BM, int BN, bool CONJA, int MODE>
+__global__ void __launch_bounds__(Tile<BM, BN>::THREADS, 2) zgemm_dmma_kernel(ZgemmArgs p) {
+  constexpr int THREADS = Tile<BM, BN>::THREADS, LDA_S = Tile<BM, BN>::LDA_S;
+  constexpr int A_STAGE = Tile<BM, BN>::A_STAGE, B_STAGE = Tile<BM, BN>::B_STAGE;
+  constexpr int WN = BN / 32;   // warps along N
   extern __shared__ __align__(128) double2 smem[];
   double2* As = smem;
   double2* Bs = smem + STAGES * A_STAGE;
@@ -66,7 +73,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_kernel(ZgemmArgs p) {
   const int64_t M = p.M, N = p.N, K = p.K;
   const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = (warp / WN) * 32, wn = (warp % WN) * 32;
   const int g = lane >> 2, t = lane & 3;
 
   auto load_tile = [&](int stage, int64_t kt) {
@@ -174,18 +181,34 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_kernel(ZgemmArgs p) {
     }
 }
 
-template <bool CONJA, int MODE>
-void launch_t(const ZgemmArgs& p, cudaStream_t s) {
-  ProfScope ps_(K_ZGEMM, 8.0 * (double)p.M * (double)p.N * (double)p.K * p.batch, 0.0, s);
+template <int BM, int BN, bool CONJA, int MODE>
+void launch_tile(const ZgemmArgs& p, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(zgemm_dmma_kernel<CONJA, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)SMEM_BYTES);
+    cudaFuncSetAttribute(zgemm_dmma_kernel<BM, BN, CONJA, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Tile<BM, BN>::SMEM_BYTES);
     configured = true;
   }
   dim3 grid((unsigned)((p.N + BN - 1) / BN), (unsigned)((p.M + BM - 1) / BM), (unsigned)p.batch);
-  zgemm_dmma_kernel<CONJA, MODE><<<grid, THREADS, SMEM_BYTES, s>>>(p);
+  zgemm_dmma_kernel<BM, BN, CONJA, MODE><<<grid, Tile<BM, BN>::THREADS, Tile<BM, BN>::SMEM_BYTES, s>>>(p);
   count_launch();
+}
+
+// Tile choice: 64x64 CTAs (4 warps) normally; 32x32 CTAs (1 warp) when the 64x64 grid would not
+// fill the 148 SMs twice over (small, latency-bound launches: diagonal-block applications,
+// in-block updates, the substitution updates of late blocks).
+template <bool CONJA, int MODE>
+void launch_t(const ZgemmArgs& p, cudaStream_t s) {
+  ProfScope ps_(K_ZGEMM, 8.0 * (double)p.M * (double)p.N * (double)p.K * p.batch, 0.0, s);
+  const int64_t big = ((p.M + 63) / 64) * ((p.N + 63) / 64) * p.batch;
+  if (p.inplace) {   // every CTA must read its whole B column block before writing it: BM >= M
+    if (big < 296) launch_tile<64, 32, CONJA, MODE>(p, s);
+    else launch_tile<64, 64, CONJA, MODE>(p, s);
+  } else if (big < 296) {
+    launch_tile<32, 32, CONJA, MODE>(p, s);
+  } else {
+    launch_tile<64, 64, CONJA, MODE>(p, s);
+  }
 }
 
 }  // namespace

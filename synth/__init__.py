@@ -136,3 +136,65 @@ def node_owner_range(q: int, rank: int, world: int) -> tuple[int, int]:
 
 def random_block(n: int, m: int, seed: int) -> np.ndarray:
     return np.asfortranarray(_cn(np.random.Generator(np.random.PCG64(seed)), (n, m)))
+
+
+def make_pencil_torch(key: str, n: int | None = None, m0: int | None = None, device="cuda", seed_offset: int = 0):
+    """GPU variant of make_pencil for the large configs (C3-C5 at full size): the same recipe
+    drawn with torch's seeded generator on the device, and A built with a library solve
+    (torch.linalg.solve, cuSOLVER) — fixture generation, not the method.  Returns a Pencil
+    whose matrices are column-major complex128 torch tensors on `device` (V and lam kept for
+    the spectral identity, on the device as well)."""
+    import torch
+
+    spec = CONFIGS[key]
+    n = spec.n if n is None else int(n)
+    m0 = spec.m0 if m0 is None else int(m0)
+    k = int(key[1:]) - 1
+    g = torch.Generator(device=device)
+    g.manual_seed(SEED_BASE + k + 1000 * seed_offset + 7)
+    sq = math.sqrt(n)
+    f64 = dict(dtype=torch.float64, device=device)
+
+    def cn(shape):
+        return torch.complex(torch.randn(shape, generator=g, **f64), torch.randn(shape, generator=g, **f64)) / math.sqrt(2.0)
+
+    def colmajor(t):
+        return t.t().contiguous().t()
+
+    lam = V = None
+    if spec.kind == "csym":
+        gh = torch.randn((n, n), generator=g, **f64)
+        H = (gh + gh.T) / (2.0 * sq)
+        del gh
+        D = torch.rand(n, generator=g, **f64) * 0.05
+        A = torch.complex(H, torch.diag(D))
+        del H
+        gs = torch.randn((n, n), generator=g, **f64)
+        B = torch.eye(n, **f64) + spec.bscale * (gs + gs.T) / (2.0 * sq)
+        del gs
+        B = torch.complex(B, torch.zeros_like(B))
+        A, B = colmajor(A), colmajor(B)
+    else:
+        if spec.lam == "square1":
+            lam = torch.complex(torch.rand(n, generator=g, **f64) * 2 - 1, torch.rand(n, generator=g, **f64) * 2 - 1)
+        elif spec.lam == "rect2x1":
+            lam = torch.complex(torch.rand(n, generator=g, **f64) * 4 - 2, torch.rand(n, generator=g, **f64) * 2 - 1)
+        else:
+            rr = torch.sqrt(torch.rand(n, generator=g, **f64))
+            th = 2 * math.pi * torch.rand(n, generator=g, **f64)
+            lam = torch.polar(rr, th)
+        V = cn((n, n)) * (spec.vscale / sq)
+        V.diagonal().add_(1.0)
+        # A = V diag(lam) V^-1 (= solve(V^T, (V diag(lam))^T)^T)
+        M = torch.linalg.solve(V.T, (V * lam[None, :]).T).T
+        if spec.b_is_identity:
+            B = None
+            A = colmajor(M)
+        else:
+            B = cn((n, n)) * (spec.bscale / sq)
+            B.diagonal().add_(1.0)
+            A = colmajor(B @ M)
+            B = colmajor(B)
+        del M
+    X0 = colmajor(cn((n, m0)))
+    return Pencil(spec, n, m0, A, B, X0, lam, V)

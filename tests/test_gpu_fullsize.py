@@ -1,0 +1,58 @@
+"""Full BASELINE sizes (C3, C4, C5) in the launch configuration bench.py / tools use, checked
+with properties that hold at any size (the oracle cannot factor n = 8192..32768 in a test):
+  * spectral identity Q = V rho(Lambda) V^-1 X (eq. quadf_surM) with the closed-form
+    filter 1/(1 + x^q) (reading R1) and a cuSOLVER solve for V^-1 X — independent of the FEAST
+    kernels (C4 right and left, C5);
+  * complex-symmetric invariant (B X)^T Q symmetric for C3 (C_j^T = C_j).
+Bar: relative Frobenius error <= 1e-10 (BASELINE north_star)."""
+import pytest
+import torch
+
+import synth
+from paper_1404_2891_b200 import Feast, feast as fb
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def _rel(a, b):
+    return float(torch.linalg.norm(a - b) / torch.linalg.norm(b))
+
+
+def _rho(P):
+    s = P.spec
+    return 1.0 / (1.0 + ((P.lam - s.c) / s.r) ** P.q)
+
+
+def test_c3_full_complex_symmetric():
+    P = synth.make_pencil_torch("C3")
+    s = P.spec
+    f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, False)
+    Q = f.project(P.A, P.B, P.X0)
+    assert torch.isfinite(torch.view_as_real(Q)).all()
+    M = (P.B @ P.X0).T @ Q
+    assert _rel(M, M.T) <= TOL
+    # linearity on the same factorizations' inputs: project(2i X) = 2i project(X)
+    Q2 = f.project(P.A, P.B, (2j * P.X0).t().contiguous().t())
+    assert _rel(Q2, 2j * Q) <= 1e-13
+
+
+def test_c4_full_bi_spectral():
+    P = synth.make_pencil_torch("C4")
+    s = P.spec
+    f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.BI, True, max_batch=16)
+    V0 = torch.linalg.solve(P.X0.conj().T @ P.X0, P.X0.conj().T).conj().T.t().contiguous().t()  # reading R6
+    Q, QL = f.project_bi(P.A, None, P.X0, V0)
+    rho = _rho(P)
+    assert _rel(Q, P.V @ (rho[:, None] * torch.linalg.solve(P.V, P.X0))) <= TOL
+    QLs = torch.linalg.solve(P.V.conj().T, rho.conj()[:, None] * (P.V.conj().T @ V0))
+    assert _rel(QL, QLs) <= TOL
+
+
+def test_c5_full_spectral():
+    P = synth.make_pencil_torch("C5")
+    s = P.spec
+    f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, False, max_batch=4)
+    Q = f.project(P.A, P.B, P.X0)
+    Qs = P.V @ (_rho(P)[:, None] * torch.linalg.solve(P.V, P.X0))
+    assert _rel(Q, Qs) <= TOL
