@@ -146,6 +146,15 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
  * index of the smallest ratio.  Either pointer may be NULL. */
 int feast_node_stats(feast_handle h, double* min_rel_pivot, int32_t* worst_node);
 
+/* Factor-once reuse across calls (the paper's lever P:912-913 "each linear system
+ * can be factored just once for the entire iterative process").  enable = 1 turns it on and
+ * invalidates any cached factors; while on, a projection whose A and B pointers equal those of
+ * the call that factored skips a2-a3 and runs only the substitutions on the cached L_j, U_j, P_j.
+ * The caller must call feast_factor_cache(h, 1) again after modifying A or B in place.
+ * Requires all owned nodes resident (max_batch 0 or >= q/world): FEAST_E_NOMEM otherwise.
+ * enable = 0 turns it off (every call refactors: the timed hot path of bench.py). */
+int feast_factor_cache(feast_handle h, int32_t enable);
+
 /* Number of this library's kernels launched by the last call (for bench accounting). */
 int64_t feast_last_launch_count(feast_handle h);
 

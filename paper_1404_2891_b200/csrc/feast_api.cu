@@ -36,6 +36,8 @@ struct feast_ctx {
   feast::PanelCfg pcfg{};
   int smem_cs = 0;   // cluster size of the shared-memory panel kernel (0: register-chunk kernel)
   bool lookahead = true;
+  bool cache_on = false, cache_valid = false;   // factor-once reuse across calls
+  const void *cache_A = nullptr, *cache_B = nullptr;
   int64_t nbo = 256;                  // outer block (trailing-update K); multiple of 64
   int64_t wp = 32;                    // cluster-panel width (divides 64)
   cudaStream_t side = nullptr;        // high-priority stream for the lookahead panel
@@ -346,6 +348,22 @@ void diag_apply(feast_ctx* h, double2* Y, int64_t sy, int64_t k, int w, int whic
   feast::zgemm_launch(p, conj, feast::ZG_GEN, h->stream);
 }
 
+// Y <- L^-1 Y (Y already row-permuted): used when the factors are cached (no augmented LU)
+void solve_right_fwd(feast_ctx* h, double2* Y, int64_t sy, int nbat) {
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0), m = h->m0;
+  double2* C = h->Cw;
+  for (int64_t k = 0; k < n; k += h->nb) {
+    const int w = (int)std::min<int64_t>(h->nb, n - k);
+    diag_apply(h, Y, sy, k, w, 0, false, nbat);
+    const int64_t rest = n - k - w;
+    if (rest > 0) {
+      ZgemmArgs p{rest, m, w, C + (k + w) + k * ld, ld, st, Y + k, ld, sy, Y + k + w, ld, sy,
+                  make_double2(-1, 0), make_double2(1, 0), nbat};
+      feast::zgemm_launch(p, false, feast::ZG_SUB, h->stream);
+    }
+  }
+}
+
 // Y <- U^-1 Y  (Y = L^-1 P R already: the forward substitution ran inside the augmented LU)
 void solve_right_back(feast_ctx* h, double2* Y, int64_t sy, int nbat) {
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0), m = h->m0;
@@ -418,19 +436,29 @@ int project_impl(feast_ctx* h, const double2* A, int64_t lda, const double2* B, 
     const int j = h->j0 + jb;
     h->stats_cur = h->stats + 2 * j;
     h->info_cur = h->info + j;
-    feast::stats_init_launch(h->stats_cur, h->info_cur, nbat, h->stream);
-    // a2: C_j = z_j B - A ; R appended as extra columns (augmented system [C_j | R])
     const int64_t st = ld * (n + m);
-    feast::shift_launch(bat(h->Cw, ld, st), A, lda, B, ldb, h->zd + j, n, nbat, h->stream);
-    if (doR) feast::broadcast_copy_launch(bat(h->Cw + n * ld, ld, st), Rr, ldr, n, m, nbat, h->stream);
-    // a3 (+ forward substitution of a4): P_j [C_j | R] -> [U_j | L_j^-1 P_j R]
-    lu_batched(h, nbat, doR ? m : 0);
-    if (doL) feast::perm_launch(h->ipiv, h->perm, h->iperm, n, nbat, h->stream);
-    if (doR) {
-      // a4: Y_j = U_j^-1 (L_j^-1 P_j R) ;  a5: Q (+)= sum w_j Y_j
-      solve_right_back(h, h->Cw + n * ld, st, nbat);
-      feast::accum_launch(Q, ldq, bat(h->Cw + n * ld, ld, st), h->wd + j, nullptr, n, m, nbat, false, jb > 0,
-                          h->stream);
+    const bool reuse = h->cache_on && h->cache_valid && h->batch >= owned && h->cache_A == A && h->cache_B == B;
+    if (!reuse) {
+      feast::stats_init_launch(h->stats_cur, h->info_cur, nbat, h->stream);
+      // a2: C_j = z_j B - A ; R appended as extra columns (augmented system [C_j | R])
+      feast::shift_launch(bat(h->Cw, ld, st), A, lda, B, ldb, h->zd + j, n, nbat, h->stream);
+      if (doR) feast::broadcast_copy_launch(bat(h->Cw + n * ld, ld, st), Rr, ldr, n, m, nbat, h->stream);
+      // a3 (+ forward substitution of a4): P_j [C_j | R] -> [U_j | L_j^-1 P_j R]
+      lu_batched(h, nbat, doR ? m : 0);
+      if (doL || h->cache_on) feast::perm_launch(h->ipiv, h->perm, h->iperm, n, nbat, h->stream);
+      if (h->cache_on && h->batch >= owned) { h->cache_valid = true; h->cache_A = A; h->cache_B = B; }
+      if (doR) {
+        // a4: Y_j = U_j^-1 (L_j^-1 P_j R) ;  a5: Q (+)= sum w_j Y_j
+        solve_right_back(h, h->Cw + n * ld, st, nbat);
+        feast::accum_launch(Q, ldq, bat(h->Cw + n * ld, ld, st), h->wd + j, nullptr, n, m, nbat, false, jb > 0,
+                            h->stream);
+      }
+    } else if (doR) {
+      // cached factors (NEXT-1, "factored just once"): Y_j = U^-1 L^-1 P_j R
+      feast::gather_rows_launch(bat(h->Y, ld, ld * m), Rr, ldr, 0, h->perm, n, m, nbat, h->stream);
+      solve_right_fwd(h, h->Y, ld * m, nbat);
+      solve_right_back(h, h->Y, ld * m, nbat);
+      feast::accum_launch(Q, ldq, bat(h->Y, ld, ld * m), h->wd + j, nullptr, n, m, nbat, false, jb > 0, h->stream);
     }
     if (doL) {
       // Z_j = P^T L^-H U^-H RL ;  QL (+)= sum conj(w_j) Z_j  (P^T folded into the accumulate)
@@ -561,8 +589,13 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
     const long v = atol(e);
     if (v == 8 || v == 16 || v == 32 || v == 64) h->wp = v;
   }
+  // smallest cluster whose CTAs hold <= 256 panel rows (two per thread: no register spills)
   for (int cs = 1; cs <= 16; cs *= 2)
-    if (feast::panel_smem_fits(n, (int)h->wp, cs)) { h->smem_cs = cs; break; }
+    if (feast::panel_smem_fits(n, (int)h->wp, cs) && (n + cs - 1) / cs <= 256) { h->smem_cs = cs; break; }
+  if (const char* e = getenv("FEAST_CS")) {
+    const int v = atoi(e);
+    if (v >= 1 && v <= 16 && feast::panel_smem_fits(n, (int)h->wp, v)) h->smem_cs = v;
+  }
   if (const char* e = getenv("FEAST_PANEL")) {   // debugging override: "reg" = register-chunk kernel
     if (e[0] == 'r') { h->smem_cs = 0; h->nb = 64; }
   }
@@ -591,7 +624,7 @@ static size_t layout(feast_ctx* h, char* base) {
   size_t off = 0;
   auto take = [&](size_t b) { size_t o = off; off += align256(b); return base ? (void*)(base + o) : nullptr; };
   h->Cw = (double2*)take((size_t)h->batch * ld * (n + m) * 16);   // [C_j | R] (augmented)
-  h->Y = nullptr;                                                     // right solutions live in Cw
+  h->Y = (double2*)take((size_t)h->batch * ld * m * 16);             // right solves with cached factors
   h->YL = h->mode == FEAST_BI ? (double2*)take((size_t)h->batch * ld * m * 16) : nullptr;
   h->R = !h->b_id ? (double2*)take((size_t)ld * m * 16) : nullptr;
   h->RL = (!h->b_id && h->mode == FEAST_BI) ? (double2*)take((size_t)ld * m * 16) : nullptr;
@@ -816,6 +849,16 @@ int feast_node_stats(feast_handle h, double* min_rel_pivot, int32_t* worst_node)
 }
 
 int64_t feast_last_launch_count(feast_handle h) { return h ? h->launches : 0; }
+
+int feast_factor_cache(feast_handle h, int32_t enable) {
+  if (!h) return FEAST_E_ARG;
+  h->cache_on = enable != 0;
+  h->cache_valid = false;
+  h->cache_A = h->cache_B = nullptr;
+  if (h->cache_on && h->batch < h->j1 - h->j0)
+    return fail(h, FEAST_E_NOMEM, "factor cache needs max_batch >= owned nodes (all factors resident)%s");
+  return FEAST_OK;
+}
 
 int feast_profile(feast_handle h, int32_t enable) {
   if (!h) return FEAST_E_ARG;

@@ -32,7 +32,7 @@ ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, c
 # every symbol include/feast.h declares (checked by tests/test_abi.py)
 EXPORTS = ["feast_init", "feast_workspace_bytes", "feast_bind_workspace", "feast_nodes", "feast_project",
            "feast_project_left", "feast_project_bi", "feast_reduce", "feast_set_allreduce", "feast_iterate",
-           "feast_node_stats", "feast_last_launch_count", "feast_profile", "feast_profile_summary", "feast_last_error",
+           "feast_node_stats", "feast_factor_cache", "feast_last_launch_count", "feast_profile", "feast_profile_summary", "feast_last_error",
            "feast_version", "feast_destroy"]
 K_CLASSES = ["shift", "panel", "laswp", "trsm", "zgemm", "perm", "accum", "other"]
 
@@ -68,6 +68,7 @@ def load_library(path: str = LIB_PATH):
     lib.feast_node_stats.argtypes = [P, P, P]
     lib.feast_last_launch_count.argtypes = [P]
     lib.feast_last_launch_count.restype = I64
+    lib.feast_factor_cache.argtypes = [P, I32]
     lib.feast_profile.argtypes = [P, I32]
     lib.feast_profile_summary.argtypes = [P, I32, P, P, P, P]
     lib.feast_last_error.argtypes = [P]
@@ -261,6 +262,10 @@ class Feast:
         worst = ctypes.c_int32()
         self._check(self.lib.feast_node_stats(self.h, arr, ctypes.byref(worst)))
         return list(arr), worst.value
+
+    def factor_cache(self, enable: bool):
+        """Factor-once reuse across calls with the same A, B (NEXT-1); enable=True invalidates."""
+        self._check(self.lib.feast_factor_cache(self.h, int(bool(enable))))
 
     def profile(self, enable: bool):
         """Start (clears) / stop per-kernel-class CUDA-event timing of this library's launches."""

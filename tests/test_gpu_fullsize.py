@@ -15,6 +15,17 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-10
 
 
+@pytest.fixture(autouse=True)
+def _free_device_memory():
+    """Each full-size case needs most of the 180 GB: release the previous one's tensors."""
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+    yield
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
 def _rel(a, b):
     return float(torch.linalg.norm(a - b) / torch.linalg.norm(b))
 

@@ -67,3 +67,19 @@ def test_bifeast_shadow_converges():
     inside_true = P.lam[np.abs(P.lam - s.c) < s.r]
     assert c.sum() == len(inside_true) >= 1
     assert _match(np.asarray(out["lam"])[c], inside_true, 1e-10 * s.r)
+
+
+def test_c1_iterate_with_factor_cache_matches():
+    P = synth.make_pencil("C1")
+    s = P.spec
+    outs = []
+    for cache in (False, True):
+        f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, True)
+        f.factor_cache(cache)
+        A, X = dev(P.A), dev(P.X0)
+        for _ in range(s.iters):
+            out = f.iterate(A, None, X)
+        outs.append(out)
+    c0, c1 = _converged(outs[0]), _converged(outs[1])
+    assert c0.sum() == c1.sum() >= 1
+    assert _match(np.asarray(outs[0]["lam"])[c0], np.asarray(outs[1]["lam"])[c1], 1e-10 * s.r)

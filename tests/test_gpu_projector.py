@@ -157,3 +157,28 @@ def test_blocking_variants(monkeypatch, nbo, lookahead):
     Q, QL = f.project_bi(dev(P.A), dev(P.B), dev(P.X0), dev(P.X0))
     assert rel(host(Q), oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
     assert rel(host(QL), oracle.project(P.A, P.B, P.X0, z, w, left=True)) <= TOL
+
+
+def test_factor_cache_reuse():
+    """NEXT-1: with the factor cache on, a second projection with the same pencil
+    skips the shift + LU (fewer launches) and still matches the oracle for a new block."""
+    P = synth.make_pencil("C2", n=330, m0=20)
+    z, w = _oracle_nodes(P)
+    f = _handle(P, mode=fb.BI)
+    f.factor_cache(True)
+    A, B = dev(P.A), dev(P.B)
+    X1, X2 = P.X0, synth.random_block(P.n, P.m0, 99)
+    Q1 = f.project(A, B, dev(X1))
+    n_factor = f.last_launch_count
+    Q2 = f.project(A, B, dev(X2))
+    n_reuse = f.last_launch_count
+    assert n_reuse < n_factor / 2
+    assert rel(host(Q1), oracle.project(P.A, P.B, X1, z, w)) <= TOL
+    assert rel(host(Q2), oracle.project(P.A, P.B, X2, z, w)) <= TOL
+    QL = f.project_left(A, B, dev(X2))
+    assert rel(host(QL), oracle.project(P.A, P.B, X2, z, w, left=True)) <= TOL
+    # a different pencil (new A pointer) refactors
+    A2 = dev(P.A + 0.01 * np.eye(P.n))
+    Q3 = f.project(A2, B, dev(X2))
+    assert f.last_launch_count >= n_factor - 2
+    assert rel(host(Q3), oracle.project(P.A + 0.01 * np.eye(P.n), P.B, X2, z, w)) <= TOL
