@@ -34,16 +34,32 @@ namespace {
 
 constexpr int PT = 128;          // threads per CTA (one panel row each, S rows)
 constexpr int CSM = 16;          // max cluster size
-constexpr int WC = 8;            // chunk width (columns held in registers)
 constexpr int WMAX = 64;         // max panel width
-constexpr int SLOT_BYTES = (WC + 2) * 16;
 
+template <int WC>                 // WC = chunk width (columns held in registers)
 struct __align__(16) Slot {
   double2 row[WC];
-  double val;
-  long long idx;
-  double2 pinv;      // 1 / pivot, computed by the candidate's owner before the exchange
+  unsigned long long key;   // pivot key (see make_key); 0 = no candidate
+  unsigned long long pad;
+  double2 pinv;             // 1 / pivot, computed by the candidate's owner before the exchange
 };
+
+// Pivot key: the bits of |re|+|im| (>= 0, so the IEEE pattern orders like the value) with the low
+// 16 mantissa bits replaced by 0xFFFF - row: one unsigned 64-bit max picks the largest modulus
+// and, among candidates equal to 2^-36 relative, the lowest row (reading R7: near-ties may be
+// broken differently from the oracle; the solution Y_j agrees to kappa * u either way).
+__device__ __forceinline__ unsigned long long make_key(double v, int row) {
+  if (v < 0.0) return 0ull;
+  return ((unsigned long long)__double_as_longlong(v) & ~0xFFFFull) | (unsigned long long)(0xFFFF - row);
+}
+__device__ __forceinline__ int key_row(unsigned long long k) { return 0xFFFF - (int)(k & 0xFFFFull); }
+// warp-wide unsigned 64-bit max with two 32-bit REDUX operations
+__device__ __forceinline__ unsigned long long warp_max_key(unsigned long long k) {
+  const unsigned hi = (unsigned)(k >> 32), lo = (unsigned)k;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  return ((unsigned long long)mhi << 32) | mlo;
+}
 
 __device__ __forceinline__ bool better(double v, int i, double bv, int bi) {
   return v > bv || (v == bv && i < bi);
@@ -80,7 +96,7 @@ __device__ unsigned long long g_ptrace[512];
 #define PTRACE(i) do {} while (0)
 #endif
 
-template <int S>
+template <int S, int WC>
 __global__ void __launch_bounds__(PT, 1)
 panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__ ipiv_all,
                   double* __restrict__ stats_all, int32_t* __restrict__ info_all) {
@@ -98,12 +114,12 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
   const int PLD = Lc;   // column-major smem panel: P[c * PLD + r] (consecutive rows -> conflict-free)
 
   extern __shared__ __align__(128) double2 P[];  // [w][PLD]
-  __shared__ Slot slots[2][CSM];
+  constexpr int SLOT_BYTES = (WC + 2) * 16;
+  __shared__ Slot<WC> slots[2][CSM];
   __shared__ double2 L11s[WC][WC];               // chunk pivot rows' chunk values
   __shared__ __align__(16) double2 U12s[WC][WMAX];   // chunk pivot rows' rest-of-panel values
   __shared__ int pvt[WMAX];                      // pivot (panel row index) per column
-  __shared__ double wv[PT / 32];
-  __shared__ int wi[PT / 32];
+  __shared__ unsigned long long wkey[PT / 32];
   __shared__ double2 wrow[PT / 32][WC + 1];
   __shared__ __align__(8) unsigned long long mbar[4];   // slots[0], slots[1], U12s, load
   __shared__ int pos2row[WMAX], cur[WMAX];
@@ -159,17 +175,17 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
       const uint32_t bar = saddr(&mbar[buf]);
       PTRACE(8 + 4 * col);
       if (tid == 0) mbar_arm(bar, (uint32_t)(CS * SLOT_BYTES));
-      double bv = -1.0;
-      int bi = INT_MAX, bs = -1;
+      unsigned long long bk = 0ull;
+      int bs = -1;
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const int r = tid + s * PT;
         if (r < nrow && !used[s]) {
-          const double v = cabs1(a[s][jj]);
-          if (better(v, rbeg + r, bv, bi)) { bv = v; bi = rbeg + r; bs = s; }
+          const unsigned long long kk = make_key(cabs1(a[s][jj]), rbeg + r);
+          if (kk > bk) { bk = kk; bs = s; }
         }
       }
-      // every thread inverts its own candidate now, overlapping the division with the shuffles
+      // every thread inverts its own candidate now, overlapping the division with the reduction
       double2 myrcp = make_double2(0.0, 0.0);
 #pragma unroll
       for (int s = 0; s < S; ++s)
@@ -185,16 +201,9 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
             }
           }
         }
-      double wbv = bv;
-      int wbi = bi;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, wbv, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, wbi, off);
-        if (better(ov, oi, wbv, wbi)) { wbv = ov; wbi = oi; }
-      }
+      const unsigned long long wk = warp_max_key(bk);
       // the warp's winning lane stages its chunk row and 1/pivot; one barrier for the CTA step
-      if (wbv >= 0.0 && bi == wbi) {
+      if (wk != 0ull && bk == wk) {
 #pragma unroll
         for (int s = 0; s < S; ++s)
           if (s == bs) {
@@ -203,38 +212,30 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
             wrow[warp][WC] = myrcp;
           }
       }
-      if (lane == 0) { wv[warp] = wbv; wi[warp] = wbi; }
+      if (lane == 0) wkey[warp] = wk;
       __syncthreads();
-      double cv = wv[0];
-      int ci = wi[0], cw = 0;
+      unsigned long long ck = wkey[0];
+      int cw = 0;
 #pragma unroll
       for (int q = 1; q < PT / 32; ++q)
-        if (better(wv[q], wi[q], cv, ci)) { cv = wv[q]; ci = wi[q]; cw = q; }
-      // push {row[WC], (val, idx)} into slot [buf][crank] of every CTA (st.async -> its mbarrier)
+        if (wkey[q] > ck) { ck = wkey[q]; cw = q; }
+      // push {row[WC], key, 1/pivot} into slot [buf][crank] of every CTA (st.async -> its mbarrier)
       for (int t = tid; t < CS * (WC + 2); t += PT) {
-        const int dcta = t / (WC + 2), e = t % (WC + 2);
+        const int dcta = t / (WC + 2), e = t - dcta * (WC + 2);
         const uint32_t rslot = mapa(saddr(&slots[buf][crank]), dcta);
         const uint32_t rbar = mapa(bar, dcta);
         double2 v;
-        if (e < WC) v = cv >= 0.0 ? wrow[cw][e] : make_double2(0.0, 0.0);
-        else if (e == WC) v = make_double2(cv, __longlong_as_double((long long)(cv >= 0.0 ? ci : INT_MAX)));
-        else v = cv >= 0.0 ? wrow[cw][WC] : make_double2(0.0, 0.0);
+        if (e < WC) v = ck ? wrow[cw][e] : make_double2(0.0, 0.0);
+        else if (e == WC) v = make_double2(__longlong_as_double((long long)ck), 0.0);
+        else v = ck ? wrow[cw][WC] : make_double2(0.0, 0.0);
         st_async16(rslot + e * 16, v, rbar);
       }
-      PTRACE(9 + 4 * col);
       mbar_wait(bar, (uint32_t)((col >> 1) & 1));
-      PTRACE(10 + 4 * col);
-      // global pivot: lanes scan the CS slots, warp-shuffle argmax (every warp, same result)
-      double gv = -2.0;
-      int gi = INT_MAX, gb = 0;
-      if (lane < CS) { gv = slots[buf][lane].val; gi = (int)slots[buf][lane].idx; gb = lane; }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, gv, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, gi, off);
-        const int ob = __shfl_xor_sync(0xffffffffu, gb, off);
-        if (better(ov, oi, gv, gi)) { gv = ov; gi = oi; gb = ob; }
-      }
+      // global pivot: lanes read the CS keys, 64-bit max by REDUX (every warp, same result)
+      const unsigned long long lk = lane < CS ? slots[buf][lane].key : 0ull;
+      const unsigned long long gk = warp_max_key(lk);
+      const int gb = __ffs(__ballot_sync(0xffffffffu, lane < CS && lk == gk)) - 1;
+      const int gi = key_row(gk);
       const double2* prow = slots[buf][gb].row;
       if (tid < WC) L11s[jj][tid] = prow[tid];
       if (tid == 0) pvt[col] = gi;
@@ -283,7 +284,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
         const int pr = pvt[j0 + jj] - rbeg;
         if (pr >= 0 && pr < nrow) {
           for (int idx = tid; idx < rem * CS; idx += PT) {
-            const int c = idx % rem, dcta = idx / rem;
+            const int dcta = idx / rem, c = idx - dcta * rem;
             st_async16(mapa(saddr(&U12s[jj][c]), dcta), P[(c1 + c) * PLD + pr], mapa(ubar, dcta));
           }
         }
@@ -379,7 +380,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
   // st.async that this CTA waited for (the last column's slots), so it may exit.
 }
 
-template <int S>
+template <int S, int WC>
 void launch_s(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info, int batch, int cs,
               cudaStream_t s) {
   const int64_t L = n - k;
@@ -387,8 +388,8 @@ void launch_s(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* sta
   const size_t smem = (size_t)Lc * w * sizeof(double2);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(panel_smem_kernel<S>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(panel_smem_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(panel_smem_kernel<S, WC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(panel_smem_kernel<S, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -403,7 +404,7 @@ void launch_s(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* sta
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, panel_smem_kernel<S>, C, n, k, w, ipiv, stats, info);
+  cudaLaunchKernelEx(&cfg, panel_smem_kernel<S, WC>, C, n, k, w, ipiv, stats, info);
   count_launch();
 }
 
@@ -423,9 +424,9 @@ void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, do
   const double L_ = (double)(n - k);
   ProfScope ps_(K_PANEL, (double)batch * (4.0 * L_ * w * w - 4.0 * w * (double)w * w / 3.0), 0.0, s);
   const int64_t Lc = (n + cs - 1) / cs;
-  if (Lc <= PT) launch_s<1>(C, n, k, w, ipiv, stats, info, batch, cs, s);
-  else if (Lc <= 2 * PT) launch_s<2>(C, n, k, w, ipiv, stats, info, batch, cs, s);
-  else launch_s<4>(C, n, k, w, ipiv, stats, info, batch, cs, s);
+  if (Lc <= PT) launch_s<1, 8>(C, n, k, w, ipiv, stats, info, batch, cs, s);
+  else if (Lc <= 2 * PT) launch_s<2, 8>(C, n, k, w, ipiv, stats, info, batch, cs, s);
+  else launch_s<4, 8>(C, n, k, w, ipiv, stats, info, batch, cs, s);
 }
 
 }  // namespace feast
