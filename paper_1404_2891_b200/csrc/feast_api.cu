@@ -195,10 +195,11 @@ const double2* inv_ptr(feast_ctx* h, int64_t kb, int which) { return h->Inv + (k
 // to fill the GPU (the reduced matrices Q^H (A Q) are m0 x m0 with K = n).
 void gemm_gen(feast_ctx* h, int64_t M, int64_t N, int64_t K, bool conjA, const double2* A, int64_t lda,
               const double2* B, int64_t ldb, double2* C, int64_t ldc, double2 alpha, double2 beta) {
-  const int64_t tiles = ((M + 63) / 64) * ((N + 63) / 64);
+  // 32x32 CTA tiles, 3 resident per SM: fewer than 444 tiles leave the GPU under-filled
+  const int64_t tiles = ((M + 31) / 32) * ((N + 31) / 32);
   int splits = 1;
-  if (tiles < 296 && K >= 512 && h->SK) {
-    splits = (int)std::min<int64_t>((296 + tiles - 1) / tiles, K / 256);
+  if (tiles < 444 && K >= 512 && h->SK) {
+    splits = (int)std::min<int64_t>((444 + tiles - 1) / tiles, K / 256);
     while (splits > 1 && (int64_t)splits * M * N > h->sk_elems) --splits;
   }
   if (splits <= 1) {

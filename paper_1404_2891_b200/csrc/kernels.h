@@ -18,6 +18,8 @@ struct ZgemmArgs {
   int inplace = 0;                    // 1: C aliases B (requires M <= 64: one CTA row of tiles)
 };
 void zgemm_launch(const ZgemmArgs& p, bool conjA, int mode, cudaStream_t s);
+// tile-variant selection (tools/zgemm_lab): 0 = the launcher's heuristic
+void zgemm_launch_variant(const ZgemmArgs& p, bool conjA, int mode, int variant, cudaStream_t s);
 
 // ---------------------------------------------------------------- LU pieces
 // Batched matrices: matrix b at base + b*stride (complex elements), column-major, ld.

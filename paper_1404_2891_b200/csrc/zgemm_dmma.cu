@@ -5,21 +5,12 @@
 // tcgen05 has no f64 kind on sm_100a, so the tensor-core path for FP64 is mma.sync
 // m8n8k4.f64 (SASS DMMA.8x8x4), measured at 37.17 TF/s peak on B200 (profiles/r01_fp64_peak.md).
 //
-// Complex product by real embedding: with C' the m x 2n real matrix of interleaved (re,im)
-// columns and A' the m x 2k real matrix of interleaved A, C' = A' * Bh where Bh (2k x 2n) is
-// the real 2x2-block embedding of B: [Bre Bim; -Bim Bre] per complex entry.  One DMMA
-// (8x8x4 real) is then an 8(row) x 4(complex col) x 2(complex k) complex update with no
-// wasted multiplies: 8 m n k real flops per complex GEMM, the LAPACK ZGEMM count.
-// Fragment layout (PTX m8n8k4 .f64): lane = 4 g + t;  A[g][t], B[t][g], C[g][2t..2t+1].
-//  - A' fragment: complex A[g][k = t>>1], part t&1          (conj(A): negate part 1)
-//  - Bh fragment: complex B[k = t>>1][j = g>>1], part (t&1)^(g&1), negated iff t&1 && !(g&1)
-//  - C' fragment: complex C[g][j = t] (re, im) — each thread owns whole complex outputs.
-// Sign flips are an XOR on the high word (integer pipe), so the FP64 pipe only runs DMMA.
-// C -= A B (mode SUB) folds the minus sign into the same XOR mask.
-//
-// Tiling: CTA 64x64 complex outputs, 4 warps of 32x32, BK = 16 complex per stage,
-// 3-stage cp.async pipeline (108 KB smem -> 2 CTAs/SM).  Padded smem strides make every
-// fragment load bank-conflict free (A: ld 68 complex, B: ld 18 complex).
+// Tiling (measured, tools/zgemm_lab.cu, profiles/r01_zgemm_lab.md): CTA 32x32 complex outputs,
+// 4 warps of 16x16, BK = 16 complex per stage, 4-stage cp.async ring (76 KB smem, 3 CTAs and
+// 12 warps per SM).  The small CTA tile keeps more warps resident to hide shared-memory and L2
+// latency behind the DMMA pipe, and fills the 148 SMs even on the narrow updates of the LU
+// (N = 32..256).  In-place launches (C aliases B: the 64x64 diagonal-block inverses applied to
+// a block row) use 64x32 CTAs so one CTA row covers all M <= 64 rows it overwrites.
 #include "common.cuh"
 #include "kernels.h"
 #include "prof.h"
@@ -27,16 +18,7 @@
 namespace feast {
 namespace {
 
-constexpr int BK = 16, STAGES = 3;
-constexpr int LDB_S = BK + 2;   // Bs[n][k]
-template <int BM, int BN>
-struct Tile {
-  static constexpr int THREADS = 32 * (BM / 32) * (BN / 32);
-  static constexpr int LDA_S = BM + 4;   // As[k][m]
-  static constexpr int A_STAGE = BK * LDA_S;
-  static constexpr int B_STAGE = BN * LDB_S;
-  static constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double2);
-};
+constexpr int BK = 16;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -47,24 +29,44 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-__device__ __forceinline__ double xor_sign(double v, unsigned long long m) {
-  return __longlong_as_double(__double_as_longlong(v) ^ m);
-}
-
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
 
-template <int BM, int BN, bool CONJA, int MODE>
-__global__ void __launch_bounds__(Tile<BM, BN>::THREADS, 2) zgemm_dmma_kernel(ZgemmArgs p) {
-  constexpr int THREADS = Tile<BM, BN>::THREADS, LDA_S = Tile<BM, BN>::LDA_S;
-  constexpr int A_STAGE = Tile<BM, BN>::A_STAGE, B_STAGE = Tile<BM, BN>::B_STAGE;
-  constexpr int WN = BN / 32;   // warps along N
+// PLANAR complex product — four real DMMAs per complex 8x8x4 block with separate real and
+// imaginary accumulators:  Re += ar br - ai bi,  Im += ar bi + ai br  (conj(A): ai -> -ai;
+// C -= AB: every product negated).  All sign changes are warp-uniform, so ptxas folds them
+// into the DMMA operand modifiers (no integer sign flips), and each lane's A (B) fragment is
+// one whole complex element: a single 16-byte LDS.128 per fragment.
+//   A fragment (row g, k t) = A[m0 + g][k0 + t];  B fragment (k t, col g) = B[k0 + t][n0 + g]
+//   accumulators: C[g][2t + i], i = 0, 1 (re and im in separate registers).
+// Shared layout: As[k][m] with ld BM + 2 (quarter-warp rows 32 B apart: conflict-free 128-bit
+// loads), Bs[n][k] with ld BK + 4.
+template <int BM, int BN, int WGM, int WGN, int ST>
+struct Tile {
+  static constexpr int THREADS = 32 * WGM * WGN;
+  static constexpr int TM = BM / WGM, TN = BN / WGN;
+  static constexpr int MI = TM / 8, NJ = TN / 8;
+  static constexpr int LDA_S = BM + 2, LDB_S = BK + 4;
+  static constexpr int A_STAGE = BK * LDA_S;
+  static constexpr int B_STAGE = BN * LDB_S;
+  static constexpr size_t SMEM_BYTES = (size_t)ST * (A_STAGE + B_STAGE) * sizeof(double2);
+};
+
+template <int BM, int BN, int WGM, int WGN, int ST, int MINB, bool CONJA, int MODE>
+__global__ void __launch_bounds__(32 * WGM * WGN, MINB) zgemm_dmma_kernel(ZgemmArgs p) {
+  using T = Tile<BM, BN, WGM, WGN, ST>;
+  constexpr int THREADS = T::THREADS, LDA_S = T::LDA_S, LDB3 = T::LDB_S, A_STAGE = T::A_STAGE,
+                B_STAGE = T::B_STAGE;
+  constexpr int MI = T::MI, NJ = T::NJ;
+  constexpr int LA = (BM * BK) / THREADS, LB = (BN * BK) / THREADS;
+  static_assert(MI >= 1 && NJ >= 1 && LA >= 1 && LB >= 1, "tile");
+  static_assert(THREADS % BM == 0 && THREADS % BK == 0, "load mapping");
   extern __shared__ __align__(128) double2 smem[];
   double2* As = smem;
-  double2* Bs = smem + STAGES * A_STAGE;
+  double2* Bs = smem + ST * A_STAGE;
 
   const int64_t z = blockIdx.z;
   const double2* __restrict__ A = p.A + z * p.sA;
@@ -73,151 +75,202 @@ __global__ void __launch_bounds__(Tile<BM, BN>::THREADS, 2) zgemm_dmma_kernel(Zg
   const int64_t M = p.M, N = p.N, K = p.K;
   const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wm = (warp / WN) * 32, wn = (warp % WN) * 32;
+  const int wm = (warp / WGN) * T::TM, wn = (warp % WGN) * T::TN;
   const int g = lane >> 2, t = lane & 3;
 
-  auto load_tile = [&](int stage, int64_t kt) {
-    const int64_t k0 = kt * BK;
-    double2* as = As + stage * A_STAGE;
-    double2* bs = Bs + stage * B_STAGE;
+  // ---- global -> shared mapping (fixed per thread; only the k-tile base advances)
+  //  A (op = N):  m = tid % BM, k = tid / BM + i * (THREADS / BM)
+  //  A (op = C):  k = tid % BK, m = tid / BK + i * (THREADS / BK)     (A^H read as rows of A)
+  //  B:           k = tid % BK, n = tid / BK + i * (THREADS / BK)
+  const int a_m = CONJA ? tid / BK : tid % BM, a_k = CONJA ? tid % BK : tid / BM;
+  constexpr int A_DI = CONJA ? THREADS / BK : THREADS / BM;   // step of the varying index
+  const int b_k = tid % BK, b_n = tid / BK;
+  constexpr int B_DI = THREADS / BK;
+  const double2* a_src = CONJA ? A + (m0 + a_m) * p.lda + a_k : A + (m0 + a_m) + (int64_t)a_k * p.lda;
+  const int64_t a_step = CONJA ? (int64_t)A_DI * p.lda : (int64_t)A_DI * p.lda;   // per i
+  const int64_t a_kt = CONJA ? BK : (int64_t)BK * p.lda;                          // per k-tile
+  const double2* b_src = B + (n0 + b_n) * p.ldb + b_k;
+  const int64_t b_step = (int64_t)B_DI * p.ldb;
+  unsigned a_ok = 0, b_ok = 0;   // bit i: row / column in range
 #pragma unroll
-    for (int i = 0; i < (BM * BK) / THREADS; ++i) {
-      const int idx = tid + i * THREADS;
-      int m, k;
-      if (!CONJA) { m = idx & (BM - 1); k = idx / BM; }   // A[m][k] at m + k lda
-      else { k = idx & (BK - 1); m = idx / BK; }          // Ag[k][m] at k + m lda
-      const int64_t gm = m0 + m, gk = k0 + k;
-      const bool pred = gm < M && gk < K;
-      const double2* src = pred ? (CONJA ? A + gk + gm * p.lda : A + gm + gk * p.lda) : A;
-      cp_async16(&as[k * LDA_S + m], src, pred);
+  for (int i = 0; i < LA; ++i)
+    if (CONJA ? (m0 + a_m + i * A_DI < M) : (m0 + a_m < M)) a_ok |= 1u << i;
+#pragma unroll
+  for (int i = 0; i < LB; ++i)
+    if (n0 + b_n + i * B_DI < N) b_ok |= 1u << i;
+  const uint32_t as_dst = (uint32_t)__cvta_generic_to_shared(As + a_k * LDA_S + a_m);
+  const uint32_t bs_dst = (uint32_t)__cvta_generic_to_shared(Bs + b_n * LDB3 + b_k);
+  constexpr uint32_t A_DST_STEP = (CONJA ? A_DI : A_DI * LDA_S) * 16;
+  constexpr uint32_t B_DST_STEP = B_DI * LDB3 * 16;
+
+  auto load_tile = [&](int stage, int kt) {
+    const int64_t k0 = (int64_t)kt * BK;
+    const double2* as = a_src + kt * a_kt;
+    const double2* bs = b_src + k0;
+    const uint32_t ad = as_dst + stage * (A_STAGE * 16), bd = bs_dst + stage * (B_STAGE * 16);
+#pragma unroll
+    for (int i = 0; i < LA; ++i) {
+      const bool kin = CONJA ? (k0 + a_k < K) : (k0 + a_k + i * A_DI < K);
+      const bool pred = ((a_ok >> i) & 1u) && kin;
+      const int sz = pred ? 16 : 0;
+      const double2* src = pred ? as + i * a_step : A;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(ad + i * A_DST_STEP), "l"(src), "r"(sz));
     }
 #pragma unroll
-    for (int i = 0; i < (BN * BK) / THREADS; ++i) {
-      const int idx = tid + i * THREADS;
-      const int k = idx & (BK - 1), n = idx / BK;
-      const int64_t gn = n0 + n, gk = k0 + k;
-      const bool pred = gn < N && gk < K;
-      const double2* src = pred ? B + gk + gn * p.ldb : B;
-      cp_async16(&bs[n * LDB_S + k], src, pred);
+    for (int i = 0; i < LB; ++i) {
+      const bool pred = ((b_ok >> i) & 1u) && (k0 + b_k < K);
+      const int sz = pred ? 16 : 0;
+      const double2* src = pred ? bs + i * b_step : B;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(bd + i * B_DST_STEP), "l"(src), "r"(sz));
     }
   };
 
-  const int64_t KT = (K + BK - 1) / BK;
+  const int KT = (int)((K + BK - 1) / BK);
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
+  for (int s = 0; s < ST; ++s) {
     if (s < KT) load_tile(s, s);
     cp_commit();
   }
 
-  double acc[4][8][2];
-  if (MODE == ZG_SUB) {
+  // accumulators start at zero; C (SUB: C_old, GEN: beta C_old) joins in the epilogue.  In SUB
+  // mode C_old is prefetched into registers here, so its latency overlaps the pipeline fill and
+  // no DMMA waits on it.
+  double cre[MI][NJ][2], cim[MI][NJ][2];
+  double2 cold[MODE == ZG_SUB ? MI : 1][MODE == ZG_SUB ? NJ : 1][2];
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 8; ++ni) {
-        const int64_t r = m0 + wm + mi * 8 + g, c = n0 + wn + ni * 4 + t;
-        double2 v = make_double2(0.0, 0.0);
-        if (r < M && c < N) v = C[r + c * p.ldc];
-        acc[mi][ni][0] = v.x;
-        acc[mi][ni][1] = v.y;
+    for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        cre[mi][nj][i] = cim[mi][nj][i] = 0.0;
+        if (MODE == ZG_SUB) {
+          const int64_t r = m0 + wm + mi * 8 + g, c = n0 + wn + nj * 8 + 2 * t + i;
+          cold[mi][nj][i] = (r < M && c < N) ? C[r + c * p.ldc] : make_double2(0.0, 0.0);
+        }
       }
-  } else {
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 8; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-  }
 
-  const unsigned long long SIGN = 0x8000000000000000ULL;
-  const unsigned long long signA = (CONJA && (t & 1)) ? SIGN : 0ULL;
-  bool negB = (t & 1) && !(g & 1);
-  if (MODE == ZG_SUB) negB = !negB;
-  const unsigned long long signB = negB ? SIGN : 0ULL;
-  const int partA = t & 1;
-  const int partB = (t & 1) ^ (g & 1);
-  const int kA = t >> 1;
+  const int offA = t * LDA_S + wm + g;          // complex offsets inside a stage
+  const int offB = (wn + g) * LDB3 + t;
+  double2 af[2][MI], bf[2][NJ];
+  auto load_frags = [&](int fb, int stage, int ks) {   // ks: complex k offset (multiple of 4)
+    const double2* as = As + stage * A_STAGE + offA + ks * LDA_S;
+    const double2* bs = Bs + stage * B_STAGE + offB + ks;
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) af[fb][mi] = as[mi * 8];
+#pragma unroll
+    for (int nj = 0; nj < NJ; ++nj) bf[fb][nj] = bs[nj * 8 * LDB3];
+  };
+  constexpr double SA = MODE == ZG_SUB ? -1.0 : 1.0;     // sign of every product
+  constexpr double SI = CONJA ? -1.0 : 1.0;             // sign of ai
 
-  for (int64_t kt = 0; kt < KT; ++kt) {
-    cp_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      const int64_t nk = kt + STAGES - 1;
-      if (nk < KT) load_tile((int)(nk % STAGES), nk);
-      cp_commit();
+  cp_wait<ST - 1>();
+  __syncthreads();
+  load_frags(0, 0, 0);
+  int cur = 0;
+  for (int kt = 0; kt < KT; ++kt) {
+    const int nxt = cur + 1 == ST ? 0 : cur + 1;
+#pragma unroll
+    for (int k4 = 0; k4 < BK / 4; ++k4) {
+      const int fb = k4 & 1;
+      if (k4 == BK / 4 - 1) {
+        cp_wait<ST - 2>();
+        __syncthreads();                            // every warp is done reading buffer `cur`
+        if (kt + ST < KT) load_tile(cur, kt + ST);
+        cp_commit();
+        if (kt + 1 < KT) load_frags(fb ^ 1, nxt, 0);
+      } else {
+        load_frags(fb ^ 1, cur, 4 * (k4 + 1));
+      }
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi) {
+        const double ar = SA * af[fb][mi].x, ai = SA * SI * af[fb][mi].y;
+#pragma unroll
+        for (int nj = 0; nj < NJ; ++nj) {
+          dmma(cre[mi][nj][0], cre[mi][nj][1], ar, bf[fb][nj].x);
+          dmma(cim[mi][nj][0], cim[mi][nj][1], ar, bf[fb][nj].y);
+        }
+#pragma unroll
+        for (int nj = 0; nj < NJ; ++nj) {
+          dmma(cre[mi][nj][0], cre[mi][nj][1], -ai, bf[fb][nj].y);
+          dmma(cim[mi][nj][0], cim[mi][nj][1], ai, bf[fb][nj].x);
+        }
+      }
     }
-    const double* as = reinterpret_cast<const double*>(As + (kt % STAGES) * A_STAGE);
-    const double* bs = reinterpret_cast<const double*>(Bs + (kt % STAGES) * B_STAGE);
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 2) {
-      double af[4], bf[8];
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-        af[mi] = xor_sign(as[2 * ((kk + kA) * LDA_S + wm + mi * 8 + g) + partA], signA);
-#pragma unroll
-      for (int ni = 0; ni < 8; ++ni)
-        bf[ni] = xor_sign(bs[2 * ((wn + ni * 4 + (g >> 1)) * LDB_S + kk + kA) + partB], signB);
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 8; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
-    }
+    cur = nxt;
   }
   cp_wait<0>();
 
-  // epilogue
+  const bool use_beta = MODE == ZG_GEN && (p.beta.x != 0.0 || p.beta.y != 0.0);
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 8; ++ni) {
-      const int64_t r = m0 + wm + mi * 8 + g, c = n0 + wn + ni * 4 + t;
-      if (r < M && c < N) {
-        double2 v = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
-        if (MODE == ZG_GEN) {
-          v = cmul(p.alpha, v);
-          if (p.beta.x != 0.0 || p.beta.y != 0.0) v = cadd(v, cmul(p.beta, C[r + c * p.ldc]));
+    for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int64_t r = m0 + wm + mi * 8 + g, c = n0 + wn + nj * 8 + 2 * t + i;
+        if (r < M && c < N) {
+          double2* cp = C + r + c * p.ldc;
+          double2 v = make_double2(cre[mi][nj][i], cim[mi][nj][i]);
+          if (MODE == ZG_SUB) {
+            v = cadd(cold[MODE == ZG_SUB ? mi : 0][MODE == ZG_SUB ? nj : 0][i], v);
+          } else {
+            v = cmul(p.alpha, v);
+            if (use_beta) v = cadd(v, cmul(p.beta, *cp));
+          }
+          *cp = v;
         }
-        C[r + c * p.ldc] = v;
       }
-    }
 }
-
-template <int BM, int BN, bool CONJA, int MODE>
-void launch_tile(const ZgemmArgs& p, cudaStream_t s) {
+template <int BM, int BN, int WGM, int WGN, int ST, int MINB, bool CONJA, int MODE>
+void launch3(const ZgemmArgs& p, cudaStream_t s) {
+  using T = Tile<BM, BN, WGM, WGN, ST>;
+  auto kern = zgemm_dmma_kernel<BM, BN, WGM, WGN, ST, MINB, CONJA, MODE>;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(zgemm_dmma_kernel<BM, BN, CONJA, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Tile<BM, BN>::SMEM_BYTES);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_BYTES);
     configured = true;
   }
   dim3 grid((unsigned)((p.N + BN - 1) / BN), (unsigned)((p.M + BM - 1) / BM), (unsigned)p.batch);
-  zgemm_dmma_kernel<BM, BN, CONJA, MODE><<<grid, Tile<BM, BN>::THREADS, Tile<BM, BN>::SMEM_BYTES, s>>>(p);
+  kern<<<grid, T::THREADS, T::SMEM_BYTES, s>>>(p);
   count_launch();
 }
 
-// Tile choice: 64x64 CTAs (4 warps) normally; 32x32 CTAs (1 warp) when the 64x64 grid would not
-// fill the 148 SMs twice over (small, latency-bound launches: diagonal-block applications,
-// in-block updates, the substitution updates of late blocks).
+
 template <bool CONJA, int MODE>
 void launch_t(const ZgemmArgs& p, cudaStream_t s) {
   ProfScope ps_(K_ZGEMM, 8.0 * (double)p.M * (double)p.N * (double)p.K * p.batch, 0.0, s);
-  const int64_t big = ((p.M + 63) / 64) * ((p.N + 63) / 64) * p.batch;
-  if (p.inplace) {   // every CTA must read its whole B column block before writing it: BM >= M
-    if (big < 296) launch_tile<64, 32, CONJA, MODE>(p, s);
-    else launch_tile<64, 64, CONJA, MODE>(p, s);
-  } else if (big < 296) {
-    launch_tile<32, 32, CONJA, MODE>(p, s);
-  } else {
-    launch_tile<64, 64, CONJA, MODE>(p, s);
+  if (p.inplace) launch3<64, 32, 2, 2, 4, 2, CONJA, MODE>(p, s);   // BM >= M: one CTA row
+  else launch3<32, 32, 2, 2, 4, 3, CONJA, MODE>(p, s);
+}
+
+// tile variants kept for tools/zgemm_lab (0 = the production choice above)
+template <bool CONJA, int MODE>
+void launch_variant(const ZgemmArgs& p, int v, cudaStream_t s) {
+  switch (v) {
+    case 1: launch3<64, 64, 2, 2, 3, 2, CONJA, MODE>(p, s); break;
+    case 2: launch3<64, 32, 2, 2, 4, 2, CONJA, MODE>(p, s); break;
+    case 3: launch3<32, 32, 2, 2, 3, 4, CONJA, MODE>(p, s); break;
+    case 4: launch3<128, 64, 4, 2, 3, 1, CONJA, MODE>(p, s); break;
+    case 5: launch3<32, 64, 2, 2, 4, 2, CONJA, MODE>(p, s); break;
+    default: launch_t<CONJA, MODE>(p, s); break;
   }
 }
 
 }  // namespace
 
+void zgemm_launch_variant(const ZgemmArgs& p, bool conjA, int mode, int variant, cudaStream_t s) {
+  if (p.M <= 0 || p.N <= 0 || p.batch <= 0) return;
+  if (conjA) {
+    if (mode == ZG_SUB) launch_variant<true, ZG_SUB>(p, variant, s); else launch_variant<true, ZG_GEN>(p, variant, s);
+  } else {
+    if (mode == ZG_SUB) launch_variant<false, ZG_SUB>(p, variant, s); else launch_variant<false, ZG_GEN>(p, variant, s);
+  }
+}
+
 void zgemm_launch(const ZgemmArgs& p, bool conjA, int mode, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.batch <= 0) return;
-  if (p.K <= 0) {
-    if (mode == ZG_SUB) return;  // C -= 0
-  }
+  if (p.K <= 0 && mode == ZG_SUB) return;  // C -= 0
   if (conjA) {
     if (mode == ZG_SUB) launch_t<true, ZG_SUB>(p, s); else launch_t<true, ZG_GEN>(p, s);
   } else {
