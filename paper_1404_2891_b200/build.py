@@ -59,7 +59,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 print(f"== {os.path.basename(src)}\n{log}", file=sys.stderr)
     if force or jobs or _stale(LIB, objs):
         tmp = LIB + f".tmp{os.getpid()}"
-        cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L/usr/local/cuda/lib64", "-lcusolver", "-lcublas",
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", tmp, *objs, "-L/usr/local/cuda/lib64", "-lcusolver",
+               "-lcublas",
                "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

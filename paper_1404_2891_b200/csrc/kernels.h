@@ -45,6 +45,7 @@ void laswp_launch(Batched C, int64_t n, int64_t k, int cnt, const int32_t* ipiv,
                   cudaStream_t s);
 // Cluster panel with the panel resident in shared memory (rows never moved; see panel_smem.cu).
 bool panel_smem_fits(int64_t n, int w, int cs);
+int panel_smem_max_clusters(int64_t L, int w, int cs);
 void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info, int batch,
                        int cs, cudaStream_t s);
 

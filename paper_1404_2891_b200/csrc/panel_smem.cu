@@ -111,9 +111,12 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
   const int Lc = (L + CS - 1) / CS;
   const int rbeg = crank * Lc;
   const int nrow = max(0, min(L, rbeg + Lc) - rbeg);
-  const int PLD = Lc;   // column-major smem panel: P[c * PLD + r] (consecutive rows -> conflict-free)
+  const int PLD = Lc;   // column-major smem panel: P[(c - WC) * PLD + r] (consecutive rows -> conflict-free)
 
-  extern __shared__ __align__(128) double2 P[];  // [w][PLD]
+  // Shared memory holds only the panel columns [WC, w): the first chunk lives in registers from
+  // the start, and every finished chunk is stored straight from registers to global memory, so
+  // the footprint (and the number of co-resident clusters) is set by w - WC columns.
+  extern __shared__ __align__(128) double2 P[];  // [w - WC][PLD]
   constexpr int SLOT_BYTES = (WC + 2) * 16;
   __shared__ Slot<WC> slots[2][CSM];
   __shared__ double2 L11s[WC][WC];               // chunk pivot rows' chunk values
@@ -139,33 +142,47 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (nrow > 0) {
-    if (tid == 0) mbar_arm(lbar, (uint32_t)(w * nrow * 16));
-    for (int c = tid; c < w; c += PT) {
+  const bool tma = nrow > 0 && w > WC;
+  if (tma) {
+    if (tid == 0) mbar_arm(lbar, (uint32_t)((w - WC) * nrow * 16));
+    for (int c = WC + tid; c < w; c += PT) {
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                   ::"r"(saddr(P + c * PLD)), "l"(C + rbeg + c * ld), "r"(nrow * 16), "r"(lbar) : "memory");
+                   ::"r"(saddr(P + (c - WC) * PLD)), "l"(C + rbeg + c * ld), "r"(nrow * 16), "r"(lbar) : "memory");
+    }
+  }
+  // first chunk: straight from global into registers (coalesced: consecutive threads, rows)
+  double2 a[S][WC];
+  {
+    const int wc0 = min(WC, w);
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int r = tid + s * PT;
+#pragma unroll
+      for (int jj = 0; jj < WC; ++jj)
+        a[s][jj] = (r < nrow && jj < wc0) ? C[rbeg + r + (int64_t)jj * ld] : make_double2(0.0, 0.0);
     }
   }
   cluster.sync();   // mbarrier inits visible cluster-wide before any remote st.async
-  if (nrow > 0) mbar_wait(lbar, 0);
+  if (tma) mbar_wait(lbar, 0);
   PTRACE(1);
 
   bool used[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) used[s] = false;
-  double2 a[S][WC];
   double pmin = DBL_MAX, pmax = 0.0;
   int info = 0;
   int chunk = 0;
 
   for (int j0 = 0; j0 < w; j0 += WC, ++chunk) {
     const int wc = min(WC, w - j0);
+    if (j0 > 0) {
 #pragma unroll
-    for (int s = 0; s < S; ++s) {
-      const int r = tid + s * PT;
+      for (int s = 0; s < S; ++s) {
+        const int r = tid + s * PT;
 #pragma unroll
-      for (int jj = 0; jj < WC; ++jj)
-        a[s][jj] = (r < nrow && jj < wc) ? P[(j0 + jj) * PLD + r] : make_double2(0.0, 0.0);
+        for (int jj = 0; jj < WC; ++jj)
+          a[s][jj] = (r < nrow && jj < wc) ? P[(j0 - WC + jj) * PLD + r] : make_double2(0.0, 0.0);
+      }
     }
 #pragma unroll
     for (int jj = 0; jj < WC; ++jj) {
@@ -219,6 +236,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
 #pragma unroll
       for (int q = 1; q < PT / 32; ++q)
         if (wkey[q] > ck) { ck = wkey[q]; cw = q; }
+      PTRACE(9 + 4 * col);
       // push {row[WC], key, 1/pivot} into slot [buf][crank] of every CTA (st.async -> its mbarrier)
       for (int t = tid; t < CS * (WC + 2); t += PT) {
         const int dcta = t / (WC + 2), e = t - dcta * (WC + 2);
@@ -231,6 +249,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
         st_async16(rslot + e * 16, v, rbar);
       }
       mbar_wait(bar, (uint32_t)((col >> 1) & 1));
+      PTRACE(10 + 4 * col);
       // global pivot: lanes read the CS keys, 64-bit max by REDUX (every warp, same result)
       const unsigned long long lk = lane < CS ? slots[buf][lane].key : 0ull;
       const unsigned long long gk = warp_max_key(lk);
@@ -263,14 +282,14 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
         if (pzero && !info) info = (int)(k + col + 1);
       }
     }
-    // ---- chunk done: registers back to smem
+    // ---- chunk done: its columns are final (L multipliers; U for the pivot rows) -> global
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int r = tid + s * PT;
       if (r < nrow) {
 #pragma unroll
         for (int jj = 0; jj < WC; ++jj)
-          if (jj < wc) P[(j0 + jj) * PLD + r] = a[s][jj];
+          if (jj < wc) C[rbeg + r + (int64_t)(j0 + jj) * ld] = a[s][jj];
       }
     }
     const int c1 = j0 + wc;
@@ -285,7 +304,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
         if (pr >= 0 && pr < nrow) {
           for (int idx = tid; idx < rem * CS; idx += PT) {
             const int dcta = idx / rem, c = idx - dcta * rem;
-            st_async16(mapa(saddr(&U12s[jj][c]), dcta), P[(c1 + c) * PLD + pr], mapa(ubar, dcta));
+            st_async16(mapa(saddr(&U12s[jj][c]), dcta), P[(c1 - WC + c) * PLD + pr], mapa(ubar, dcta));
           }
         }
       }
@@ -312,13 +331,13 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
       for (int jj = 0; jj < wc; ++jj) {
         const int pr = pvt[j0 + jj] - rbeg;
         if (pr >= 0 && pr < nrow)
-          for (int c = tid; c < rem; c += PT) P[(c1 + c) * PLD + pr] = U12s[jj][c];
+          for (int c = tid; c < rem; c += PT) P[(c1 - WC + c) * PLD + pr] = U12s[jj][c];
       }
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const int r = tid + s * PT;
         if (r < nrow && !used[s]) {
-          double2* colp = P + c1 * PLD + r;
+          double2* colp = P + (c1 - WC) * PLD + r;
           int c = 0;
           for (; c + 4 <= rem; c += 4) {
             double2 v0 = colp[(c + 0) * PLD], v1 = colp[(c + 1) * PLD], v2 = colp[(c + 2) * PLD], v3 = colp[(c + 3) * PLD];
@@ -347,15 +366,6 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
     }
   }
   PTRACE(2);
-  // ---- store own rows back (physical order): bulk (TMA) shared -> global per column
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncthreads();
-  if (nrow > 0) {
-    for (int c = tid; c < w; c += PT)
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                   ::"l"(C + rbeg + c * ld), "r"(saddr(P + c * PLD)), "r"(nrow * 16) : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  }
   // ---- LAPACK ipiv from the pivot sequence (rows / positions relative to k)
   if (crank == 0 && tid == 0) {
     for (int i = 0; i < w; ++i) { pos2row[i] = i; cur[i] = i; }
@@ -374,7 +384,6 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
     stats_all[2 * b + 1] = fmax(stats_all[2 * b + 1], sqrt(pmax));
     if (info && !info_all[b]) info_all[b] = info;
   }
-  if (nrow > 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   PTRACE(3);
   // No trailing cluster barrier: every remote write into this CTA's shared memory was a
   // st.async that this CTA waited for (the last column's slots), so it may exit.
@@ -385,7 +394,7 @@ void launch_s(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* sta
               cudaStream_t s) {
   const int64_t L = n - k;
   const int Lc = (int)((L + cs - 1) / cs);
-  const size_t smem = (size_t)Lc * w * sizeof(double2);
+  const size_t smem = (size_t)Lc * (w > WC ? w - WC : 0) * sizeof(double2);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(panel_smem_kernel<S, WC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -414,9 +423,34 @@ void launch_s(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* sta
 void panel_trace_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_ptrace, sizeof(g_ptrace)); }
 #endif
 
+// Diagnostics: how many clusters of `cs` CTAs with the panel of L rows x w columns can be
+// co-resident (cudaOccupancyMaxActiveClusters); decides whether a batch needs several waves.
+int panel_smem_max_clusters(int64_t L, int w, int cs) {
+  const int Lc = (int)((L + cs - 1) / cs);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(16 * cs), 1, 1);
+  cfg.blockDim = dim3(PT, 1, 1);
+  const int wc = 8;
+  cfg.dynamicSmemBytes = (size_t)Lc * (w > wc ? w - wc : 0) * sizeof(double2);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nc = -1;
+  auto k = Lc <= PT ? panel_smem_kernel<1, 8> : (Lc <= 2 * PT ? panel_smem_kernel<2, 8> : panel_smem_kernel<4, 8>);
+  cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (cudaOccupancyMaxActiveClusters(&nc, k, &cfg) != cudaSuccess) { cudaGetLastError(); return -1; }
+  return nc;
+}
+
 bool panel_smem_fits(int64_t n, int w, int cs) {
   const int64_t Lc = (n + cs - 1) / cs;
-  return w <= WMAX && (size_t)Lc * w * sizeof(double2) <= 190 * 1024 && Lc <= 4 * PT;
+  const int wc = 8;   // register chunk width (see panel_smem_launch)
+  return w <= WMAX && (size_t)Lc * (w > wc ? w - wc : 0) * sizeof(double2) <= 190 * 1024 && Lc <= 4 * PT;
 }
 
 void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info, int batch,
@@ -424,6 +458,7 @@ void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, do
   const double L_ = (double)(n - k);
   ProfScope ps_(K_PANEL, (double)batch * (4.0 * L_ * w * w - 4.0 * w * (double)w * w / 3.0), 0.0, s);
   const int64_t Lc = (n + cs - 1) / cs;
+  // register chunk: 8 columns (a 16-column chunk spills at 2 rows per thread)
   if (Lc <= PT) launch_s<1, 8>(C, n, k, w, ipiv, stats, info, batch, cs, s);
   else if (Lc <= 2 * PT) launch_s<2, 8>(C, n, k, w, ipiv, stats, info, batch, cs, s);
   else launch_s<4, 8>(C, n, k, w, ipiv, stats, info, batch, cs, s);
