@@ -21,8 +21,12 @@
  *     torch.complex128 / cuDoubleComplex / C99 double _Complex.  "ld" is the leading
  *     dimension in complex elements, ld >= n (or >= m0 for m0 x m0 matrices).
  *   - Matrix arguments are DEVICE pointers (16-byte aligned), unless marked (host).
- *   - All device work is enqueued on the handle's CUDA stream; every call returns after
- *     synchronising that stream (host outputs are valid on return).
+ *   - Streams: every call is ordered after the work already enqueued on the stream given to
+ *     feast_init (the caller's stream) and before anything enqueued there afterwards.  The
+ *     library runs its kernels on its own stream (forked from / joined to the caller's with
+ *     events) so that a repeated projector call can be captured once into a CUDA graph and
+ *     replayed (2nd identical call captured, later ones replayed; FEAST_GRAPH=0 disables).
+ *     Calls return after synchronising the library stream (host outputs valid on return).
  *   - The caller owns every matrix and the workspace; the library never frees caller memory.
  *   - Return value: 0 = ok, < 0 = error (result not valid), > 0 = warning (result valid).
  *     No exception or exit() crosses the ABI; feast_last_error() has the message.
@@ -124,7 +128,8 @@ int feast_reduce(feast_handle h, const void* A, int64_t lda, const void* B, int6
                  void* Ahat, int64_t ldah, void* Bhat, int64_t ldbh);
 
 /* All-reduce callback for world > 1: sum `count` float64 values at device pointer `buf`
- * across ranks, in place, ordered on `cuda_stream`; return 0 on success. */
+ * across ranks, in place, ordered on `cuda_stream` (the library's stream: the callback must
+ * enqueue its collective there, or complete it before returning); return 0 on success. */
 typedef int (*feast_allreduce_fn)(void* buf, int64_t count, void* cuda_stream, void* user);
 int feast_set_allreduce(feast_handle h, feast_allreduce_fn fn, void* user);
 
@@ -168,6 +173,12 @@ enum { FEAST_K_SHIFT = 0, FEAST_K_PANEL = 1, FEAST_K_LASWP = 2, FEAST_K_TRSM = 3
 int feast_profile(feast_handle h, int32_t enable);
 int feast_profile_summary(feast_handle h, int32_t kclass, int64_t* launches, double* ms, double* flops,
                           double* bytes);
+/* The recorded launches one by one (a timeline; tools/timeline.py): class, stream (0 = the
+ * handle's stream, 1 = its lookahead side stream), start / end in ms relative to the first
+ * record's start, algorithmic flops.  Host arrays of max_records entries (any may be NULL);
+ * *count = number of records.  Synchronises the device. */
+int feast_profile_records(feast_handle h, int64_t max_records, int32_t* kclass, int32_t* stream, double* t0_ms,
+                          double* t1_ms, double* flops, int64_t* count);
 
 /* Message for the last error on this handle ("" if none).  Valid until the next call. */
 const char* feast_last_error(feast_handle h);

@@ -31,7 +31,10 @@ struct feast_ctx {
   bool b_id = true;
   int rank = 0, world = 1, q = 0, j0 = 0, j1 = 0, batch = 1;
   std::vector<double2> z, w;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;      // the library's own stream (capturable into CUDA graphs)
+  cudaStream_t caller = nullptr;      // the caller's stream: every call is ordered after / before it
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  bool own_stream = false;
   int nb = 64;
   feast::PanelCfg pcfg{};
   int smem_cs = 0;   // cluster size of the shared-memory panel kernel (0: register-chunk kernel)
@@ -70,6 +73,21 @@ struct feast_ctx {
     size_t sw_bytes;
     std::vector<char> hw;
   } it{};
+  // CUDA graph of the projector's launch sequence (replayed when the call signature repeats)
+  struct GraphKey {
+    const void *A, *B, *X, *V, *Q, *QL;
+    int64_t lda, ldb, ldx, ldv, ldq, ldql;
+    bool reuse;
+    bool operator==(const GraphKey& o) const {
+      return A == o.A && B == o.B && X == o.X && V == o.V && Q == o.Q && QL == o.QL && lda == o.lda && ldb == o.ldb &&
+             ldx == o.ldx && ldv == o.ldv && ldq == o.ldq && ldql == o.ldql && reuse == o.reuse;
+    }
+  };
+  bool graphs = true;
+  cudaGraphExec_t gexec = nullptr;
+  GraphKey gkey{}, gseen{};
+  bool gseen_valid = false;
+  int64_t glaunches = 0;
   feast_allreduce_fn ar = nullptr;
   void* ar_user = nullptr;
   std::string err;
@@ -100,6 +118,30 @@ int fail(feast_ctx* h, int code, const char* fmt, const char* a = "") {
   } while (0)
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// Every public call runs on the library's own stream, ordered after the work already queued on
+// the caller's stream and before anything the caller queues afterwards (event fork / join).
+struct Join {
+  feast_ctx* h;
+  explicit Join(feast_ctx* hh) : h(hh) {
+    if (h->own_stream) {
+      cudaEventRecord(h->ev_in, h->caller);
+      cudaStreamWaitEvent(h->stream, h->ev_in, 0);
+    }
+  }
+  ~Join() {
+    if (h->own_stream) {
+      cudaEventRecord(h->ev_out, h->stream);
+      cudaStreamWaitEvent(h->caller, h->ev_out, 0);
+    }
+  }
+};
+
+void graph_reset(feast_ctx* h) {   // the captured sequence depends on the workspace and cache mode
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  h->gexec = nullptr;
+  h->gseen_valid = false;
+}
 
 // ---------------------------------------------------------------- nodes (product side)
 // Quadrature on [-1,1] mapped to the ellipse of eq. ellipses: theta = pi/2 (1+t),
@@ -415,12 +457,13 @@ int check_args_common(feast_ctx* h, const void* A, int64_t lda, const void* B, i
   return FEAST_OK;
 }
 
-// The projector driver: right (X -> Q) and/or left (V -> QL) from one factorisation per node.
-int project_impl(feast_ctx* h, const double2* A, int64_t lda, const double2* B, int64_t ldb, const double2* X,
-                 int64_t ldx, const double2* V, int64_t ldv, double2* Q, int64_t ldq, double2* QL, int64_t ldql) {
+// The projector's launch sequence: right (X -> Q) and/or left (V -> QL) from one factorisation
+// per node.  Pure enqueue (no host synchronisation), so it can be captured into a CUDA graph.
+void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2* B, int64_t ldb, const double2* X,
+                     int64_t ldx, const double2* V, int64_t ldv, double2* Q, int64_t ldq, double2* QL, int64_t ldql,
+                     bool reuse) {
   const bool doR = X != nullptr, doL = V != nullptr;
   const int64_t n = h->n, m = h->m0, ld = h->ldc;
-  const int64_t t0 = feast::g_launches;
   const double2 one = make_double2(1, 0), zero = make_double2(0, 0);
   // a1: right-hand sides R = B X, RL = B^H V (shared by all nodes; skipped for B = I)
   const double2* Rr = X;
@@ -438,7 +481,6 @@ int project_impl(feast_ctx* h, const double2* A, int64_t lda, const double2* B, 
     h->stats_cur = h->stats + 2 * j;
     h->info_cur = h->info + j;
     const int64_t st = ld * (n + m);
-    const bool reuse = h->cache_on && h->cache_valid && h->batch >= owned && h->cache_A == A && h->cache_B == B;
     if (!reuse) {
       feast::stats_init_launch(h->stats_cur, h->info_cur, nbat, h->stream);
       // a2: C_j = z_j B - A ; R appended as extra columns (augmented system [C_j | R])
@@ -447,7 +489,6 @@ int project_impl(feast_ctx* h, const double2* A, int64_t lda, const double2* B, 
       // a3 (+ forward substitution of a4): P_j [C_j | R] -> [U_j | L_j^-1 P_j R]
       lu_batched(h, nbat, doR ? m : 0);
       if (doL || h->cache_on) feast::perm_launch(h->ipiv, h->perm, h->iperm, n, nbat, h->stream);
-      if (h->cache_on && h->batch >= owned) { h->cache_valid = true; h->cache_A = A; h->cache_B = B; }
       if (doR) {
         // a4: Y_j = U_j^-1 (L_j^-1 P_j R) ;  a5: Q (+)= sum w_j Y_j
         solve_right_back(h, h->Cw + n * ld, st, nbat);
@@ -470,9 +511,53 @@ int project_impl(feast_ctx* h, const double2* A, int64_t lda, const double2* B, 
     }
   }
   if (owned == 0) {
-    if (doR) for (int64_t c = 0; c < m; ++c) CUDA_TRY(h, cudaMemsetAsync(Q + c * ldq, 0, n * 16, h->stream));
-    if (doL) for (int64_t c = 0; c < m; ++c) CUDA_TRY(h, cudaMemsetAsync(QL + c * ldql, 0, n * 16, h->stream));
+    if (doR) cudaMemset2DAsync(Q, ldq * 16, 0, n * 16, m, h->stream);
+    if (doL) cudaMemset2DAsync(QL, ldql * 16, 0, n * 16, m, h->stream);
   }
+}
+
+// Driver: enqueue the sequence (replaying a CUDA graph of it when the call repeats with the same
+// pointers: the second identical call is captured, later ones replay it), then read back the
+// pivot diagnostics.
+int project_impl(feast_ctx* h, const double2* A, int64_t lda, const double2* B, int64_t ldb, const double2* X,
+                 int64_t ldx, const double2* V, int64_t ldv, double2* Q, int64_t ldq, double2* QL, int64_t ldql) {
+  const int64_t t0 = feast::g_launches;
+  const int owned = h->j1 - h->j0;
+  const bool reuse = h->cache_on && h->cache_valid && h->batch >= owned && h->cache_A == A && h->cache_B == B;
+  const feast_ctx::GraphKey key{A, B, X, V, Q, QL, lda, ldb, ldx, ldv, ldq, ldql, reuse};
+  const bool use_graph = h->graphs && !feast::prof().on;
+  if (use_graph && h->gexec && h->gkey == key) {
+    CUDA_TRY(h, cudaGraphLaunch(h->gexec, h->stream));
+    feast::count_launch((int)h->glaunches);
+  } else if (use_graph && h->gseen_valid && h->gseen == key) {
+    // second identical call: capture, instantiate, launch
+    if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+    cudaGraph_t g = nullptr;
+    const int64_t c0 = feast::g_launches;
+    CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    project_enqueue(h, A, lda, B, ldb, X, ldx, V, ldv, Q, ldq, QL, ldql, reuse);
+    const cudaError_t ce = cudaStreamEndCapture(h->stream, &g);
+    h->glaunches = feast::g_launches - c0;
+    feast::g_launches = c0;
+    if (ce != cudaSuccess ||
+        cudaGraphInstantiateWithFlags(&h->gexec, g, cudaGraphInstantiateFlagUseNodePriority) != cudaSuccess) {
+      cudaGetLastError();
+      if (g) cudaGraphDestroy(g);
+      h->gexec = nullptr;
+      h->graphs = false;   // capture unsupported here: keep launching the same kernels eagerly
+      project_enqueue(h, A, lda, B, ldb, X, ldx, V, ldv, Q, ldq, QL, ldql, reuse);
+    } else {
+      cudaGraphDestroy(g);
+      h->gkey = key;
+      CUDA_TRY(h, cudaGraphLaunch(h->gexec, h->stream));
+      feast::count_launch((int)h->glaunches);
+    }
+  } else {
+    project_enqueue(h, A, lda, B, ldb, X, ldx, V, ldv, Q, ldq, QL, ldql, reuse);
+    h->gseen = key;
+    h->gseen_valid = true;
+  }
+  if (!reuse && h->cache_on && h->batch >= owned) { h->cache_valid = true; h->cache_A = A; h->cache_B = B; }
   CUDA_TRY(h, cudaGetLastError());
   h->launches = feast::g_launches - t0;
   // pivot diagnostics of the owned nodes
@@ -575,7 +660,7 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   h->n = n; h->m0 = m0; h->c_re = c_re; h->c_im = c_im; h->r = r; h->aspect = aspect;
   h->n_e = n_e; h->rule = rule; h->mode = mode; h->b_id = b_is_identity != 0;
   h->rank = rank; h->world = world;
-  h->stream = (cudaStream_t)cuda_stream;
+  h->stream = h->caller = (cudaStream_t)cuda_stream;
   if (make_nodes(h) != 0 || h->q % world != 0) { delete h; return FEAST_E_ARG; }
   h->j0 = rank * (h->q / world);
   h->j1 = (rank + 1) * (h->q / world);
@@ -601,6 +686,7 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
     if (e[0] == 'r') { h->smem_cs = 0; h->nb = 64; }
   }
   if (const char* e = getenv("FEAST_LOOKAHEAD")) h->lookahead = e[0] != '0';
+  if (const char* e = getenv("FEAST_GRAPH")) h->graphs = e[0] != '0';
   if (const char* e = getenv("FEAST_NBO")) {
     const long v = atol(e);
     if (v >= 64 && v <= 256 && v % 64 == 0) h->nbo = v;
@@ -613,6 +699,13 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
         cudaEventCreateWithFlags(&h->ev_p, cudaEventDisableTiming) != cudaSuccess) {
       cudaGetLastError();
       h->lookahead = false;   // no CUDA context (CPU-only validation): launches never happen
+    } else if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) == cudaSuccess &&
+               cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming) == cudaSuccess &&
+               cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming) == cudaSuccess) {
+      h->own_stream = true;
+    } else {
+      cudaGetLastError();
+      h->stream = h->caller;
     }
   }
   h->ldc = (n + 7) / 8 * 8;
@@ -657,6 +750,7 @@ int feast_bind_workspace(feast_handle h, void* p, size_t bytes) {
   const size_t need = layout(h, nullptr);
   if (bytes < need) return fail(h, FEAST_E_NOMEM, "workspace too small%s");
   if (((uintptr_t)p) & 255) return fail(h, FEAST_E_ARG, "workspace not 256-byte aligned%s");
+  graph_reset(h);
   h->ws = p;
   h->ws_bytes = bytes;
   layout(h, (char*)p);
@@ -681,6 +775,7 @@ int feast_project(feast_handle h, const void* A, int64_t lda, const void* B, int
   int e = check_args_common(h, A, lda, B, ldb);
   if (e) return e;
   if (!X || !Q || ldx < h->n || ldq < h->n) return fail(h, FEAST_E_ARG, "X/Q null or ld < n%s");
+  Join j_(h);
   return project_impl(h, (const double2*)A, lda, (const double2*)B, ldb, (const double2*)X, ldx, nullptr, 0,
                       (double2*)Q, ldq, nullptr, 0);
 }
@@ -691,6 +786,7 @@ int feast_project_left(feast_handle h, const void* A, int64_t lda, const void* B
   if (e) return e;
   if (h->mode != FEAST_BI) return fail(h, FEAST_E_STATE, "left projector needs a FEAST_BI handle%s");
   if (!V || !QL || ldv < h->n || ldql < h->n) return fail(h, FEAST_E_ARG, "V/QL null or ld < n%s");
+  Join j_(h);
   return project_impl(h, (const double2*)A, lda, (const double2*)B, ldb, nullptr, 0, (const double2*)V, ldv, nullptr,
                       0, (double2*)QL, ldql);
 }
@@ -702,6 +798,7 @@ int feast_project_bi(feast_handle h, const void* A, int64_t lda, const void* B, 
   if (h->mode != FEAST_BI) return fail(h, FEAST_E_STATE, "bi projector needs a FEAST_BI handle%s");
   if (!X || !Q || !V || !QL || ldx < h->n || ldq < h->n || ldv < h->n || ldql < h->n)
     return fail(h, FEAST_E_ARG, "X/V/Q/QL null or ld < n%s");
+  Join j_(h);
   return project_impl(h, (const double2*)A, lda, (const double2*)B, ldb, (const double2*)X, ldx, (const double2*)V, ldv,
                       (double2*)Q, ldq, (double2*)QL, ldql);
 }
@@ -712,6 +809,7 @@ int feast_reduce(feast_handle h, const void* A, int64_t lda, const void* B, int6
   if (e) return e;
   if (!Q || !Ahat || !Bhat || ldq < h->n || ldah < h->m0 || ldbh < h->m0 || (QL && ldql < h->n))
     return fail(h, FEAST_E_ARG, "reduce: null pointer or bad ld%s");
+  Join j_(h);
   const int64_t n = h->n, m = h->m0, ld = h->ldc;
   const double2 one = make_double2(1, 0), zero = make_double2(0, 0);
   const double2* Qr = (const double2*)Q;
@@ -747,6 +845,7 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
   const bool bi = h->mode == FEAST_BI;
   if (!X || ldx < h->n || (bi && (!V || ldv < h->n))) return fail(h, FEAST_E_ARG, "X/V null or ld < n%s");
   if (h->world > 1 && !h->ar) return fail(h, FEAST_E_COMM, "world > 1 needs feast_set_allreduce%s");
+  Join j_(h);
   e = ensure_iter_mem(h);
   if (e) return e;
   const int64_t n = h->n, m = h->m0, ld = h->ldc;
@@ -853,6 +952,7 @@ int64_t feast_last_launch_count(feast_handle h) { return h ? h->launches : 0; }
 
 int feast_factor_cache(feast_handle h, int32_t enable) {
   if (!h) return FEAST_E_ARG;
+  graph_reset(h);
   h->cache_on = enable != 0;
   h->cache_valid = false;
   h->cache_A = h->cache_B = nullptr;
@@ -890,13 +990,41 @@ int feast_profile_summary(feast_handle h, int32_t kclass, int64_t* launches, dou
   return FEAST_OK;
 }
 
+int feast_profile_records(feast_handle h, int64_t max_records, int32_t* kclass, int32_t* stream, double* t0_ms,
+                          double* t1_ms, double* flops, int64_t* count) {
+  if (!h || max_records < 0) return FEAST_E_ARG;
+  CUDA_TRY(h, cudaDeviceSynchronize());
+  const auto& recs = feast::prof().recs;
+  const int64_t nrec = (int64_t)recs.size();
+  if (count) *count = nrec;
+  for (int64_t i = 0; i < nrec && i < max_records; ++i) {
+    const auto& r = recs[(size_t)i];
+    float e0 = 0.f, e1 = 0.f;
+    CUDA_TRY(h, cudaEventElapsedTime(&e0, recs[0].a, r.a));
+    CUDA_TRY(h, cudaEventElapsedTime(&e1, recs[0].a, r.b));
+    if (kclass) kclass[i] = r.cls;
+    if (stream) stream[i] = r.s == h->stream ? 0 : (r.s == h->side ? 1 : 2);
+    if (t0_ms) t0_ms[i] = e0;
+    if (t1_ms) t1_ms[i] = e1;
+    if (flops) flops[i] = r.flops;
+  }
+  return FEAST_OK;
+}
+
 const char* feast_last_error(feast_handle h) { return h ? h->err.c_str() : "null handle"; }
 
 void feast_destroy(feast_handle h) {
   if (!h) return;
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->ev_a) cudaEventDestroy(h->ev_a);
   if (h->ev_p) cudaEventDestroy(h->ev_p);
   if (h->side) cudaStreamDestroy(h->side);
+  if (h->own_stream) {
+    cudaStreamSynchronize(h->stream);
+    cudaStreamDestroy(h->stream);
+    cudaEventDestroy(h->ev_in);
+    cudaEventDestroy(h->ev_out);
+  }
   if (h->itmem) cudaFree(h->itmem);
   if (h->solp) cusolverDnDestroyParams(h->solp);
   if (h->sol) cusolverDnDestroy(h->sol);

@@ -387,121 +387,7 @@ void laswp_launch(Batched C, int64_t n, int64_t k, int cnt, const int32_t* ipiv,
   count_launch();
 }
 
-// ============================================================================ trsm
-// op(T) X = X for an nb x nb (nb <= 64) diagonal block; one thread per right-hand side column,
-// the column held in registers in two 32-row halves (no barriers, no shared memory):
-//   forward (op(T) lower): solve rows 0..31, update rows 32..63 with them, solve rows 32..63;
-//   backward (op(T) upper): mirror image.
-// T entries are read through the read-only path (all threads of a warp read the same
-// address: broadcast).  Used for U12 = L11^-1 A12 in the LU and for the diagonal blocks of
-// the blocked substitutions (L, U; U^H, L^H for the conjugate-transposed left solves).
-namespace {
-constexpr int TR_T = 128, TR_H = 32;
-
-template <bool CONJT>
-__device__ __forceinline__ double2 tget(const double2* __restrict__ Ts, int r, int i) {
-  // op(T)[r][i] from the shared-memory copy Ts[c * 65 + r] = T[r][c]
-  if (!CONJT) return Ts[i * (TR_H * 2 + 1) + r];
-  const double2 v = Ts[r * (TR_H * 2 + 1) + i];
-  return make_double2(v.x, -v.y);
-}
-
-// solve the h x h triangular block at rows/cols [o, o+h) of op(T), in place on x
-template <bool LOWER, bool UNIT, bool CONJT>
-__device__ __forceinline__ void tri_solve(const double2* __restrict__ Ts, int o, int h, double2 (&x)[TR_H]) {
-  if (LOWER) {
-#pragma unroll
-    for (int i = 0; i < TR_H; ++i) {
-      if (i < h) {
-        if (!UNIT) x[i] = cdiv(x[i], tget<CONJT>(Ts, o + i, o + i));
-#pragma unroll
-        for (int r = i + 1; r < TR_H; ++r)
-          if (r < h) x[r] = cfms(x[r], tget<CONJT>(Ts, o + r, o + i), x[i]);
-      }
-    }
-  } else {
-#pragma unroll
-    for (int i = TR_H - 1; i >= 0; --i) {
-      if (i < h) {
-        if (!UNIT) x[i] = cdiv(x[i], tget<CONJT>(Ts, o + i, o + i));
-#pragma unroll
-        for (int r = 0; r < i; ++r) x[r] = cfms(x[r], tget<CONJT>(Ts, o + r, o + i), x[i]);
-      }
-    }
-  }
-}
-
-template <bool LOWER, bool UNIT, bool CONJT>
-__global__ void __launch_bounds__(TR_T) trsm_kernel(Batched Tb, Batched Xb, int nb, int64_t ncols) {
-  extern __shared__ __align__(16) double2 Ts[];   // T[r][c] at Ts[c * 65 + r] (nb <= 64)
-  const int b = blockIdx.y;
-  const double2* __restrict__ T = Tb.p + (int64_t)b * Tb.stride;
-  for (int idx = threadIdx.x; idx < nb * nb; idx += TR_T) {
-    const int r = idx % nb, c = idx / nb;
-    Ts[c * (TR_H * 2 + 1) + r] = T[r + (int64_t)c * Tb.ld];
-  }
-  __syncthreads();
-  const int64_t c = (int64_t)blockIdx.x * TR_T + threadIdx.x;
-  if (c >= ncols) return;
-  double2* __restrict__ X = Xb.p + (int64_t)b * Xb.stride + c * Xb.ld;
-  const int h0 = min(nb, TR_H), h1 = nb - h0;
-  double2 x[TR_H];
-  // first half to solve: rows [0,h0) for forward, rows [h0,nb) for backward
-  const int oa = LOWER ? 0 : h0, ha = LOWER ? h0 : h1;
-  const int ob = LOWER ? h0 : 0, hb = LOWER ? h1 : h0;
-  if (ha > 0) {
-#pragma unroll
-    for (int r = 0; r < TR_H; ++r) if (r < ha) x[r] = X[oa + r];
-    tri_solve<LOWER, UNIT, CONJT>(Ts, oa, ha, x);
-#pragma unroll
-    for (int r = 0; r < TR_H; ++r) if (r < ha) X[oa + r] = x[r];
-  }
-  if (hb > 0) {
-    // second half: x <- rows [ob, ob+hb) - op(T)[ob.., oa..] * (first-half solution, re-read)
-#pragma unroll
-    for (int r = 0; r < TR_H; ++r) if (r < hb) x[r] = X[ob + r];
-    for (int t = 0; t < ha; ++t) {
-      const double2 xt = X[oa + t];
-#pragma unroll
-      for (int r = 0; r < TR_H; ++r)
-        if (r < hb) x[r] = cfms(x[r], tget<CONJT>(Ts, ob + r, oa + t), xt);
-    }
-    tri_solve<LOWER, UNIT, CONJT>(Ts, ob, hb, x);
-#pragma unroll
-    for (int r = 0; r < TR_H; ++r) if (r < hb) X[ob + r] = x[r];
-  }
-}
-
-template <bool LOWER, bool UNIT, bool CONJT>
-void trsm_t(Batched T, Batched X, int nb, int64_t ncols, int batch, cudaStream_t s) {
-  static bool configured = false;
-  const size_t smem = (size_t)(TR_H * 2 + 1) * 64 * sizeof(double2);
-  if (!configured) {
-    cudaFuncSetAttribute(trsm_kernel<LOWER, UNIT, CONJT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
-  dim3 grid((unsigned)((ncols + TR_T - 1) / TR_T), (unsigned)batch);
-  trsm_kernel<LOWER, UNIT, CONJT><<<grid, TR_T, smem, s>>>(T, X, nb, ncols);
-  count_launch();
-}
-}  // namespace
-
-void trsm_launch(Batched T, Batched X, int nb, int64_t ncols, bool lower_op, bool unit, bool conjT, int batch,
-                 cudaStream_t s) {
-  ProfScope ps_(K_TRSM, (double)batch * 4.0 * nb * nb * ncols, 0.0, s);
-  if (ncols <= 0 || nb <= 0) return;
-#define TR_CASE(L, U, C) \
-  if (lower_op == L && unit == U && conjT == C) { trsm_t<L, U, C>(T, X, nb, ncols, batch, s); return; }
-  TR_CASE(true, true, false)
-  TR_CASE(true, false, false)
-  TR_CASE(false, true, false)
-  TR_CASE(false, false, false)
-  TR_CASE(true, true, true)
-  TR_CASE(true, false, true)
-  TR_CASE(false, true, true)
-  TR_CASE(false, false, true)
-#undef TR_CASE
-}
+// trsm (in-block U12 = L11^-1 A12) lives in trtri.cu with the diagonal-block inverses.
 
 // ============================================================================ permutations
 // perm_b: result of applying the sequential swaps ipiv to 0..n-1 (one thread per matrix,

@@ -16,6 +16,7 @@ struct ProfRec {
   int cls;
   double flops, bytes;
   cudaEvent_t a, b;
+  cudaStream_t s;
 };
 
 struct Prof {
@@ -40,7 +41,7 @@ struct ProfScope {
   cudaStream_t s;
   ProfScope(int cls, double flops, double bytes, cudaStream_t st) : on(prof().on), s(st) {
     if (on) {
-      r.cls = cls; r.flops = flops; r.bytes = bytes;
+      r.cls = cls; r.flops = flops; r.bytes = bytes; r.s = st;
       r.a = prof().get(); r.b = prof().get();
       cudaEventRecord(r.a, s);
     }

@@ -1,14 +1,18 @@
-// trtri.cu — inverses of the 64x64 diagonal blocks of L (unit lower) and U (upper) of each
-// factored node, so that every triangular solve of the LU (U12 = L11^-1 A12) and of the blocked
-// substitutions (Y_k = L_kk^-1 Y_k, Y_k = U_kk^-1 Y_k, and the ^H forms of the left solves,
-// P:438-439) becomes an in-place DMMA ZGEMM with M = 64 (tensor pipe instead of a latency-bound
-// serial solve).
+// trtri.cu — the small triangular pieces of the blocked LU:
+//   * trsm:  op(T) X = X in place for an nb x nb diagonal block T (nb <= 64) and nb x ncols X —
+//            the in-block U12 = L11^-1 A12 of the 64-column blocks;
+//   * trtri: the inverses of the 64x64 diagonal blocks of L (unit lower) and U (upper) of each
+//            factored node, so that every other triangular solve of the LU (the outer
+//            U12 = L11^-1 A12) and of the blocked substitutions (Y_k = L_kk^-1 Y_k,
+//            Y_k = U_kk^-1 Y_k and the ^H forms of the left solves) becomes an
+//            in-place DMMA ZGEMM with M = 64 on the tensor pipe.
 //
-// Recursive doubling in shared memory: invert the eight 8x8 diagonal blocks (one thread per
-// column, in registers), then combine
-//   lower:  [A 0; B C]^-1 = [A^-1 0; -C^-1 B A^-1  C^-1]
-//   upper:  [A B; 0 C]^-1 = [A^-1  -A^-1 B C^-1; 0  C^-1]
-// for block sizes 8 -> 16 -> 32 -> 64.  A partial block (nb < 64) is padded with the identity.
+// Both are latency-bound chains of nb dependent steps, so the design minimises the latency of one
+// step: one WARP per right-hand-side column (columns of X, or of the identity for trtri), lane l
+// holding rows l and l + 32 in registers; T sits in shared memory.  Step t of a forward solve:
+// x_t is broadcast from its owner lane by shuffle (scaled by the precomputed 1/T_tt if not unit),
+// and every lane applies x_r -= T_rt x_t to its rows r > t (two LDS.128 + two complex FMAs).
+// Each warp carries CPW independent columns to overlap the chains; all warps of a CTA share one T.
 #include "common.cuh"
 #include "kernels.h"
 #include "prof.h"
@@ -16,95 +20,158 @@
 namespace feast {
 namespace {
 
-constexpr int TT = 256, NB = 64, LDS = NB + 1;
+constexpr int NB = 64, LDT = NB + 1;   // T[r][c] at Ts[r * LDT + c]: lanes (rows) 16 B x 65 apart
+constexpr int WARPS = 16;
 
-template <bool UPPER, bool UNIT>
-__device__ void trtri_block(const double2* __restrict__ T, int64_t ld, int nb, double2* __restrict__ out,
-                            double2* S, double2* X, double2* Tmp) {
-  const int tid = threadIdx.x;
-  // load (padded with identity), keep only the relevant triangle
-  for (int idx = tid; idx < NB * NB; idx += TT) {
-    const int r = idx % NB, c = idx / NB;
-    double2 v = make_double2(0.0, 0.0);
+__device__ __forceinline__ double2 shfl2(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+// op(T)[r][c] from the shared copy (CONJT: op = ^H)
+template <bool CONJT>
+__device__ __forceinline__ double2 opT(const double2* Ts, int r, int c) {
+  if (!CONJT) return Ts[r * LDT + c];
+  const double2 v = Ts[c * LDT + r];
+  return make_double2(v.x, -v.y);
+}
+
+// Load the nb x nb block (identity-padded to NB when PAD) into Ts, keeping only op(T)'s triangle
+// (the other triangle of the LU workspace holds the other factor); 1 / diagonal into dinv.
+template <bool LOWER, bool UNIT, bool CONJT>
+__device__ void load_tri(const double2* __restrict__ T, int64_t ld, int nb, int nbp, double2* Ts, double2* dinv) {
+  for (int idx = threadIdx.x; idx < nbp * nbp; idx += blockDim.x) {
+    const int r = idx % nbp, c = idx / nbp;   // source element T[r][c] (coalesced along r)
+    double2 v = make_double2(r == c ? 1.0 : 0.0, 0.0);
     if (r < nb && c < nb) {
-      const bool keep = UPPER ? (r <= c) : (r >= c);
+      // keep the triangle of T whose op() is LOWER/UPPER: op = ^H flips it
+      const bool lower_src = CONJT ? !LOWER : LOWER;
+      const bool keep = lower_src ? (r >= c) : (r <= c);
       if (keep) v = T[r + (int64_t)c * ld];
       if (r == c && UNIT) v = make_double2(1.0, 0.0);
-    } else if (r == c) {
-      v = make_double2(1.0, 0.0);
     }
-    S[r * LDS + c] = v;
-    X[r * LDS + c] = make_double2(0.0, 0.0);
+    Ts[r * LDT + c] = v;
   }
   __syncthreads();
-  // 8x8 diagonal blocks: thread = (block, column)
-  if (tid < NB) {
-    const int blk = tid >> 3, j = tid & 7, o = blk * 8;
-    double2 x[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-    if (!UPPER) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        x[i] = cdiv(x[i], S[(o + i) * LDS + o + i]);
-#pragma unroll
-        for (int r = i + 1; r < 8; ++r) x[r] = cfms(x[r], S[(o + r) * LDS + o + i], x[i]);
-      }
-    } else {
-#pragma unroll
-      for (int i = 7; i >= 0; --i) {
-        x[i] = cdiv(x[i], S[(o + i) * LDS + o + i]);
-#pragma unroll
-        for (int r = 0; r < i; ++r) x[r] = cfms(x[r], S[(o + r) * LDS + o + i], x[i]);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) X[(o + i) * LDS + o + j] = x[i];
-  }
+  if (!UNIT)
+    for (int i = threadIdx.x; i < nbp; i += blockDim.x) dinv[i] = crcp(opT<CONJT>(Ts, i, i));
   __syncthreads();
-  for (int s = 8; s < NB; s *= 2) {
-    const int nblk = NB / (2 * s);
-    // lower: Tmp = B A^-1   (B = S[o+s.., o..], A^-1 = X[o.., o..])
-    // upper: Tmp = B C^-1   (B = S[o.., o+s..], C^-1 = X[o+s.., o+s..])
-    for (int idx = tid; idx < nblk * s * s; idx += TT) {
-      const int blk = idx / (s * s), e = idx % (s * s), r = e / s, c = e % s, o = blk * 2 * s;
-      double2 acc = make_double2(0.0, 0.0);
-      if (!UPPER) {
-        for (int t = 0; t < s; ++t) acc = cfms(acc, S[(o + s + r) * LDS + o + t], X[(o + t) * LDS + o + c]);
-      } else {
-        for (int t = 0; t < s; ++t) acc = cfms(acc, S[(o + r) * LDS + o + s + t], X[(o + s + t) * LDS + o + s + c]);
-      }
-      Tmp[blk * s * s + r * s + c] = acc;   // = -(product)
+}
+
+// Solve op(T) x = x for CPW columns held as x[c][0] (row lane), x[c][1] (row lane + 32).
+template <bool LOWER, bool UNIT, bool CONJT, int CPW>
+__device__ __forceinline__ void warp_solve(const double2* Ts, const double2* dinv, int nbp, int t_lo, int t_hi,
+                                           double2 (&x)[CPW][2]) {
+  const int lane = threadIdx.x & 31;
+  for (int s = 0; s < nbp; ++s) {
+    const int t = LOWER ? s : nbp - 1 - s;
+    if (t < t_lo || t > t_hi) continue;   // warp-uniform
+    const int src = t & 31, half = t >> 5;
+    double2 xt[CPW];
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) {
+      xt[c] = shfl2(half ? x[c][1] : x[c][0], src);
+      if (!UNIT) xt[c] = cmul(xt[c], dinv[t]);
     }
-    __syncthreads();
-    // lower: X21 = C^-1 (-B A^-1) ; upper: X12 = A^-1 (-B C^-1)
-    for (int idx = tid; idx < nblk * s * s; idx += TT) {
-      const int blk = idx / (s * s), e = idx % (s * s), r = e / s, c = e % s, o = blk * 2 * s;
-      double2 acc = make_double2(0.0, 0.0);
-      if (!UPPER) {
-        for (int t = 0; t < s; ++t) acc = cadd(acc, cmul(X[(o + s + r) * LDS + o + s + t], Tmp[blk * s * s + t * s + c]));
-        X[(o + s + r) * LDS + o + c] = acc;
-      } else {
-        for (int t = 0; t < s; ++t) acc = cadd(acc, cmul(X[(o + r) * LDS + o + t], Tmp[blk * s * s + t * s + c]));
-        X[(o + r) * LDS + o + s + c] = acc;
+    if (!UNIT && lane == src) {
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {
+        if (half) x[c][1] = xt[c];
+        else x[c][0] = xt[c];
       }
     }
-    __syncthreads();
-  }
-  for (int idx = tid; idx < NB * NB; idx += TT) {
-    const int r = idx % NB, c = idx / NB;
-    out[r + c * NB] = X[r * LDS + c];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = lane + 32 * h;
+      if (r < nbp && (LOWER ? r > t : r < t)) {
+        const double2 trt = opT<CONJT>(Ts, r, t);
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) x[c][h] = cfms(x[c][h], trt, xt[c]);
+      }
+    }
   }
 }
 
-// blockIdx.x = node (batch), blockIdx.y = 0 (L^-1) / 1 (U^-1), blockIdx.z = diagonal block index
-// relative to kb0.  Source block j at matrix offset (o, o), o = (kb0 + j) * 64.
-__global__ void __launch_bounds__(TT) trtri_kernel(Batched Cb, int64_t n, int64_t kb0, double2* __restrict__ inv,
-                                                   int64_t inv_node_stride, int which) {
+// ---------------------------------------------------------------- trsm (in place on X)
+template <bool LOWER, bool UNIT, bool CONJT, int CPW>
+__global__ void __launch_bounds__(32 * WARPS) trsm_warp_kernel(Batched Tb, Batched Xb, int nb, int64_t ncols) {
   extern __shared__ __align__(16) double2 sm[];
-  double2* S = sm;
-  double2* X = sm + NB * LDS;
-  double2* Tmp = sm + 2 * NB * LDS;
+  double2* Ts = sm;
+  double2* dinv = sm + NB * LDT;
+  const int b = blockIdx.y;
+  load_tri<LOWER, UNIT, CONJT>(Tb.p + (int64_t)b * Tb.stride, Tb.ld, nb, nb, Ts, dinv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c0 = ((int64_t)blockIdx.x * WARPS + warp) * CPW;
+  if (c0 >= ncols) return;
+  double2* X = Xb.p + (int64_t)b * Xb.stride;
+  double2 x[CPW][2];
+#pragma unroll
+  for (int c = 0; c < CPW; ++c)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = lane + 32 * h;
+      x[c][h] = (c0 + c < ncols && r < nb) ? X[r + (c0 + c) * Xb.ld] : make_double2(0.0, 0.0);
+    }
+  warp_solve<LOWER, UNIT, CONJT, CPW>(Ts, dinv, nb, 0, nb - 1, x);
+#pragma unroll
+  for (int c = 0; c < CPW; ++c)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = lane + 32 * h;
+      if (c0 + c < ncols && r < nb) X[r + (c0 + c) * Xb.ld] = x[c][h];
+    }
+}
+
+template <bool LOWER, bool UNIT, bool CONJT>
+void trsm_t(Batched T, Batched X, int nb, int64_t ncols, int batch, cudaStream_t s) {
+  constexpr int CPW = 2;
+  const size_t smem = (size_t)(NB * LDT + NB) * sizeof(double2);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(trsm_warp_kernel<LOWER, UNIT, CONJT, CPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    configured = true;
+  }
+  dim3 grid((unsigned)((ncols + WARPS * CPW - 1) / (WARPS * CPW)), (unsigned)batch);
+  trsm_warp_kernel<LOWER, UNIT, CONJT, CPW><<<grid, 32 * WARPS, smem, s>>>(T, X, nb, ncols);
+  count_launch();
+}
+
+// ---------------------------------------------------------------- trtri (64x64 diagonal blocks)
+// blockIdx.x = node, blockIdx.y = 0 (L^-1, unit lower) / 1 (U^-1, upper), blockIdx.z = diagonal
+// block index relative to kb0.  Warp w inverts columns w*4 .. w*4+3 (identity right-hand sides;
+// column j of L^-1 is zero above row j, of U^-1 zero below, so the chains start at t = j).
+template <bool UPPER>
+__device__ void trtri_block(const double2* __restrict__ T, int64_t ld, int nb, double2* __restrict__ out,
+                            double2* Ts, double2* dinv) {
+  constexpr int CPW = NB / WARPS;   // 4 columns per warp
+  if (UPPER) load_tri<false, false, false>(T, ld, nb, NB, Ts, dinv);
+  else load_tri<true, true, false>(T, ld, nb, NB, Ts, dinv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // columns j = warp + WARPS * c: every warp gets a mix of long and short chains
+  double2 x[CPW][2];
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) {
+    const int j = warp + WARPS * c;
+    x[c][0] = make_double2(lane == j ? 1.0 : 0.0, 0.0);
+    x[c][1] = make_double2(lane + 32 == j ? 1.0 : 0.0, 0.0);
+  }
+  const int jmin = warp, jmax = warp + WARPS * (CPW - 1);
+  if (UPPER) warp_solve<false, false, false, CPW>(Ts, dinv, NB, 0, jmax, x);
+  else warp_solve<true, true, false, CPW>(Ts, dinv, NB, jmin, NB - 1, x);
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) {
+    const int j = warp + WARPS * c;
+    out[lane + j * NB] = x[c][0];
+    out[lane + 32 + j * NB] = x[c][1];
+  }
+}
+
+__global__ void __launch_bounds__(32 * WARPS) trtri_kernel(Batched Cb, int64_t n, int64_t kb0,
+                                                          double2* __restrict__ inv, int64_t inv_node_stride,
+                                                          int which) {
+  extern __shared__ __align__(16) double2 sm[];
+  double2* Ts = sm;
+  double2* dinv = sm + NB * LDT;
   const int b = blockIdx.x;
   const int lu = (which == 2) ? (int)blockIdx.y : which;
   const int64_t kb = kb0 + blockIdx.z;
@@ -112,23 +179,40 @@ __global__ void __launch_bounds__(TT) trtri_kernel(Batched Cb, int64_t n, int64_
   const int nb = (int)((n - o) < NB ? (n - o) : NB);
   const double2* T = Cb.p + (int64_t)b * Cb.stride + o + o * Cb.ld;
   double2* out = inv + (int64_t)b * inv_node_stride + (kb * 2 + lu) * (int64_t)NB * NB;
-  if (lu == 0) trtri_block<false, true>(T, Cb.ld, nb, out, S, X, Tmp);
-  else trtri_block<true, false>(T, Cb.ld, nb, out, S, X, Tmp);
+  if (lu == 0) trtri_block<false>(T, Cb.ld, nb, out, Ts, dinv);
+  else trtri_block<true>(T, Cb.ld, nb, out, Ts, dinv);
 }
 
 }  // namespace
 
+void trsm_launch(Batched T, Batched X, int nb, int64_t ncols, bool lower_op, bool unit, bool conjT, int batch,
+                 cudaStream_t s) {
+  ProfScope ps_(K_TRSM, (double)batch * 4.0 * nb * nb * ncols, 0.0, s);
+  if (ncols <= 0 || nb <= 0) return;
+#define TR_CASE(L, U, C) \
+  if (lower_op == L && unit == U && conjT == C) { trsm_t<L, U, C>(T, X, nb, ncols, batch, s); return; }
+  TR_CASE(true, true, false)
+  TR_CASE(true, false, false)
+  TR_CASE(false, true, false)
+  TR_CASE(false, false, false)
+  TR_CASE(true, true, true)
+  TR_CASE(true, false, true)
+  TR_CASE(false, true, true)
+  TR_CASE(false, false, true)
+#undef TR_CASE
+}
+
 void trtri_launch(Batched C, int64_t n, int64_t kb0, int64_t nblocks, double2* inv, int64_t inv_node_stride, int which,
                   int batch, cudaStream_t s) {
   ProfScope ps_(K_TRSM, (double)batch * nblocks * (which == 2 ? 2 : 1) * 8.0 * NB * NB * NB / 3.0, 0.0, s);
-  const size_t smem = (size_t)(2 * NB * LDS + NB * NB / 2) * sizeof(double2);
+  const size_t smem = (size_t)(NB * LDT + NB) * sizeof(double2);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(trtri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
   dim3 grid((unsigned)batch, which == 2 ? 2u : 1u, (unsigned)nblocks);
-  trtri_kernel<<<grid, TT, smem, s>>>(C, n, kb0, inv, inv_node_stride, which);
+  trtri_kernel<<<grid, 32 * WARPS, smem, s>>>(C, n, kb0, inv, inv_node_stride, which);
   count_launch();
 }
 

@@ -11,6 +11,8 @@
 // latency behind the DMMA pipe, and fills the 148 SMs even on the narrow updates of the LU
 // (N = 32..256).  In-place launches (C aliases B: the 64x64 diagonal-block inverses applied to
 // a block row) use 64x32 CTAs so one CTA row covers all M <= 64 rows it overwrites.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "prof.h"
@@ -239,7 +241,6 @@ void launch3(const ZgemmArgs& p, cudaStream_t s) {
 
 template <bool CONJA, int MODE>
 void launch_t(const ZgemmArgs& p, cudaStream_t s) {
-  ProfScope ps_(K_ZGEMM, 8.0 * (double)p.M * (double)p.N * (double)p.K * p.batch, 0.0, s);
   if (p.inplace) launch3<64, 32, 2, 2, 4, 2, CONJA, MODE>(p, s);   // BM >= M: one CTA row
   else launch3<32, 32, 2, 2, 4, 3, CONJA, MODE>(p, s);
 }
@@ -261,6 +262,7 @@ void launch_variant(const ZgemmArgs& p, int v, cudaStream_t s) {
 
 void zgemm_launch_variant(const ZgemmArgs& p, bool conjA, int mode, int variant, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.batch <= 0) return;
+  ProfScope ps_(K_ZGEMM, 8.0 * (double)p.M * (double)p.N * (double)p.K * p.batch, 0.0, s);
   if (conjA) {
     if (mode == ZG_SUB) launch_variant<true, ZG_SUB>(p, variant, s); else launch_variant<true, ZG_GEN>(p, variant, s);
   } else {
@@ -271,6 +273,15 @@ void zgemm_launch_variant(const ZgemmArgs& p, bool conjA, int mode, int variant,
 void zgemm_launch(const ZgemmArgs& p, bool conjA, int mode, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.batch <= 0) return;
   if (p.K <= 0 && mode == ZG_SUB) return;  // C -= 0
+  static const int env_variant = [] {       // experiments only (FEAST_ZGEMM_VARIANT=<n>)
+    const char* e = getenv("FEAST_ZGEMM_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  if (env_variant > 0 && !p.inplace) {
+    zgemm_launch_variant(p, conjA, mode, env_variant, s);
+    return;
+  }
+  ProfScope ps_(K_ZGEMM, 8.0 * (double)p.M * (double)p.N * (double)p.K * p.batch, 0.0, s);
   if (conjA) {
     if (mode == ZG_SUB) launch_t<true, ZG_SUB>(p, s); else launch_t<true, ZG_GEN>(p, s);
   } else {

@@ -32,7 +32,8 @@ ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, c
 # every symbol include/feast.h declares (checked by tests/test_abi.py)
 EXPORTS = ["feast_init", "feast_workspace_bytes", "feast_bind_workspace", "feast_nodes", "feast_project",
            "feast_project_left", "feast_project_bi", "feast_reduce", "feast_set_allreduce", "feast_iterate",
-           "feast_node_stats", "feast_factor_cache", "feast_last_launch_count", "feast_profile", "feast_profile_summary", "feast_last_error",
+           "feast_node_stats", "feast_factor_cache", "feast_last_launch_count", "feast_profile", "feast_profile_summary",
+           "feast_profile_records", "feast_last_error",
            "feast_version", "feast_destroy"]
 K_CLASSES = ["shift", "panel", "laswp", "trsm", "zgemm", "perm", "accum", "other"]
 
@@ -71,6 +72,7 @@ def load_library(path: str = LIB_PATH):
     lib.feast_factor_cache.argtypes = [P, I32]
     lib.feast_profile.argtypes = [P, I32]
     lib.feast_profile_summary.argtypes = [P, I32, P, P, P, P]
+    lib.feast_profile_records.argtypes = [P, I64, P, P, P, P, P, P]
     lib.feast_last_error.argtypes = [P]
     lib.feast_last_error.restype = ctypes.c_char_p
     lib.feast_version.restype = ctypes.c_char_p
@@ -156,7 +158,8 @@ class Feast:
         try:
             import torch.distributed as dist
             t = torch.as_tensor(_CudaPtr(buf, count), device=self.device)
-            dist.all_reduce(t, group=self.group)
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream, device=self.device)):
+                dist.all_reduce(t, group=self.group)   # ordered on the library's stream
             return 0
         except Exception:  # noqa: BLE001 — reported as FEAST_E_COMM by the library
             return 1
@@ -280,6 +283,16 @@ class Feast:
                                                        ctypes.byref(by)))
             out[name] = {"launches": c.value, "ms": ms.value, "flops": fl.value, "bytes": by.value}
         return out
+
+    def profile_records(self, max_records: int = 100000):
+        """Per-launch timeline since profile(True): list of (class, stream, t0_ms, t1_ms, flops)."""
+        cnt = ctypes.c_int64()
+        self._check(self.lib.feast_profile_records(self.h, 0, None, None, None, None, None, ctypes.byref(cnt)))
+        m = min(cnt.value, max_records)
+        cl, st = (ctypes.c_int32 * m)(), (ctypes.c_int32 * m)()
+        t0, t1, fl = (ctypes.c_double * m)(), (ctypes.c_double * m)(), (ctypes.c_double * m)()
+        self._check(self.lib.feast_profile_records(self.h, m, cl, st, t0, t1, fl, ctypes.byref(cnt)))
+        return [(K_CLASSES[cl[i]], st[i], t0[i], t1[i], fl[i]) for i in range(m)]
 
     @property
     def last_launch_count(self) -> int:

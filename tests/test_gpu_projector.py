@@ -182,3 +182,23 @@ def test_factor_cache_reuse():
     Q3 = f.project(A2, B, dev(X2))
     assert f.last_launch_count >= n_factor - 2
     assert rel(host(Q3), oracle.project(P.A + 0.01 * np.eye(P.n), P.B, X2, z, w)) <= TOL
+
+
+def test_graph_replay_reads_current_inputs():
+    """Repeated calls with the same buffers are captured into a CUDA graph (2nd call) and replayed
+    (3rd on): every call must still project the CURRENT contents of A, B and X."""
+    P = synth.make_pencil("C2", n=260, m0=24)
+    z, w = _oracle_nodes(P)
+    f = _handle(P)
+    A, B, X = dev(P.A), dev(P.B), dev(P.X0)
+    Q = torch.empty_like(X)
+    launches = []
+    for it in range(4):
+        Xh = synth.random_block(P.n, P.m0, 500 + it)
+        Ah = P.A + (0.002 * it) * np.eye(P.n)
+        X.copy_(dev(Xh))
+        A.copy_(dev(Ah))
+        f.project(A, B, X, Q)
+        launches.append(f.last_launch_count)
+        assert rel(host(Q), oracle.project(Ah, P.B, Xh, z, w)) <= TOL, it
+    assert len(set(launches)) == 1   # the replayed graph holds the same kernels
