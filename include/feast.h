@@ -165,7 +165,9 @@ int64_t feast_last_launch_count(feast_handle h);
 
 /* Per-kernel-class timing (bench roofline accounting).  feast_profile(h, 1) starts recording
  * a CUDA-event pair around every launch of this library on the launching stream (and clears
- * earlier records); feast_profile(h, 0) stops.  feast_profile_summary aggregates the records of
+ * earlier records); feast_profile(h, 2) does the same with every launch serialised on one
+ * stream (no lookahead, no concurrent node groups, no graph), so an event pair brackets only
+ * its own kernel; feast_profile(h, 0) stops.  feast_profile_summary aggregates the records of
  * one class: launches, summed event time (ms), algorithmic flops and algorithmic bytes
  * (DESIGN.md "Roofline" defines them per class).  Classes: */
 enum { FEAST_K_SHIFT = 0, FEAST_K_PANEL = 1, FEAST_K_LASWP = 2, FEAST_K_TRSM = 3, FEAST_K_ZGEMM = 4,

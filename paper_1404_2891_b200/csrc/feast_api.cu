@@ -45,6 +45,16 @@ struct feast_ctx {
   int64_t wp = 32;                    // cluster-panel width (divides 64)
   cudaStream_t side = nullptr;        // high-priority stream for the lookahead panel
   cudaEvent_t ev_a = nullptr, ev_p = nullptr;
+  // concurrent node groups (group 0 uses stream / side / ev_a / ev_p)
+  static constexpr int GMAX = 4;
+  bool prof_serial = false;           // feast_profile(h, 2): one stream, no lookahead / groups
+  int groups = 4;                     // concurrent node groups per batch (FEAST_GROUPS)
+  bool group_streams = false;
+  cudaStream_t gs[GMAX] = {}, gside[GMAX] = {};
+  cudaEvent_t gev_a[GMAX] = {}, gev_p[GMAX] = {}, gev_done[GMAX] = {};
+  cudaEvent_t ev_fork = nullptr;
+  cudaEvent_t gev_first[GMAX] = {};
+  bool stagger = false;  // true: group g starts once group g-1 has factored its first block
   int64_t ldc = 0;
   // workspace
   void* ws = nullptr;
@@ -56,8 +66,6 @@ struct feast_ctx {
   int64_t sk_elems = 0;
   int32_t *ipiv = nullptr, *perm = nullptr, *iperm = nullptr, *info = nullptr;
   double* stats = nullptr;
-  double* stats_cur = nullptr;   // stats/info of the batch being factored
-  int32_t* info_cur = nullptr;
   std::vector<double> minrel;
   int worst = -1;
   // iterate extras (library-owned, allocated lazily; outside the hot path)
@@ -230,7 +238,22 @@ int make_nodes(feast_ctx* h) {
 }
 
 Batched bat(double2* p, int64_t ld, int64_t stride) { return Batched{p, ld, stride}; }
-const double2* inv_ptr(feast_ctx* h, int64_t kb, int which) { return h->Inv + (kb * 2 + which) * 4096; }
+
+// A group of nodes factored together (lockstep batch): its slice of the workspace and its
+// streams.  Several groups run concurrently on their own stream pairs, so one group's latency-
+// bound panel chain overlaps another group's trailing-update GEMMs.
+struct Lu {
+  double2* Cw;          // first node's augmented block [C_j | R]
+  double2* Inv;         // first node's 64x64 diagonal-block inverses
+  int32_t* ipiv;        // first node's pivots
+  double* stats;        // first node's pivot statistics
+  int32_t* info;
+  int nbat;
+  cudaStream_t sm, sp;  // main / high-priority lookahead stream
+  cudaEvent_t ev_a, ev_p;
+  cudaEvent_t ev_first;  // recorded after the first block is factored (nullptr: none)
+};
+const double2* inv_ptr(const Lu& v, int64_t kb, int which) { return v.Inv + (kb * 2 + which) * 4096; }
 
 // ---------------------------------------------------------------- GEMM helpers
 // C = alpha op(A) B + beta C (single), with split-K when the output tile grid is too small
@@ -269,12 +292,12 @@ void gemm_gen(feast_ctx* h, int64_t M, int64_t N, int64_t K, bool conjA, const d
 }
 
 // ---------------------------------------------------------------- blocked LU (batched)
-void panel_at(feast_ctx* h, int64_t k, int w, int nbat, cudaStream_t s) {
+void panel_at(feast_ctx* h, const Lu& v, int64_t k, int w, cudaStream_t s) {
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0);
   if (h->smem_cs)
-    feast::panel_smem_launch(bat(h->Cw, ld, st), n, k, w, h->ipiv, h->stats_cur, h->info_cur, nbat, h->smem_cs, s);
+    feast::panel_smem_launch(bat(v.Cw, ld, st), n, k, w, v.ipiv, v.stats, v.info, v.nbat, h->smem_cs, s);
   else
-    feast::panel_launch(bat(h->Cw, ld, st), n, k, w, h->ipiv, h->stats_cur, h->info_cur, nbat, h->pcfg, s);
+    feast::panel_launch(bat(v.Cw, ld, st), n, k, w, v.ipiv, v.stats, v.info, v.nbat, h->pcfg, s);
 }
 
 // Two-level right-looking blocked LU of the batch with one-step LOOKAHEAD.
@@ -288,22 +311,23 @@ void panel_at(feast_ctx* h, int64_t k, int w, int nbat, cudaStream_t s) {
 // stream (disjoint columns; the next block's swaps reach the other columns afterwards).
 // aug > 0: columns [n, n + aug) hold R, so swaps, U12 and updates also perform the forward
 // substitution L^-1 P R.
-void factor_block(feast_ctx* h, int64_t K0, int64_t Wo, int nbat, cudaStream_t s) {
+void factor_block(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, cudaStream_t s) {
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0);
-  double2* C = h->Cw;
+  double2* C = v.Cw;
+  const int nbat = v.nbat;
   const int64_t wp = h->smem_cs ? h->wp : 64;
   for (int64_t ki = K0; ki < K0 + Wo; ki += 64) {
     const int wi = (int)std::min<int64_t>(64, K0 + Wo - ki);
     // the 64-block is factored as narrow cluster panels of wp columns (small SM footprint), with
-    // the in-block U12 (register TRSM) and update (DMMA) between them
+    // the in-block U12 (warp TRSM) and update (DMMA) between them
     for (int64_t kp = ki; kp < ki + wi; kp += wp) {
       const int wpp = (int)std::min<int64_t>(wp, ki + wi - kp);
-      panel_at(h, kp, wpp, nbat, s);
+      panel_at(h, v, kp, wpp, s);
       if (h->smem_cs) {
-        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, h->ipiv, K0, K0 + Wo, nbat, s);
+        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, K0 + Wo, nbat, s);
       } else {   // the register-chunk panel already swapped its own columns
-        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, h->ipiv, K0, kp, nbat, s);
-        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, h->ipiv, kp + wpp, K0 + Wo, nbat, s);
+        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, kp, nbat, s);
+        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, kp + wpp, K0 + Wo, nbat, s);
       }
       const int64_t cp = kp + wpp, remb = ki + wi - cp;
       if (remb > 0) {
@@ -314,10 +338,10 @@ void factor_block(feast_ctx* h, int64_t K0, int64_t Wo, int nbat, cudaStream_t s
         feast::zgemm_launch(p, false, feast::ZG_SUB, s);
       }
     }
-    feast::trtri_launch(bat(C, ld, st), n, ki / 64, 1, h->Inv, h->inv_stride, 2, nbat, s);
+    feast::trtri_launch(bat(C, ld, st), n, ki / 64, 1, v.Inv, h->inv_stride, 2, nbat, s);
     const int64_t c1 = ki + wi, rem = K0 + Wo - c1;
     if (rem > 0) {
-      ZgemmArgs u{wi, rem, wi, inv_ptr(h, ki / 64, 0), 64, h->inv_stride, C + ki + c1 * ld, ld, st, C + ki + c1 * ld,
+      ZgemmArgs u{wi, rem, wi, inv_ptr(v, ki / 64, 0), 64, h->inv_stride, C + ki + c1 * ld, ld, st, C + ki + c1 * ld,
                   ld, st, make_double2(1, 0), make_double2(0, 0), nbat, 1};
       feast::zgemm_launch(u, false, feast::ZG_GEN, s);
       ZgemmArgs p{n - c1, rem, wi, C + c1 + ki * ld, ld, st, C + ki + c1 * ld, ld, st, C + c1 + c1 * ld, ld, st,
@@ -328,13 +352,14 @@ void factor_block(feast_ctx* h, int64_t K0, int64_t Wo, int nbat, cudaStream_t s
 }
 
 // U12 = L11^-1 A12 and A22 -= L21 U12 for the columns [c0, c0 + nc) of outer block (K0, Wo).
-void outer_update(feast_ctx* h, int64_t K0, int64_t Wo, int64_t c0, int64_t nc, int nbat, cudaStream_t s) {
+void outer_update(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, int64_t c0, int64_t nc, cudaStream_t s) {
   if (nc <= 0) return;
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0), K1 = K0 + Wo;
-  double2* C = h->Cw;
+  double2* C = v.Cw;
+  const int nbat = v.nbat;
   for (int64_t ki = K0; ki < K1; ki += 64) {
     const int wi = (int)std::min<int64_t>(64, K1 - ki);
-    ZgemmArgs u{wi, nc, wi, inv_ptr(h, ki / 64, 0), 64, h->inv_stride, C + ki + c0 * ld, ld, st, C + ki + c0 * ld, ld,
+    ZgemmArgs u{wi, nc, wi, inv_ptr(v, ki / 64, 0), 64, h->inv_stride, C + ki + c0 * ld, ld, st, C + ki + c0 * ld, ld,
                 st, make_double2(1, 0), make_double2(0, 0), nbat, 1};
     feast::zgemm_launch(u, false, feast::ZG_GEN, s);
     if (ki + wi < K1) {
@@ -350,101 +375,104 @@ void outer_update(feast_ctx* h, int64_t K0, int64_t Wo, int64_t c0, int64_t nc, 
   }
 }
 
-void lu_batched(feast_ctx* h, int nbat, int64_t aug) {
+void lu_batched(feast_ctx* h, const Lu& v, int64_t aug) {
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0), ntot = n + aug;
-  double2* C = h->Cw;
-  cudaStream_t sm = h->stream, sp = h->side;
+  double2* C = v.Cw;
+  const int nbat = v.nbat;
+  cudaStream_t sm = v.sm, sp = v.sp;
   const int64_t NBO = h->nbo;
   int64_t Wo = std::min<int64_t>(NBO, n);
-  factor_block(h, 0, Wo, nbat, sm);
-  feast::laswp_launch(bat(C, ld, st), n, 0, (int)Wo, h->ipiv, Wo, ntot, nbat, sm);
+  factor_block(h, v, 0, Wo, sm);
+  if (v.ev_first) cudaEventRecord(v.ev_first, sm);   // releases the next (staggered) group
+  feast::laswp_launch(bat(C, ld, st), n, 0, (int)Wo, v.ipiv, Wo, ntot, nbat, sm);
   for (int64_t K0 = 0; K0 < n; K0 += Wo, Wo = std::min<int64_t>(NBO, n - K0)) {
     const int64_t K1 = K0 + Wo;
     if (K1 >= n) {
-      outer_update(h, K0, Wo, n, aug, nbat, sm);      // last block: augmented columns only
+      outer_update(h, v, K0, Wo, n, aug, sm);      // last block: augmented columns only
       break;
     }
     const int64_t Wo1 = std::min<int64_t>(NBO, n - K1);
-    outer_update(h, K0, Wo, K1, Wo1, nbat, sm);       // next block's columns first
-    if (h->lookahead) {
-      cudaEventRecord(h->ev_a, sm);
-      cudaStreamWaitEvent(sp, h->ev_a, 0);
-      factor_block(h, K1, Wo1, nbat, sp);             // overlaps the rest of the outer update
-      cudaEventRecord(h->ev_p, sp);
-      outer_update(h, K0, Wo, K1 + Wo1, ntot - K1 - Wo1, nbat, sm);
-      cudaStreamWaitEvent(sm, h->ev_p, 0);
+    outer_update(h, v, K0, Wo, K1, Wo1, sm);       // next block's columns first
+    if (h->lookahead && !h->prof_serial) {
+      cudaEventRecord(v.ev_a, sm);
+      cudaStreamWaitEvent(sp, v.ev_a, 0);
+      factor_block(h, v, K1, Wo1, sp);             // overlaps the rest of the outer update
+      cudaEventRecord(v.ev_p, sp);
+      outer_update(h, v, K0, Wo, K1 + Wo1, ntot - K1 - Wo1, sm);
+      cudaStreamWaitEvent(sm, v.ev_p, 0);
     } else {
-      outer_update(h, K0, Wo, K1 + Wo1, ntot - K1 - Wo1, nbat, sm);
-      factor_block(h, K1, Wo1, nbat, sm);
+      outer_update(h, v, K0, Wo, K1 + Wo1, ntot - K1 - Wo1, sm);
+      factor_block(h, v, K1, Wo1, sm);
     }
     // block K1's swaps on every column outside it
-    feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, h->ipiv, 0, K1, nbat, sm);
-    feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, h->ipiv, K1 + Wo1, ntot, nbat, sm);
+    feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, 0, K1, nbat, sm);
+    feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, K1 + Wo1, ntot, nbat, sm);
   }
 }
 
 // Y_k <- op(T_kk^-1) Y_k in place (M = w <= 64): which 0 = L^-1, 1 = U^-1; conj: (.)^H
-void diag_apply(feast_ctx* h, double2* Y, int64_t sy, int64_t k, int w, int which, bool conj, int nbat) {
+void diag_apply(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t k, int w, int which, bool conj) {
   const int64_t ld = h->ldc;
-  ZgemmArgs p{w, h->m0, w, inv_ptr(h, k / 64, which), 64, h->inv_stride, Y + k, ld, sy, Y + k, ld, sy,
-              make_double2(1, 0), make_double2(0, 0), nbat, 1};
-  feast::zgemm_launch(p, conj, feast::ZG_GEN, h->stream);
+  ZgemmArgs p{w, h->m0, w, inv_ptr(v, k / 64, which), 64, h->inv_stride, Y + k, ld, sy, Y + k, ld, sy,
+              make_double2(1, 0), make_double2(0, 0), v.nbat, 1};
+  feast::zgemm_launch(p, conj, feast::ZG_GEN, v.sm);
 }
 
 // Y <- L^-1 Y (Y already row-permuted): used when the factors are cached (no augmented LU)
-void solve_right_fwd(feast_ctx* h, double2* Y, int64_t sy, int nbat) {
+void solve_right_fwd(feast_ctx* h, const Lu& v, double2* Y, int64_t sy) {
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0), m = h->m0;
-  double2* C = h->Cw;
+  double2* C = v.Cw;
   for (int64_t k = 0; k < n; k += h->nb) {
     const int w = (int)std::min<int64_t>(h->nb, n - k);
-    diag_apply(h, Y, sy, k, w, 0, false, nbat);
+    diag_apply(h, v, Y, sy, k, w, 0, false);
     const int64_t rest = n - k - w;
     if (rest > 0) {
       ZgemmArgs p{rest, m, w, C + (k + w) + k * ld, ld, st, Y + k, ld, sy, Y + k + w, ld, sy,
-                  make_double2(-1, 0), make_double2(1, 0), nbat};
-      feast::zgemm_launch(p, false, feast::ZG_SUB, h->stream);
+                  make_double2(-1, 0), make_double2(1, 0), v.nbat};
+      feast::zgemm_launch(p, false, feast::ZG_SUB, v.sm);
     }
   }
 }
 
 // Y <- U^-1 Y  (Y = L^-1 P R already: the forward substitution ran inside the augmented LU)
-void solve_right_back(feast_ctx* h, double2* Y, int64_t sy, int nbat) {
+void solve_right_back(feast_ctx* h, const Lu& v, double2* Y, int64_t sy) {
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0), m = h->m0;
-  double2* C = h->Cw;
+  double2* C = v.Cw;
   const int64_t last = ((n - 1) / h->nb) * h->nb;
   for (int64_t k = last; k >= 0; k -= h->nb) {
     const int w = (int)std::min<int64_t>(h->nb, n - k);
-    diag_apply(h, Y, sy, k, w, 1, false, nbat);
+    diag_apply(h, v, Y, sy, k, w, 1, false);
     if (k > 0) {
-      ZgemmArgs p{k, m, w, C + k * ld, ld, st, Y + k, ld, sy, Y, ld, sy, make_double2(-1, 0), make_double2(1, 0), nbat};
-      feast::zgemm_launch(p, false, feast::ZG_SUB, h->stream);
+      ZgemmArgs p{k, m, w, C + k * ld, ld, st, Y + k, ld, sy, Y, ld, sy, make_double2(-1, 0), make_double2(1, 0),
+                  v.nbat};
+      feast::zgemm_launch(p, false, feast::ZG_SUB, v.sm);
     }
   }
 }
 
 // Y <- L^-H U^-H Y   (then the caller applies P^T): M^H = U^H L^H P  (P:438-439 same factors)
-void solve_left(feast_ctx* h, double2* Y, int nbat) {
+void solve_left(feast_ctx* h, const Lu& v, double2* Y) {
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0), m = h->m0, sy = ld * m;
-  double2* C = h->Cw;
+  double2* C = v.Cw;
   for (int64_t k = 0; k < n; k += h->nb) {  // U^H: lower, non-unit
     const int w = (int)std::min<int64_t>(h->nb, n - k);
-    diag_apply(h, Y, sy, k, w, 1, true, nbat);      // (U_kk^H)^-1 = (U_kk^-1)^H
+    diag_apply(h, v, Y, sy, k, w, 1, true);      // (U_kk^H)^-1 = (U_kk^-1)^H
     const int64_t rest = n - k - w;
     if (rest > 0) {
       // Y[k+w:] -= (U[k:k+w, k+w:])^H Y[k:k+w]
       ZgemmArgs p{rest, m, w, C + k + (k + w) * ld, ld, st, Y + k, ld, sy, Y + k + w, ld, sy,
-                  make_double2(-1, 0), make_double2(1, 0), nbat};
-      feast::zgemm_launch(p, true, feast::ZG_SUB, h->stream);
+                  make_double2(-1, 0), make_double2(1, 0), v.nbat};
+      feast::zgemm_launch(p, true, feast::ZG_SUB, v.sm);
     }
   }
   const int64_t last = ((n - 1) / h->nb) * h->nb;
   for (int64_t k = last; k >= 0; k -= h->nb) {  // L^H: upper, unit
     const int w = (int)std::min<int64_t>(h->nb, n - k);
-    diag_apply(h, Y, sy, k, w, 0, true, nbat);      // (L_kk^H)^-1 = (L_kk^-1)^H
+    diag_apply(h, v, Y, sy, k, w, 0, true);      // (L_kk^H)^-1 = (L_kk^-1)^H
     if (k > 0) {
       // Y[0:k] -= (L[k:k+w, 0:k])^H Y[k:k+w]
-      ZgemmArgs p{k, m, w, C + k, ld, st, Y + k, ld, sy, Y, ld, sy, make_double2(-1, 0), make_double2(1, 0), nbat};
-      feast::zgemm_launch(p, true, feast::ZG_SUB, h->stream);
+      ZgemmArgs p{k, m, w, C + k, ld, st, Y + k, ld, sy, Y, ld, sy, make_double2(-1, 0), make_double2(1, 0), v.nbat};
+      feast::zgemm_launch(p, true, feast::ZG_SUB, v.sm);
     }
   }
 }
@@ -475,40 +503,58 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
     if (doL) { gemm_gen(h, n, m, n, true, B, ldb, V, ldv, h->RL, ld, one, zero); Rl = h->RL; ldrl = ld; }
   }
   const int owned = h->j1 - h->j0;
+  const int64_t st = ld * (n + m);
   for (int jb = 0; jb < owned; jb += h->batch) {
     const int nbat = std::min(h->batch, owned - jb);
     const int j = h->j0 + jb;
-    h->stats_cur = h->stats + 2 * j;
-    h->info_cur = h->info + j;
-    const int64_t st = ld * (n + m);
-    if (!reuse) {
-      feast::stats_init_launch(h->stats_cur, h->info_cur, nbat, h->stream);
-      // a2: C_j = z_j B - A ; R appended as extra columns (augmented system [C_j | R])
-      feast::shift_launch(bat(h->Cw, ld, st), A, lda, B, ldb, h->zd + j, n, nbat, h->stream);
-      if (doR) feast::broadcast_copy_launch(bat(h->Cw + n * ld, ld, st), Rr, ldr, n, m, nbat, h->stream);
-      // a3 (+ forward substitution of a4): P_j [C_j | R] -> [U_j | L_j^-1 P_j R]
-      lu_batched(h, nbat, doR ? m : 0);
-      if (doL || h->cache_on) feast::perm_launch(h->ipiv, h->perm, h->iperm, n, nbat, h->stream);
-      if (doR) {
-        // a4: Y_j = U_j^-1 (L_j^-1 P_j R) ;  a5: Q (+)= sum w_j Y_j
-        solve_right_back(h, h->Cw + n * ld, st, nbat);
+    // split the batch into G concurrent groups (group 0 on the handle's stream)
+    const int G = (h->group_streams && !h->prof_serial) ? std::max(1, std::min(h->groups, nbat)) : 1;
+    if (G > 1) cudaEventRecord(h->ev_fork, h->stream);
+    for (int g = 0; g < G; ++g) {
+      const int b0 = g * nbat / G, b1 = (g + 1) * nbat / G;
+      Lu v{h->Cw + b0 * st, h->Inv + b0 * h->inv_stride, h->ipiv + (int64_t)b0 * n, h->stats + 2 * (j + b0),
+           h->info + (j + b0), b1 - b0, g ? h->gs[g] : h->stream, g ? h->gside[g] : h->side, g ? h->gev_a[g] : h->ev_a,
+           g ? h->gev_p[g] : h->ev_p, (h->stagger && g + 1 < G) ? h->gev_first[g] : nullptr};
+      if (g) cudaStreamWaitEvent(v.sm, (h->stagger && g > 0) ? h->gev_first[g - 1] : h->ev_fork, 0);
+      if (!reuse) {
+        feast::stats_init_launch(v.stats, v.info, v.nbat, v.sm);
+        // a2: C_j = z_j B - A ; R appended as extra columns (augmented system [C_j | R])
+        feast::shift_launch(bat(v.Cw, ld, st), A, lda, B, ldb, h->zd + j + b0, n, v.nbat, v.sm);
+        if (doR) feast::broadcast_copy_launch(bat(v.Cw + n * ld, ld, st), Rr, ldr, n, m, v.nbat, v.sm);
+        // a3 (+ forward substitution of a4): P_j [C_j | R] -> [U_j | L_j^-1 P_j R]
+        lu_batched(h, v, doR ? m : 0);
+        if (doL || h->cache_on)
+          feast::perm_launch(v.ipiv, h->perm + (int64_t)b0 * n, h->iperm + (int64_t)b0 * n, n, v.nbat, v.sm);
+        // a4: Y_j = U_j^-1 (L_j^-1 P_j R)
+        if (doR) solve_right_back(h, v, v.Cw + n * ld, st);
+      } else if (doR) {
+        // cached factors (NEXT-1, "factored just once"): Y_j = U^-1 L^-1 P_j R
+        double2* Yg = h->Y + b0 * ld * m;
+        feast::gather_rows_launch(bat(Yg, ld, ld * m), Rr, ldr, 0, h->perm + (int64_t)b0 * n, n, m, v.nbat, v.sm);
+        solve_right_fwd(h, v, Yg, ld * m);
+        solve_right_back(h, v, Yg, ld * m);
+      }
+      if (doL) {
+        // Z_j = P^T L^-H U^-H RL  (P^T folded into the accumulate below)
+        double2* Yg = h->YL + b0 * ld * m;
+        feast::broadcast_copy_launch(bat(Yg, ld, ld * m), Rl, ldrl, n, m, v.nbat, v.sm);
+        solve_left(h, v, Yg);
+      }
+      if (g) {
+        cudaEventRecord(h->gev_done[g], v.sm);
+        cudaStreamWaitEvent(h->stream, h->gev_done[g], 0);
+      }
+    }
+    // a5: Q (+)= sum_j w_j Y_j, QL (+)= sum_j conj(w_j) Z_j over the batch in node order
+    if (doR) {
+      if (!reuse)
         feast::accum_launch(Q, ldq, bat(h->Cw + n * ld, ld, st), h->wd + j, nullptr, n, m, nbat, false, jb > 0,
                             h->stream);
-      }
-    } else if (doR) {
-      // cached factors (NEXT-1, "factored just once"): Y_j = U^-1 L^-1 P_j R
-      feast::gather_rows_launch(bat(h->Y, ld, ld * m), Rr, ldr, 0, h->perm, n, m, nbat, h->stream);
-      solve_right_fwd(h, h->Y, ld * m, nbat);
-      solve_right_back(h, h->Y, ld * m, nbat);
-      feast::accum_launch(Q, ldq, bat(h->Y, ld, ld * m), h->wd + j, nullptr, n, m, nbat, false, jb > 0, h->stream);
+      else
+        feast::accum_launch(Q, ldq, bat(h->Y, ld, ld * m), h->wd + j, nullptr, n, m, nbat, false, jb > 0, h->stream);
     }
-    if (doL) {
-      // Z_j = P^T L^-H U^-H RL ;  QL (+)= sum conj(w_j) Z_j  (P^T folded into the accumulate)
-      feast::broadcast_copy_launch(bat(h->YL, ld, ld * m), Rl, ldrl, n, m, nbat, h->stream);
-      solve_left(h, h->YL, nbat);
-      feast::accum_launch(QL, ldql, bat(h->YL, ld, ld * m), h->wd + j, h->iperm, n, m, nbat, true, jb > 0,
-                          h->stream);
-    }
+    if (doL)
+      feast::accum_launch(QL, ldql, bat(h->YL, ld, ld * m), h->wd + j, h->iperm, n, m, nbat, true, jb > 0, h->stream);
   }
   if (owned == 0) {
     if (doR) cudaMemset2DAsync(Q, ldq * 16, 0, n * 16, m, h->stream);
@@ -687,6 +733,11 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   }
   if (const char* e = getenv("FEAST_LOOKAHEAD")) h->lookahead = e[0] != '0';
   if (const char* e = getenv("FEAST_GRAPH")) h->graphs = e[0] != '0';
+  if (const char* e = getenv("FEAST_STAGGER")) h->stagger = e[0] != '0';
+  if (const char* e = getenv("FEAST_GROUPS")) {
+    const int v = atoi(e);
+    if (v >= 1 && v <= feast_ctx::GMAX) h->groups = v;
+  }
   if (const char* e = getenv("FEAST_NBO")) {
     const long v = atol(e);
     if (v >= 64 && v <= 256 && v % 64 == 0) h->nbo = v;
@@ -703,6 +754,17 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
                cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming) == cudaSuccess &&
                cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming) == cudaSuccess) {
       h->own_stream = true;
+      bool ok = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) == cudaSuccess;
+      for (int g = 1; g < feast_ctx::GMAX && ok; ++g)
+        ok = cudaStreamCreateWithFlags(&h->gs[g], cudaStreamNonBlocking) == cudaSuccess &&
+             cudaStreamCreateWithPriority(&h->gside[g], cudaStreamNonBlocking, hi) == cudaSuccess &&
+             cudaEventCreateWithFlags(&h->gev_a[g], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&h->gev_p[g], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&h->gev_done[g], cudaEventDisableTiming) == cudaSuccess;
+      for (int g = 0; g < feast_ctx::GMAX && ok; ++g)
+        ok = cudaEventCreateWithFlags(&h->gev_first[g], cudaEventDisableTiming) == cudaSuccess;
+      if (!ok) { cudaGetLastError(); h->groups = 1; h->group_streams = false; }
+      else h->group_streams = true;
     } else {
       cudaGetLastError();
       h->stream = h->caller;
@@ -965,6 +1027,7 @@ int feast_profile(feast_handle h, int32_t enable) {
   if (!h) return FEAST_E_ARG;
   feast::Prof& p = feast::prof();
   p.on = enable != 0;
+  h->prof_serial = enable == 2;
   p.recs.clear();
   p.used = 0;
   return FEAST_OK;
@@ -1019,6 +1082,16 @@ void feast_destroy(feast_handle h) {
   if (h->ev_a) cudaEventDestroy(h->ev_a);
   if (h->ev_p) cudaEventDestroy(h->ev_p);
   if (h->side) cudaStreamDestroy(h->side);
+  for (int g = 1; g < feast_ctx::GMAX; ++g) {
+    if (h->gs[g]) cudaStreamDestroy(h->gs[g]);
+    if (h->gside[g]) cudaStreamDestroy(h->gside[g]);
+    if (h->gev_a[g]) cudaEventDestroy(h->gev_a[g]);
+    if (h->gev_p[g]) cudaEventDestroy(h->gev_p[g]);
+    if (h->gev_done[g]) cudaEventDestroy(h->gev_done[g]);
+  }
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  for (int g = 0; g < feast_ctx::GMAX; ++g)
+    if (h->gev_first[g]) cudaEventDestroy(h->gev_first[g]);
   if (h->own_stream) {
     cudaStreamSynchronize(h->stream);
     cudaStreamDestroy(h->stream);

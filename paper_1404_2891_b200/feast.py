@@ -270,9 +270,10 @@ class Feast:
         """Factor-once reuse across calls with the same A, B (NEXT-1); enable=True invalidates."""
         self._check(self.lib.feast_factor_cache(self.h, int(bool(enable))))
 
-    def profile(self, enable: bool):
-        """Start (clears) / stop per-kernel-class CUDA-event timing of this library's launches."""
-        self._check(self.lib.feast_profile(self.h, int(bool(enable))))
+    def profile(self, enable, serial: bool = False):
+        """Start (clears) / stop per-kernel-class CUDA-event timing of this library's launches;
+        serial=True serialises every launch on one stream so each event pair times one kernel."""
+        self._check(self.lib.feast_profile(self.h, (2 if serial else 1) if enable else 0))
 
     def profile_summary(self):
         """{class: {launches, ms, flops, bytes}} of the launches recorded since profile(True)."""

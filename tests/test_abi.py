@@ -95,3 +95,13 @@ def test_workspace_size_scales_with_batch():
         sizes.append(b.value)
         lib.feast_destroy(h)
     assert sizes[1] - sizes[0] >= 3 * 16 * 512 * 512
+
+
+def test_library_has_no_static_tls():
+    """The .so is dlopen'ed into a process that already loaded torch/CUDA: a STATIC_TLS flag
+    (initial-exec TLS, e.g. from a statically linked cudart) can fail with 'cannot allocate
+    memory in static TLS block'.  The build links cudart shared to avoid it."""
+    import subprocess
+    out = subprocess.run(["readelf", "-d", fb.LIB_PATH], capture_output=True, text=True).stdout
+    assert "STATIC_TLS" not in out
+    assert "libcudart.so" in out

@@ -16,10 +16,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("key", nargs="?", default="C2")
 ap.add_argument("--out", default=None)
 ap.add_argument("--n", type=int, default=None)
+ap.add_argument("--batch", type=int, default=0)
 args = ap.parse_args()
 P = synth.make_pencil(args.key, n=args.n)
 s = P.spec
-f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, P.B is None)
+f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, P.B is None, max_batch=args.batch)
 d = lambda a: None if a is None else torch.from_numpy(np.asfortranarray(a)).to("cuda")
 A, B, X = d(P.A), d(P.B), d(P.X0)
 Q = f.project(A, B, X)
