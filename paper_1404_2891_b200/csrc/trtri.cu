@@ -12,7 +12,8 @@
 // holding rows l and l + 32 in registers; T sits in shared memory.  Step t of a forward solve:
 // x_t is broadcast from its owner lane by shuffle (scaled by the precomputed 1/T_tt if not unit),
 // and every lane applies x_r -= T_rt x_t to its rows r > t (two LDS.128 + two complex FMAs).
-// Each warp carries CPW independent columns to overlap the chains; all warps of a CTA share one T.
+// One column per warp and few warps per CTA spread the independent chains over many SMs (the
+// pieces are issue-latency bound per warp); all warps of a CTA share one copy of T.
 #include "common.cuh"
 #include "kernels.h"
 #include "prof.h"
@@ -21,7 +22,7 @@ namespace feast {
 namespace {
 
 constexpr int NB = 64, LDT = NB + 1;   // T[r][c] at Ts[r * LDT + c]: lanes (rows) 16 B x 65 apart
-constexpr int WARPS = 16;
+constexpr int WARPS = 4;      // warps per CTA; one right-hand-side column per warp (spread over SMs)
 
 __device__ __forceinline__ double2 shfl2(double2 v, int src) {
   return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
@@ -35,22 +36,22 @@ __device__ __forceinline__ double2 opT(const double2* Ts, int r, int c) {
   return make_double2(v.x, -v.y);
 }
 
-// Load the nb x nb block (identity-padded to NB when PAD) into Ts, keeping only op(T)'s triangle
-// (the other triangle of the LU workspace holds the other factor); 1 / diagonal into dinv.
+// Load the nb x nb block into Ts (identity-padded to nbp), all elements in flight at once with
+// cp.async (a latency chain of dependent loads would dominate these microsecond kernels).  The
+// solves read only the strict triangle of op(T) and its diagonal (through dinv), so the other
+// factor stored in the same LU workspace block needs no masking.  1 / diagonal into dinv.
 template <bool LOWER, bool UNIT, bool CONJT>
 __device__ void load_tri(const double2* __restrict__ T, int64_t ld, int nb, int nbp, double2* Ts, double2* dinv) {
   for (int idx = threadIdx.x; idx < nbp * nbp; idx += blockDim.x) {
     const int r = idx % nbp, c = idx / nbp;   // source element T[r][c] (coalesced along r)
-    double2 v = make_double2(r == c ? 1.0 : 0.0, 0.0);
     if (r < nb && c < nb) {
-      // keep the triangle of T whose op() is LOWER/UPPER: op = ^H flips it
-      const bool lower_src = CONJT ? !LOWER : LOWER;
-      const bool keep = lower_src ? (r >= c) : (r <= c);
-      if (keep) v = T[r + (int64_t)c * ld];
-      if (r == c && UNIT) v = make_double2(1.0, 0.0);
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(&Ts[r * LDT + c]);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(T + r + (int64_t)c * ld));
+    } else {
+      Ts[r * LDT + c] = make_double2(r == c ? 1.0 : 0.0, 0.0);
     }
-    Ts[r * LDT + c] = v;
   }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
   if (!UNIT)
     for (int i = threadIdx.x; i < nbp; i += blockDim.x) dinv[i] = crcp(opT<CONJT>(Ts, i, i));
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(32 * WARPS) trsm_warp_kernel(Batched Tb, Batch
 
 template <bool LOWER, bool UNIT, bool CONJT>
 void trsm_t(Batched T, Batched X, int nb, int64_t ncols, int batch, cudaStream_t s) {
-  constexpr int CPW = 2;
+  constexpr int CPW = 1;
   const size_t smem = (size_t)(NB * LDT + NB) * sizeof(double2);
   static bool configured = false;
   if (!configured) {
@@ -138,32 +139,26 @@ void trsm_t(Batched T, Batched X, int nb, int64_t ncols, int batch, cudaStream_t
 
 // ---------------------------------------------------------------- trtri (64x64 diagonal blocks)
 // blockIdx.x = node, blockIdx.y = 0 (L^-1, unit lower) / 1 (U^-1, upper), blockIdx.z = diagonal
-// block index relative to kb0.  Warp w inverts columns w*4 .. w*4+3 (identity right-hand sides;
-// column j of L^-1 is zero above row j, of U^-1 zero below, so the chains start at t = j).
+// block index relative to kb0 times TR_CB column groups.  Each CTA inverts WARPS columns of one
+// block (identity right-hand sides; column j of L^-1 is zero above row j, of U^-1 zero below, so
+// the chains start at t = j), with a CTA per group of columns so the 2 x 64 chains of a node run
+// on many SMs at once.
+constexpr int TR_CB = NB / WARPS;   // column groups per diagonal block
 template <bool UPPER>
 __device__ void trtri_block(const double2* __restrict__ T, int64_t ld, int nb, double2* __restrict__ out,
-                            double2* Ts, double2* dinv) {
-  constexpr int CPW = NB / WARPS;   // 4 columns per warp
+                            double2* Ts, double2* dinv, int cgroup) {
   if (UPPER) load_tri<false, false, false>(T, ld, nb, NB, Ts, dinv);
   else load_tri<true, true, false>(T, ld, nb, NB, Ts, dinv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // columns j = warp + WARPS * c: every warp gets a mix of long and short chains
-  double2 x[CPW][2];
-#pragma unroll
-  for (int c = 0; c < CPW; ++c) {
-    const int j = warp + WARPS * c;
-    x[c][0] = make_double2(lane == j ? 1.0 : 0.0, 0.0);
-    x[c][1] = make_double2(lane + 32 == j ? 1.0 : 0.0, 0.0);
-  }
-  const int jmin = warp, jmax = warp + WARPS * (CPW - 1);
-  if (UPPER) warp_solve<false, false, false, CPW>(Ts, dinv, NB, 0, jmax, x);
-  else warp_solve<true, true, false, CPW>(Ts, dinv, NB, jmin, NB - 1, x);
-#pragma unroll
-  for (int c = 0; c < CPW; ++c) {
-    const int j = warp + WARPS * c;
-    out[lane + j * NB] = x[c][0];
-    out[lane + 32 + j * NB] = x[c][1];
-  }
+  // interleave long and short chains across the CTAs: column j = cgroup + TR_CB * warp
+  const int j = cgroup + TR_CB * warp;
+  double2 x[1][2];
+  x[0][0] = make_double2(lane == j ? 1.0 : 0.0, 0.0);
+  x[0][1] = make_double2(lane + 32 == j ? 1.0 : 0.0, 0.0);
+  if (UPPER) warp_solve<false, false, false, 1>(Ts, dinv, NB, 0, j, x);
+  else warp_solve<true, true, false, 1>(Ts, dinv, NB, j, NB - 1, x);
+  out[lane + j * NB] = x[0][0];
+  out[lane + 32 + j * NB] = x[0][1];
 }
 
 __global__ void __launch_bounds__(32 * WARPS) trtri_kernel(Batched Cb, int64_t n, int64_t kb0,
@@ -174,13 +169,14 @@ __global__ void __launch_bounds__(32 * WARPS) trtri_kernel(Batched Cb, int64_t n
   double2* dinv = sm + NB * LDT;
   const int b = blockIdx.x;
   const int lu = (which == 2) ? (int)blockIdx.y : which;
-  const int64_t kb = kb0 + blockIdx.z;
+  const int64_t kb = kb0 + blockIdx.z / TR_CB;
+  const int cgroup = (int)(blockIdx.z % TR_CB);
   const int64_t o = kb * NB;
   const int nb = (int)((n - o) < NB ? (n - o) : NB);
   const double2* T = Cb.p + (int64_t)b * Cb.stride + o + o * Cb.ld;
   double2* out = inv + (int64_t)b * inv_node_stride + (kb * 2 + lu) * (int64_t)NB * NB;
-  if (lu == 0) trtri_block<false>(T, Cb.ld, nb, out, Ts, dinv);
-  else trtri_block<true>(T, Cb.ld, nb, out, Ts, dinv);
+  if (lu == 0) trtri_block<false>(T, Cb.ld, nb, out, Ts, dinv, cgroup);
+  else trtri_block<true>(T, Cb.ld, nb, out, Ts, dinv, cgroup);
 }
 
 }  // namespace
@@ -211,7 +207,7 @@ void trtri_launch(Batched C, int64_t n, int64_t kb0, int64_t nblocks, double2* i
     cudaFuncSetAttribute(trtri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
-  dim3 grid((unsigned)batch, which == 2 ? 2u : 1u, (unsigned)nblocks);
+  dim3 grid((unsigned)batch, which == 2 ? 2u : 1u, (unsigned)(nblocks * TR_CB));
   trtri_kernel<<<grid, 32 * WARPS, smem, s>>>(C, n, kb0, inv, inv_node_stride, which);
   count_launch();
 }
