@@ -457,7 +457,11 @@ void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, do
                        int cs, cudaStream_t s) {
   const double L_ = (double)(n - k);
   ProfScope ps_(K_PANEL, (double)batch * (4.0 * L_ * w * w - 4.0 * w * (double)w * w / 3.0), 0.0, s);
-  const int64_t Lc = (n + cs - 1) / cs;
+  // Shrink the cluster as the panel gets shorter (L = n - k): the smallest cluster that keeps
+  // <= 2*PT rows per CTA.  Fewer CTAs per column exchange (cs = 1: no DSMEM at all) and fewer SMs
+  // held while the latency-bound panel runs next to the trailing-update GEMMs.
+  while (cs > 1 && (n - k + cs / 2 - 1) / (cs / 2) <= 2 * PT) cs /= 2;
+  const int64_t Lc = (n - k + cs - 1) / cs;
   // register chunk: 8 columns (a 16-column chunk spills at 2 rows per thread)
   if (Lc <= PT) launch_s<1, 8>(C, n, k, w, ipiv, stats, info, batch, cs, s);
   else if (Lc <= 2 * PT) launch_s<2, 8>(C, n, k, w, ipiv, stats, info, batch, cs, s);
