@@ -91,6 +91,21 @@ int feast_init(feast_handle* h, int64_t n, int64_t m0, double c_re, double c_im,
                double aspect, int32_t n_e, int32_t rule, int32_t mode, int32_t b_is_identity,
                int32_t rank, int32_t world, int32_t max_batch, void* cuda_stream);
 
+/* Real-pencil mode (SURVEY NEXT-2b; the paper's real application pencils): when A and B
+ * are real-valued (zero imaginary parts) and the contour is symmetric about the real axis
+ * (c_im = 0), the pole pair {z, conj z} shares one LU, since C(conj z) = conj(C(z)):
+ *     (conj z B - A)^-1 R = conj( (z B - A)^-1 conj(R) ),
+ * so each pair is factored once with the right-hand sides [R | conj R] (left solves alike with
+ * [R_L | conj R_L]) — half the LU work.  Poles on the real axis stay single units.  The
+ * factorisation units are then the orbits: rank ownership, max_batch and feast_nodes' j0/j1
+ * count orbits (orbits % world must be 0).  Must be called before feast_workspace_bytes /
+ * feast_bind_workspace (the augmented block is n x (n + 2 m0) per unit).  Returns FEAST_E_ARG if
+ * the contour is not symmetric or the poles do not pair up, FEAST_E_STATE after the workspace
+ * is bound or with the factor cache on.  Every projector call checks the premise on the device:
+ * FEAST_E_ARG ("A or B has a nonzero imaginary part") and Q invalid if it fails.
+ * enable = 0 restores per-node factorisation. */
+int feast_set_real_pencil(feast_handle h, int32_t enable);
+
 /* Device workspace size in bytes for this handle (caller allocates, e.g. with torch). */
 int feast_workspace_bytes(feast_handle h, size_t* bytes);
 
@@ -98,7 +113,9 @@ int feast_workspace_bytes(feast_handle h, size_t* bytes);
 int feast_bind_workspace(feast_handle h, void* dev_ptr, size_t bytes);
 
 /* Quadrature data (host outputs): *q; z, w = 2*q doubles each (complex interleaved poles
- * z_j and weights w_j); *j0, *j1 = this rank's owned node range.  Any pointer may be NULL. */
+ * z_j and weights w_j); *j0, *j1 = this rank's owned range of factorisation units (nodes; in
+ * real-pencil mode, conjugate-pole orbits in increasing primary-node order).  Any pointer may
+ * be NULL. */
 int feast_nodes(feast_handle h, int32_t* q, double* z, double* w, int32_t* j0, int32_t* j1);
 
 /* Right projector, this rank's partial sum (eq. Rasp):

@@ -29,8 +29,17 @@ struct feast_ctx {
   double c_re = 0, c_im = 0, r = 0, aspect = 1;
   int n_e = 0, rule = 0, mode = 0;
   bool b_id = true;
-  int rank = 0, world = 1, q = 0, j0 = 0, j1 = 0, batch = 1;
+  int rank = 0, world = 1, q = 0, j0 = 0, j1 = 0, batch = 1, max_batch = 0;
   std::vector<double2> z, w;
+  // Factorisation UNITS: the nodes, or in real-pencil mode (NEXT-2b) the orbits {z, conj z} of
+  // conjugate poles, which share one LU (C(conj z) = conj(C(z)) for real A, B).  j0/j1 and the
+  // batches index units.  Per unit: pole zu (primary node), weight wu, partner weight wpu (0 if
+  // the pole is real), primary node unode, partner node upart (-1).
+  bool real = false;
+  int nu = 0;
+  int64_t mr = 0;                     // right-hand-side columns per unit: m0, or 2 m0 ([R | conj R])
+  std::vector<double2> zu, wu, wpu;
+  std::vector<int> unode, upart;
   cudaStream_t stream = nullptr;      // the library's own stream (capturable into CUDA graphs)
   cudaStream_t caller = nullptr;      // the caller's stream: every call is ordered after / before it
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -60,6 +69,8 @@ struct feast_ctx {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   double2 *Cw = nullptr, *Y = nullptr, *YL = nullptr, *R = nullptr, *RL = nullptr, *zd = nullptr, *wd = nullptr;
+  double2* wpd = nullptr;             // partner weights per unit (real-pencil mode)
+  int32_t* realviol = nullptr;        // device flag: A or B not real (real-pencil mode)
   double2 *AQ = nullptr, *BQ = nullptr, *SK = nullptr;
   double2* Inv = nullptr;          // batch x nblk x {L^-1, U^-1} 64x64 diagonal-block inverses
   int64_t inv_stride = 0, nblk = 0;
@@ -293,7 +304,7 @@ void gemm_gen(feast_ctx* h, int64_t M, int64_t N, int64_t K, bool conjA, const d
 
 // ---------------------------------------------------------------- blocked LU (batched)
 void panel_at(feast_ctx* h, const Lu& v, int64_t k, int w, cudaStream_t s) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0);
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr);
   if (h->smem_cs)
     feast::panel_smem_launch(bat(v.Cw, ld, st), n, k, w, v.ipiv, v.stats, v.info, v.nbat, h->smem_cs, s);
   else
@@ -312,7 +323,7 @@ void panel_at(feast_ctx* h, const Lu& v, int64_t k, int w, cudaStream_t s) {
 // aug > 0: columns [n, n + aug) hold R, so swaps, U12 and updates also perform the forward
 // substitution L^-1 P R.
 void factor_block(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, cudaStream_t s) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0);
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr);
   double2* C = v.Cw;
   const int nbat = v.nbat;
   const int64_t wp = h->smem_cs ? h->wp : 64;
@@ -354,7 +365,7 @@ void factor_block(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, cudaStream_
 // U12 = L11^-1 A12 and A22 -= L21 U12 for the columns [c0, c0 + nc) of outer block (K0, Wo).
 void outer_update(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, int64_t c0, int64_t nc, cudaStream_t s) {
   if (nc <= 0) return;
-  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0), K1 = K0 + Wo;
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), K1 = K0 + Wo;
   double2* C = v.Cw;
   const int nbat = v.nbat;
   for (int64_t ki = K0; ki < K1; ki += 64) {
@@ -376,7 +387,7 @@ void outer_update(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, int64_t c0,
 }
 
 void lu_batched(feast_ctx* h, const Lu& v, int64_t aug) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0), ntot = n + aug;
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), ntot = n + aug;
   double2* C = v.Cw;
   const int nbat = v.nbat;
   cudaStream_t sm = v.sm, sp = v.sp;
@@ -413,14 +424,14 @@ void lu_batched(feast_ctx* h, const Lu& v, int64_t aug) {
 // Y_k <- op(T_kk^-1) Y_k in place (M = w <= 64): which 0 = L^-1, 1 = U^-1; conj: (.)^H
 void diag_apply(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t k, int w, int which, bool conj) {
   const int64_t ld = h->ldc;
-  ZgemmArgs p{w, h->m0, w, inv_ptr(v, k / 64, which), 64, h->inv_stride, Y + k, ld, sy, Y + k, ld, sy,
+  ZgemmArgs p{w, h->mr, w, inv_ptr(v, k / 64, which), 64, h->inv_stride, Y + k, ld, sy, Y + k, ld, sy,
               make_double2(1, 0), make_double2(0, 0), v.nbat, 1};
   feast::zgemm_launch(p, conj, feast::ZG_GEN, v.sm);
 }
 
 // Y <- L^-1 Y (Y already row-permuted): used when the factors are cached (no augmented LU)
 void solve_right_fwd(feast_ctx* h, const Lu& v, double2* Y, int64_t sy) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0), m = h->m0;
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), m = h->mr;
   double2* C = v.Cw;
   for (int64_t k = 0; k < n; k += h->nb) {
     const int w = (int)std::min<int64_t>(h->nb, n - k);
@@ -436,7 +447,7 @@ void solve_right_fwd(feast_ctx* h, const Lu& v, double2* Y, int64_t sy) {
 
 // Y <- U^-1 Y  (Y = L^-1 P R already: the forward substitution ran inside the augmented LU)
 void solve_right_back(feast_ctx* h, const Lu& v, double2* Y, int64_t sy) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0), m = h->m0;
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), m = h->mr;
   double2* C = v.Cw;
   const int64_t last = ((n - 1) / h->nb) * h->nb;
   for (int64_t k = last; k >= 0; k -= h->nb) {
@@ -452,7 +463,7 @@ void solve_right_back(feast_ctx* h, const Lu& v, double2* Y, int64_t sy) {
 
 // Y <- L^-H U^-H Y   (then the caller applies P^T): M^H = U^H L^H P  (P:438-439 same factors)
 void solve_left(feast_ctx* h, const Lu& v, double2* Y) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->m0), m = h->m0, sy = ld * m;
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), m = h->mr, sy = ld * m;
   double2* C = v.Cw;
   for (int64_t k = 0; k < n; k += h->nb) {  // U^H: lower, non-unit
     const int w = (int)std::min<int64_t>(h->nb, n - k);
@@ -503,7 +514,14 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
     if (doL) { gemm_gen(h, n, m, n, true, B, ldb, V, ldv, h->RL, ld, one, zero); Rl = h->RL; ldrl = ld; }
   }
   const int owned = h->j1 - h->j0;
-  const int64_t st = ld * (n + m);
+  const int64_t mr = h->mr, st = ld * (n + mr);
+  const bool pair = h->real;          // units are conjugate-pole orbits: RHS [R | conj R]
+  const double2* wp = pair ? h->wpd : nullptr;
+  if (pair && owned > 0) {            // the real-pencil premise, checked on the device
+    cudaMemsetAsync(h->realviol, 0, 4, h->stream);
+    feast::imag_check_launch(A, lda, n, h->realviol, h->stream);
+    if (!h->b_id) feast::imag_check_launch(B, ldb, n, h->realviol, h->stream);
+  }
   for (int jb = 0; jb < owned; jb += h->batch) {
     const int nbat = std::min(h->batch, owned - jb);
     const int j = h->j0 + jb;
@@ -520,24 +538,24 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
         feast::stats_init_launch(v.stats, v.info, v.nbat, v.sm);
         // a2: C_j = z_j B - A ; R appended as extra columns (augmented system [C_j | R])
         feast::shift_launch(bat(v.Cw, ld, st), A, lda, B, ldb, h->zd + j + b0, n, v.nbat, v.sm);
-        if (doR) feast::broadcast_copy_launch(bat(v.Cw + n * ld, ld, st), Rr, ldr, n, m, v.nbat, v.sm);
+        if (doR) feast::broadcast_copy_launch(bat(v.Cw + n * ld, ld, st), Rr, ldr, n, m, v.nbat, pair, v.sm);
         // a3 (+ forward substitution of a4): P_j [C_j | R] -> [U_j | L_j^-1 P_j R]
-        lu_batched(h, v, doR ? m : 0);
+        lu_batched(h, v, doR ? mr : 0);
         if (doL || h->cache_on)
           feast::perm_launch(v.ipiv, h->perm + (int64_t)b0 * n, h->iperm + (int64_t)b0 * n, n, v.nbat, v.sm);
         // a4: Y_j = U_j^-1 (L_j^-1 P_j R)
         if (doR) solve_right_back(h, v, v.Cw + n * ld, st);
       } else if (doR) {
         // cached factors (NEXT-1, "factored just once"): Y_j = U^-1 L^-1 P_j R
-        double2* Yg = h->Y + b0 * ld * m;
-        feast::gather_rows_launch(bat(Yg, ld, ld * m), Rr, ldr, 0, h->perm + (int64_t)b0 * n, n, m, v.nbat, v.sm);
-        solve_right_fwd(h, v, Yg, ld * m);
-        solve_right_back(h, v, Yg, ld * m);
+        double2* Yg = h->Y + b0 * ld * mr;   // (factor cache and real-pencil mode are exclusive: mr = m)
+        feast::gather_rows_launch(bat(Yg, ld, ld * mr), Rr, ldr, 0, h->perm + (int64_t)b0 * n, n, m, v.nbat, v.sm);
+        solve_right_fwd(h, v, Yg, ld * mr);
+        solve_right_back(h, v, Yg, ld * mr);
       }
       if (doL) {
         // Z_j = P^T L^-H U^-H RL  (P^T folded into the accumulate below)
-        double2* Yg = h->YL + b0 * ld * m;
-        feast::broadcast_copy_launch(bat(Yg, ld, ld * m), Rl, ldrl, n, m, v.nbat, v.sm);
+        double2* Yg = h->YL + b0 * ld * mr;
+        feast::broadcast_copy_launch(bat(Yg, ld, ld * mr), Rl, ldrl, n, m, v.nbat, pair, v.sm);
         solve_left(h, v, Yg);
       }
       if (g) {
@@ -546,15 +564,18 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
       }
     }
     // a5: Q (+)= sum_j w_j Y_j, QL (+)= sum_j conj(w_j) Z_j over the batch in node order
+    const double2* wpj = wp ? wp + j : nullptr;
     if (doR) {
       if (!reuse)
-        feast::accum_launch(Q, ldq, bat(h->Cw + n * ld, ld, st), h->wd + j, nullptr, n, m, nbat, false, jb > 0,
+        feast::accum_launch(Q, ldq, bat(h->Cw + n * ld, ld, st), h->wd + j, wpj, nullptr, n, m, nbat, false, jb > 0,
                             h->stream);
       else
-        feast::accum_launch(Q, ldq, bat(h->Y, ld, ld * m), h->wd + j, nullptr, n, m, nbat, false, jb > 0, h->stream);
+        feast::accum_launch(Q, ldq, bat(h->Y, ld, ld * mr), h->wd + j, wpj, nullptr, n, m, nbat, false, jb > 0,
+                            h->stream);
     }
     if (doL)
-      feast::accum_launch(QL, ldql, bat(h->YL, ld, ld * m), h->wd + j, h->iperm, n, m, nbat, true, jb > 0, h->stream);
+      feast::accum_launch(QL, ldql, bat(h->YL, ld, ld * mr), h->wd + j, wpj, h->iperm, n, m, nbat, true, jb > 0,
+                          h->stream);
   }
   if (owned == 0) {
     if (doR) cudaMemset2DAsync(Q, ldq * 16, 0, n * 16, m, h->stream);
@@ -606,21 +627,26 @@ int project_impl(feast_ctx* h, const double2* A, int64_t lda, const double2* B, 
   if (!reuse && h->cache_on && h->batch >= owned) { h->cache_valid = true; h->cache_A = A; h->cache_B = B; }
   CUDA_TRY(h, cudaGetLastError());
   h->launches = feast::g_launches - t0;
-  // pivot diagnostics of the owned nodes
-  std::vector<double> st(2 * (size_t)h->q);
-  std::vector<int32_t> inf(h->q);
+  // pivot diagnostics of the owned units, reported per node (both poles of an orbit share it)
+  std::vector<double> st(2 * (size_t)h->nu);
+  std::vector<int32_t> inf(h->nu);
+  int32_t viol = 0;
   CUDA_TRY(h, cudaMemcpyAsync(st.data(), h->stats, st.size() * 8, cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(h, cudaMemcpyAsync(inf.data(), h->info, inf.size() * 4, cudaMemcpyDeviceToHost, h->stream));
+  if (h->real) CUDA_TRY(h, cudaMemcpyAsync(&viol, h->realviol, 4, cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  if (viol) return fail(h, FEAST_E_ARG, "real-pencil mode: A or B has a nonzero imaginary part%s");
   h->minrel.assign(h->q, -1.0);
   h->worst = -1;
   double wr = INFINITY;
   bool singular = false, ill = false;
-  for (int jj = h->j0; jj < h->j1; ++jj) {
-    const double ratio = st[2 * jj + 1] > 0 ? st[2 * jj] / st[2 * jj + 1] : 0.0;
-    h->minrel[jj] = inf[jj] ? 0.0 : ratio;
+  for (int u = h->j0; u < h->j1; ++u) {
+    const double ratio = st[2 * u + 1] > 0 ? st[2 * u] / st[2 * u + 1] : 0.0;
+    const int jj = h->unode[u];
+    h->minrel[jj] = inf[u] ? 0.0 : ratio;
+    if (h->upart[u] >= 0) h->minrel[h->upart[u]] = h->minrel[jj];
     if (h->minrel[jj] < wr) { wr = h->minrel[jj]; h->worst = jj; }
-    if (inf[jj] || ratio < 1e-14) singular = true;
+    if (inf[u] || ratio < 1e-14) singular = true;
     else if (ratio < 1e-10) ill = true;
   }
   if (singular) {
@@ -687,6 +713,45 @@ int ensure_iter_mem(feast_ctx* h) {
   return FEAST_OK;
 }
 
+// Factorisation units and their ownership (reading R17 applied to units): plain nodes, or in
+// real-pencil mode the orbits of conjugate poles {z, conj z} (NEXT-2b; P:899-905 / S:282, S:291:
+// for real A, B, C(conj z) = conj(C(z)), so the partner's solve is conj(C(z)^-1 conj R)).
+int setup_units(feast_ctx* h) {
+  h->zu.clear(); h->wu.clear(); h->wpu.clear(); h->unode.clear(); h->upart.clear();
+  if (!h->real) {
+    h->zu = h->z; h->wu = h->w;
+    for (int j = 0; j < h->q; ++j) { h->unode.push_back(j); h->upart.push_back(-1); }
+  } else {
+    const double tol = 1e-12 * h->r;
+    std::vector<bool> taken(h->q, false);
+    for (int j = 0; j < h->q; ++j) {
+      if (h->z[j].y < -tol) continue;        // lower half plane: a partner, found below
+      int p = -1;
+      if (h->z[j].y > tol)
+        for (int k = 0; k < h->q; ++k)
+          if (!taken[k] && h->z[k].y < -tol && std::fabs(h->z[k].x - h->z[j].x) <= tol &&
+              std::fabs(h->z[k].y + h->z[j].y) <= tol) { p = k; break; }
+      if (h->z[j].y > tol && p < 0) return -1;   // contour not symmetric about the real axis
+      if (p >= 0) taken[p] = true;
+      h->zu.push_back(h->z[j]);
+      h->wu.push_back(h->w[j]);
+      h->wpu.push_back(p >= 0 ? h->w[p] : make_double2(0.0, 0.0));
+      h->unode.push_back(j);
+      h->upart.push_back(p);
+    }
+    for (int k = 0; k < h->q; ++k)
+      if (h->z[k].y < -tol && !taken[k]) return -1;
+  }
+  h->nu = (int)h->zu.size();
+  if (h->nu % h->world != 0) return -1;
+  h->j0 = h->rank * (h->nu / h->world);
+  h->j1 = (h->rank + 1) * (h->nu / h->world);
+  const int owned = h->j1 - h->j0;
+  h->batch = std::max(1, h->max_batch == 0 ? owned : std::min<int>(h->max_batch, owned));
+  h->mr = h->real ? 2 * h->m0 : h->m0;
+  return 0;
+}
+
 }  // namespace
 
 // ================================================================== C ABI
@@ -707,11 +772,8 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   h->n_e = n_e; h->rule = rule; h->mode = mode; h->b_id = b_is_identity != 0;
   h->rank = rank; h->world = world;
   h->stream = h->caller = (cudaStream_t)cuda_stream;
-  if (make_nodes(h) != 0 || h->q % world != 0) { delete h; return FEAST_E_ARG; }
-  h->j0 = rank * (h->q / world);
-  h->j1 = (rank + 1) * (h->q / world);
-  const int owned = h->j1 - h->j0;
-  h->batch = std::max(1, max_batch == 0 ? owned : std::min<int>(max_batch, owned));
+  h->max_batch = max_batch;
+  if (make_nodes(h) != 0 || h->q % world != 0 || setup_units(h) != 0) { delete h; return FEAST_E_ARG; }
   h->pcfg = feast::panel_config(n);
   if (h->pcfg.cluster == 0) { delete h; return FEAST_E_ARG; }
   // panel strategy: shared-memory cluster panel when the n x nb panel fits in <= 16 CTAs
@@ -740,7 +802,7 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   }
   if (const char* e = getenv("FEAST_NBO")) {
     const long v = atol(e);
-    if (v >= 64 && v <= 256 && v % 64 == 0) h->nbo = v;
+    if (v >= 64 && v <= 1024 && v % 64 == 0) h->nbo = v;
   }
   {
     int lo = 0, hi = 0;
@@ -779,9 +841,10 @@ static size_t layout(feast_ctx* h, char* base) {
   const int64_t n = h->n, m = h->m0, ld = h->ldc;
   size_t off = 0;
   auto take = [&](size_t b) { size_t o = off; off += align256(b); return base ? (void*)(base + o) : nullptr; };
-  h->Cw = (double2*)take((size_t)h->batch * ld * (n + m) * 16);   // [C_j | R] (augmented)
-  h->Y = (double2*)take((size_t)h->batch * ld * m * 16);             // right solves with cached factors
-  h->YL = h->mode == FEAST_BI ? (double2*)take((size_t)h->batch * ld * m * 16) : nullptr;
+  const int64_t mr = h->mr;
+  h->Cw = (double2*)take((size_t)h->batch * ld * (n + mr) * 16);  // [C_j | R (| conj R)] (augmented)
+  h->Y = (double2*)take((size_t)h->batch * ld * mr * 16);            // right solves with cached factors
+  h->YL = h->mode == FEAST_BI ? (double2*)take((size_t)h->batch * ld * mr * 16) : nullptr;
   h->R = !h->b_id ? (double2*)take((size_t)ld * m * 16) : nullptr;
   h->RL = (!h->b_id && h->mode == FEAST_BI) ? (double2*)take((size_t)ld * m * 16) : nullptr;
   h->AQ = (double2*)take((size_t)ld * m * 16);
@@ -794,10 +857,12 @@ static size_t layout(feast_ctx* h, char* base) {
   h->ipiv = (int32_t*)take((size_t)h->batch * n * 4);
   h->perm = (int32_t*)take((size_t)h->batch * n * 4);
   h->iperm = (int32_t*)take((size_t)h->batch * n * 4);
-  h->zd = (double2*)take((size_t)h->q * 16);
-  h->wd = (double2*)take((size_t)h->q * 16);
-  h->stats = (double*)take((size_t)h->q * 16);
-  h->info = (int32_t*)take((size_t)h->q * 4);
+  h->zd = (double2*)take((size_t)h->nu * 16);
+  h->wd = (double2*)take((size_t)h->nu * 16);
+  h->wpd = h->real ? (double2*)take((size_t)h->nu * 16) : nullptr;
+  h->stats = (double*)take((size_t)h->nu * 16);
+  h->info = (int32_t*)take((size_t)h->nu * 4);
+  h->realviol = (int32_t*)take(16);
   return off;
 }
 
@@ -816,8 +881,10 @@ int feast_bind_workspace(feast_handle h, void* p, size_t bytes) {
   h->ws = p;
   h->ws_bytes = bytes;
   layout(h, (char*)p);
-  CUDA_TRY(h, cudaMemcpyAsync(h->zd, h->z.data(), h->q * 16, cudaMemcpyHostToDevice, h->stream));
-  CUDA_TRY(h, cudaMemcpyAsync(h->wd, h->w.data(), h->q * 16, cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(h->zd, h->zu.data(), h->nu * 16, cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(h->wd, h->wu.data(), h->nu * 16, cudaMemcpyHostToDevice, h->stream));
+  if (h->real)
+    CUDA_TRY(h, cudaMemcpyAsync(h->wpd, h->wpu.data(), h->nu * 16, cudaMemcpyHostToDevice, h->stream));
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   return FEAST_OK;
 }
@@ -1014,12 +1081,27 @@ int64_t feast_last_launch_count(feast_handle h) { return h ? h->launches : 0; }
 
 int feast_factor_cache(feast_handle h, int32_t enable) {
   if (!h) return FEAST_E_ARG;
+  if (enable && h->real) return fail(h, FEAST_E_STATE, "factor cache is not combined with real-pencil mode%s");
   graph_reset(h);
   h->cache_on = enable != 0;
   h->cache_valid = false;
   h->cache_A = h->cache_B = nullptr;
   if (h->cache_on && h->batch < h->j1 - h->j0)
     return fail(h, FEAST_E_NOMEM, "factor cache needs max_batch >= owned nodes (all factors resident)%s");
+  return FEAST_OK;
+}
+
+int feast_set_real_pencil(feast_handle h, int32_t enable) {
+  if (!h) return FEAST_E_ARG;
+  if (h->ws) return fail(h, FEAST_E_STATE, "feast_set_real_pencil must precede feast_workspace_bytes/bind%s");
+  if (enable && h->cache_on) return fail(h, FEAST_E_STATE, "factor cache is not combined with real-pencil mode%s");
+  if (enable && h->c_im != 0.0) return fail(h, FEAST_E_ARG, "real-pencil mode needs a contour centre on the real axis%s");
+  h->real = enable != 0;
+  if (setup_units(h) != 0) {
+    h->real = false;
+    setup_units(h);
+    return fail(h, FEAST_E_ARG, "real-pencil mode: poles do not pair up or units %% world != 0%s");
+  }
   return FEAST_OK;
 }
 

@@ -355,11 +355,11 @@ void stats_init_launch(double* stats, int32_t* info, int batch, cudaStream_t s) 
 }
 
 // ============================================================================ laswp
-// Apply the cnt (<= 256) sequential swaps ipiv[k..k+cnt) to the columns [c0, c1) of every
+// Apply the cnt (<= 1024) sequential swaps ipiv[k..k+cnt) to the columns [c0, c1) of every
 // matrix.  Thread per column; each swap exchanges two 16-byte complex entries.
 __global__ void laswp_kernel(Batched C, int64_t n, int64_t k, int cnt, const int32_t* __restrict__ ipiv_all,
                              int64_t c0, int64_t c1) {
-  __shared__ int32_t pv[256];
+  __shared__ int32_t pv[1024];
   const int b = blockIdx.y;
   const int32_t* ipiv = ipiv_all + (int64_t)b * n;
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) pv[i] = ipiv[k + i];
@@ -464,28 +464,58 @@ void scatter_rows_launch(Batched Out, const double2* Y, int64_t ldy, int64_t sY,
   count_launch();
 }
 
-__global__ void broadcast_copy_kernel(Batched Y, const double2* __restrict__ R, int64_t ldr, int64_t n) {
+// Y_b[:, c] = R[:, c] (c < m) and, with pair_conj, Y_b[:, m + c] = conj(R[:, c]): the
+// right-hand sides [R | conj(R)] of a conjugate-pole pair of a real pencil (one LU, both poles).
+__global__ void broadcast_copy_kernel(Batched Y, const double2* __restrict__ R, int64_t ldr, int64_t n, int64_t m) {
   const int b = blockIdx.z;
-  const int64_t c = blockIdx.y;
+  const int64_t cc = blockIdx.y;
+  const bool cj = cc >= m;
+  const int64_t c = cj ? cc - m : cc;
   const double2* Rc = R + c * ldr;
-  double2* Yc = Y.p + (int64_t)b * Y.stride + c * Y.ld;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    Yc[i] = Rc[i];
+  double2* Yc = Y.p + (int64_t)b * Y.stride + cc * Y.ld;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = Rc[i];
+    Yc[i] = cj ? cconj(v) : v;
+  }
 }
 
-void broadcast_copy_launch(Batched Y, const double2* R, int64_t ldr, int64_t n, int64_t m, int batch,
+void broadcast_copy_launch(Batched Y, const double2* R, int64_t ldr, int64_t n, int64_t m, int batch, bool pair_conj,
                            cudaStream_t s) {
-  ProfScope ps_(K_PERM, 0.0, (double)batch * n * m * 32.0, s);
+  const int64_t cols = pair_conj ? 2 * m : m;
+  ProfScope ps_(K_PERM, 0.0, (double)batch * n * cols * 32.0, s);
   unsigned gx = (unsigned)((n + 255) / 256);
   if (gx > 16) gx = 16;
-  broadcast_copy_kernel<<<dim3(gx, (unsigned)m, (unsigned)batch), 256, 0, s>>>(Y, R, ldr, n);
+  broadcast_copy_kernel<<<dim3(gx, (unsigned)cols, (unsigned)batch), 256, 0, s>>>(Y, R, ldr, n, m);
+  count_launch();
+}
+
+// flag[0] |= 1 if any entry of the n x n matrix M has a nonzero imaginary part (real-pencil check)
+__global__ void imag_check_kernel(const double2* __restrict__ M, int64_t ld, int64_t n, int32_t* flag) {
+  const int64_t c = blockIdx.y;
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    bad |= M[i + c * ld].y != 0.0;
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+void imag_check_launch(const double2* M, int64_t ld, int64_t n, int32_t* flag, cudaStream_t s) {
+  ProfScope ps_(K_OTHER, 0.0, (double)n * n * 16.0, s);
+  unsigned gx = (unsigned)((n + 255) / 256);
+  if (gx > 8) gx = 8;
+  imag_check_kernel<<<dim3(gx, (unsigned)n), 256, 0, s>>>(M, ld, n, flag);
   count_launch();
 }
 
 // ============================================================================ accumulate
-// Q (+)= sum_b w_b Y_b in increasing b (deterministic, eq. Rasp sum).
+// Q (+)= sum_b w_b Y_b in increasing b (deterministic, eq. Rasp sum).  With wp
+// (conjugate-pole pairs of a real pencil): + wp_b conj(Y_b[:, m + c]), the partner pole's solve
+// C(conj z)^-1 R = conj(C(z)^-1 conj(R)).
+__device__ __forceinline__ double2 cfma(double2 w, double2 y, double2 acc) {
+  return make_double2(fma(w.x, y.x, fma(-w.y, y.y, acc.x)), fma(w.x, y.y, fma(w.y, y.x, acc.y)));
+}
 __global__ void accum_kernel(double2* __restrict__ Q, int64_t ldq, Batched Y, const double2* __restrict__ w,
-                             const int32_t* __restrict__ iperm, int64_t n, int batch, bool conjw, bool accumulate) {
+                             const double2* __restrict__ wp, const int32_t* __restrict__ iperm, int64_t n, int64_t m,
+                             int batch, bool conjw, bool accumulate) {
   const int64_t c = blockIdx.y;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double2 acc = accumulate ? Q[i + c * ldq] : make_double2(0.0, 0.0);
@@ -493,19 +523,26 @@ __global__ void accum_kernel(double2* __restrict__ Q, int64_t ldq, Batched Y, co
       double2 wb = w[b];
       if (conjw) wb = cconj(wb);
       const int64_t src = iperm ? (int64_t)iperm[(int64_t)b * n + i] : i;
-      const double2 y = Y.p[(int64_t)b * Y.stride + c * Y.ld + src];
-      acc = make_double2(fma(wb.x, y.x, fma(-wb.y, y.y, acc.x)), fma(wb.x, y.y, fma(wb.y, y.x, acc.y)));
+      const double2* Yb = Y.p + (int64_t)b * Y.stride + src;
+      acc = cfma(wb, Yb[c * Y.ld], acc);
+      if (wp) {
+        double2 wq = wp[b];
+        if (conjw) wq = cconj(wq);
+        acc = cfma(wq, cconj(Yb[(m + c) * Y.ld]), acc);
+      }
     }
     Q[i + c * ldq] = acc;
   }
 }
 
-void accum_launch(double2* Q, int64_t ldq, Batched Y, const double2* w, const int32_t* iperm, int64_t n, int64_t m,
-                  int batch, bool conjw, bool accumulate, cudaStream_t s) {
-  ProfScope ps_(K_ACCUM, (double)batch * n * m * 8.0, (double)(batch + (accumulate ? 2 : 1)) * n * m * 16.0, s);
+void accum_launch(double2* Q, int64_t ldq, Batched Y, const double2* w, const double2* wp, const int32_t* iperm,
+                  int64_t n, int64_t m, int batch, bool conjw, bool accumulate, cudaStream_t s) {
+  const int parts = wp ? 2 : 1;
+  ProfScope ps_(K_ACCUM, (double)batch * parts * n * m * 8.0,
+                (double)(batch * parts + (accumulate ? 2 : 1)) * n * m * 16.0, s);
   unsigned gx = (unsigned)((n + 255) / 256);
   if (gx > 16) gx = 16;
-  accum_kernel<<<dim3(gx, (unsigned)m), 256, 0, s>>>(Q, ldq, Y, w, iperm, n, batch, conjw, accumulate);
+  accum_kernel<<<dim3(gx, (unsigned)m), 256, 0, s>>>(Q, ldq, Y, w, wp, iperm, n, m, batch, conjw, accumulate);
   count_launch();
 }
 

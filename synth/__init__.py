@@ -51,6 +51,10 @@ class ConfigSpec:
     def b_is_identity(self) -> bool:
         return self.kind in ("std", "bi")
 
+    @property
+    def real_pencil(self) -> bool:
+        return self.kind == "gen_real"
+
 
 # BASELINE.json configs[0..4] (C1..C5)
 CONFIGS = {
@@ -59,6 +63,13 @@ CONFIGS = {
     "C3": ConfigSpec("C3", 8192, 256, "csym", 0j, 0.4, 0.15, 16, RULE_GAUSS_LEGENDRE, "right", 6, 0.0, 0.01, "none"),
     "C4": ConfigSpec("C4", 16384, 512, "bi", 0.5 + 0j, 0.25, 1.0, 32, RULE_TRAPEZOID, "bi", 5, 0.05, 0.0, "rect2x1"),
     "C5": ConfigSpec("C5", 32768, 1024, "gen", 0j, 0.2, 1.0, 16, RULE_TRAPEZOID, "right", 4, 0.05, 0.005, "disk1"),
+    # Companion (NOT a BASELINE config): a REAL generalized pencil of C2's size, standing in for the
+    # paper's real non-symmetric application pencils; contour centred on the real axis so the
+    # poles come in conjugate pairs (real-pencil mode, SURVEY NEXT-2b).  B = I + 0.01 G_B/sqrt(n),
+    # V = I + 0.1 G/sqrt(n) with REAL Gaussians; eigenvalues in conjugate pairs a +- ib, (a, b)
+    # uniform in the upper half of the unit disk; A = B V Lr V^-1 with Lr = blockdiag([[a, b], [-b, a]]).
+    "R2": ConfigSpec("R2", 2048, 128, "gen_real", 0.2 + 0j, 0.3, 1.0, 16, RULE_TRAPEZOID, "right", 8, 0.1, 0.01,
+                     "pairs_disk1"),
 }
 
 
@@ -88,11 +99,38 @@ def make_pencil(key: str, n: int | None = None, m0: int | None = None, seed_offs
     spec = CONFIGS[key]
     n = spec.n if n is None else int(n)
     m0 = spec.m0 if m0 is None else int(m0)
-    k = int(key[1:]) - 1
+    k = int(key[1:]) - 1 + (100 if key.startswith("R") else 0)
     ss = np.random.SeedSequence(SEED_BASE + k + 1000 * seed_offset)
     r_lam, r_v, r_b, r_x = (np.random.Generator(np.random.PCG64(s)) for s in ss.spawn(4))
     sq = math.sqrt(n)
     lam = V = None
+    if spec.kind == "gen_real":
+        if n % 2:
+            raise ValueError("gen_real needs an even n (conjugate eigenvalue pairs)")
+        h = n // 2
+        rr = np.sqrt(r_lam.uniform(0, 1, h))
+        th = math.pi * r_lam.uniform(0, 1, h)
+        a, b = rr * np.cos(th), rr * np.sin(th)
+        Vr = np.eye(n) + spec.vscale * r_v.standard_normal((n, n)) / sq
+        Lr = np.zeros((n, n))
+        idx = np.arange(h)
+        Lr[2 * idx, 2 * idx] = a
+        Lr[2 * idx + 1, 2 * idx + 1] = a
+        Lr[2 * idx, 2 * idx + 1] = b
+        Lr[2 * idx + 1, 2 * idx] = -b
+        M = np.linalg.solve(Vr.T, (Vr @ Lr).T).T          # V Lr V^-1 (library solve)
+        Br = np.eye(n) + spec.bscale * r_b.standard_normal((n, n)) / sq
+        A = np.asfortranarray((Br @ M).astype(np.complex128))
+        B = np.asfortranarray(Br.astype(np.complex128))
+        lam = np.empty(n, dtype=np.complex128)
+        lam[0::2] = a + 1j * b
+        lam[1::2] = a - 1j * b
+        V = np.empty((n, n), dtype=np.complex128)           # eigenvectors of B^-1 A: V [1, +-i]
+        V[:, 0::2] = Vr[:, 0::2] + 1j * Vr[:, 1::2]
+        V[:, 1::2] = Vr[:, 0::2] - 1j * Vr[:, 1::2]
+        V = np.asfortranarray(V)
+        X0 = np.asfortranarray(_cn(r_x, (n, m0)))
+        return Pencil(spec, n, m0, A, B, X0, lam, V)
     if spec.kind == "csym":
         gh = r_b.standard_normal((n, n))
         H = (gh + gh.T) / (2.0 * sq)

@@ -105,3 +105,24 @@ def test_library_has_no_static_tls():
     out = subprocess.run(["readelf", "-d", fb.LIB_PATH], capture_output=True, text=True).stdout
     assert "STATIC_TLS" not in out
     assert "libcudart.so" in out
+
+
+def test_real_pencil_units_and_guards():
+    """feast_set_real_pencil: conjugate-pole orbits become the factorisation units (host logic,
+    no GPU); refused for a contour off the real axis and after the workspace is bound."""
+    lib = fb.load_library()
+    rc, h = _init(n=64, m0=8, c=0.2 + 0j, n_e=16, rule=0, world=2, rank=1)
+    assert rc == 0
+    assert lib.feast_set_real_pencil(h, 1) == 0
+    q, j0, j1 = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    lib.feast_nodes(h, ctypes.byref(q), None, None, ctypes.byref(j0), ctypes.byref(j1))
+    assert (q.value, j0.value, j1.value) == (16, 4, 8)       # 8 orbits over 2 ranks
+    lib.feast_destroy(h)
+    rc, h = _init(n=64, m0=8, c=0.2 + 0.1j, n_e=16, rule=0)
+    assert lib.feast_set_real_pencil(h, 1) == -1             # FEAST_E_ARG: not symmetric
+    lib.feast_destroy(h)
+    rc, h = _init(n=64, m0=8, c=0.0 + 0j, n_e=4, rule=1)     # endpoint rule: real poles +-1
+    assert lib.feast_set_real_pencil(h, 1) == 0
+    lib.feast_nodes(h, ctypes.byref(q), None, None, ctypes.byref(j0), ctypes.byref(j1))
+    assert (q.value, j1.value - j0.value) == (4, 3)          # {1}, {i, -i}, {-1}
+    lib.feast_destroy(h)

@@ -202,3 +202,49 @@ def test_graph_replay_reads_current_inputs():
         launches.append(f.last_launch_count)
         assert rel(host(Q), oracle.project(Ah, P.B, Xh, z, w)) <= TOL, it
     assert len(set(launches)) == 1   # the replayed graph holds the same kernels
+
+
+@pytest.mark.parametrize("rule,n_e,aspect,n", [(synth.RULE_TRAPEZOID, 16, 1.0, 260),
+                                               (synth.RULE_TRAPEZOID_ENDPOINT, 8, 1.0, 200),
+                                               (synth.RULE_GAUSS_LEGENDRE, 6, 0.5, 132)])
+def test_real_pencil_mode_parity(rule, n_e, aspect, n):
+    """NEXT-2b: real A, B and a contour symmetric about the real axis — each conjugate pole pair
+    is factored once with [R | conj R]; Q and Q_L must still equal the oracle's per-node sums.
+    The endpoint rule has real poles (single units)."""
+    P = synth.make_pencil("R2", n=n, m0=21)
+    s = P.spec
+    z, w = oracle.nodes(s.c, s.r, aspect, n_e, rule)
+    f = Feast(P.n, P.m0, s.c, s.r, aspect, n_e, rule, fb.BI, False, real_pencil=True)
+    zz, _, j0, j1 = f.nodes()
+    n_real = sum(1 for x in zz if abs(x.imag) < 1e-12)
+    assert j1 - j0 == (len(zz) - n_real) // 2 + n_real          # one unit per orbit
+    A, B, X = dev(P.A), dev(P.B), dev(P.X0)
+    Vin = synth.random_block(P.n, P.m0, 7)
+    Q = host(f.project(A, B, X))
+    assert rel(Q, oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
+    Qb, QLb = f.project_bi(A, B, X, dev(Vin))
+    assert rel(host(Qb), oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
+    assert rel(host(QLb), oracle.project(P.A, P.B, Vin, z, w, left=True)) <= TOL
+    stats, worst = f.node_stats()
+    assert all(v > 0 for v in stats) and 0 <= worst < len(zz)   # every node (both poles) reported
+
+
+def test_real_pencil_mode_full_size_and_guards():
+    """R2 at full size (n = 2048): parity, half the factorisation units; a complex A is refused
+    at run time (device check) and a contour off the real axis at set-up."""
+    P = synth.make_pencil("R2")
+    s = P.spec
+    z, w = _oracle_nodes(P)
+    f = _handle(P, real_pencil=True)
+    _, _, j0, j1 = f.nodes()
+    assert j1 - j0 == P.q // 2
+    Q = host(f.project(dev(P.A), dev(P.B), dev(P.X0)))
+    assert rel(Q, oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
+    x = (P.lam - s.c) / s.r
+    Qs = P.V @ ((1 / (1 + x ** P.q))[:, None] * np.linalg.solve(P.V, P.X0))
+    assert rel(Q, Qs) <= TOL
+    Ac = dev(P.A + 1e-3j * np.eye(P.n))
+    with pytest.raises(FeastError, match="imaginary"):
+        f.project(Ac, dev(P.B), dev(P.X0))
+    with pytest.raises(FeastError):
+        Feast(P.n, P.m0, 0.2 + 0.1j, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, False, real_pencil=True)

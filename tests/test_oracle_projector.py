@@ -45,7 +45,8 @@ def test_spec_worked_example():
                           np.zeros((2, 2)))
 
 
-@pytest.mark.parametrize("key,n,m0", [("C1", 200, 64), ("C2", 96, 24), ("C4", 128, 32), ("C5", 96, 32)])
+@pytest.mark.parametrize("key,n,m0", [("C1", 200, 64), ("C2", 96, 24), ("C4", 128, 32), ("C5", 96, 32),
+                                      ("R2", 96, 24)])
 def test_spectral_identity_right(key, n, m0):
     P = synth.make_pencil(key, n=n, m0=m0)
     z, w = oracle.nodes(P.spec.c, P.spec.r, P.spec.aspect, P.spec.n_e, P.spec.rule)
@@ -113,3 +114,19 @@ def test_singular_node_detected():
     z = np.array([0.5 + 0j, -1.0]); w = np.array([1.0 + 0j, 1.0])
     with pytest.raises(ZeroDivisionError):
         oracle.project(A, None, np.eye(2), z, w)
+
+
+def test_real_pencil_conjugate_pole_symmetry():
+    """Real pencil (R2 recipe) and a contour symmetric about the real axis: the partner pole's
+    solve is the conjugate of the primary pole's solve with conj(R) (C(conj z) = conj(C(z))),
+    the identity the real-pencil mode (NEXT-2b) relies on; checked with scipy solves."""
+    P = synth.make_pencil("R2", n=40, m0=6)
+    assert np.abs(P.A.imag).max() == 0.0 and np.abs(P.B.imag).max() == 0.0
+    z, w = oracle.nodes(P.spec.c, P.spec.r, P.spec.aspect, P.spec.n_e, P.spec.rule)
+    R = P.B @ P.X0
+    for j, zj in enumerate(z):
+        k = int(np.argmin(np.abs(z - np.conj(zj))))
+        assert abs(z[k] - np.conj(zj)) < 1e-14 and abs(w[k] - np.conj(w[j])) < 1e-14
+        Yk = sla.solve(z[k] * P.B - P.A, R)
+        Yj_conj = np.conj(sla.solve(zj * P.B - P.A, np.conj(R)))
+        assert _rel(Yj_conj, Yk) < 1e-12
