@@ -106,6 +106,17 @@ int feast_init(feast_handle* h, int64_t n, int64_t m0, double c_re, double c_im,
  * enable = 0 restores per-node factorisation. */
 int feast_set_real_pencil(feast_handle h, int32_t enable);
 
+/* Complex-symmetric pencil mode (SURVEY NEXT-2a; the paper's complex-symmetric FEM / PML
+ * pencils with Bi-FEAST): the caller asserts A^T = A and B^T = B.  Then
+ * C_j^T = C_j and the left solve is a right solve of the conjugated block,
+ *     C_j^-H (B^H V) = conj( C_j^-1 conj(B^H V) ),
+ * so in FEAST_BI handles the left block rides along the right solves as m0 extra columns of the
+ * augmented system (fused forward substitution, one back substitution for both blocks) instead
+ * of a separate conjugate-transposed substitution.  Q_L = conj(sum_j w_j C_j^-1 conj(B^H V)).
+ * Same ordering rule as feast_set_real_pencil (before the workspace); exclusive with it.
+ * The symmetry is the caller's premise (not checked). */
+int feast_set_complex_symmetric(feast_handle h, int32_t enable);
+
 /* Device workspace size in bytes for this handle (caller allocates, e.g. with torch). */
 int feast_workspace_bytes(feast_handle h, size_t* bytes);
 

@@ -36,6 +36,7 @@ struct feast_ctx {
   // batches index units.  Per unit: pole zu (primary node), weight wu, partner weight wpu (0 if
   // the pole is real), primary node unode, partner node upart (-1).
   bool real = false;
+  bool csym = false;                  // A^T = A, B^T = B: left block through the right solves (NEXT-2a)
   int nu = 0;
   int64_t mr = 0;                     // right-hand-side columns per unit: m0, or 2 m0 ([R | conj R])
   std::vector<double2> zu, wu, wpu;
@@ -422,20 +423,21 @@ void lu_batched(feast_ctx* h, const Lu& v, int64_t aug) {
 }
 
 // Y_k <- op(T_kk^-1) Y_k in place (M = w <= 64): which 0 = L^-1, 1 = U^-1; conj: (.)^H
-void diag_apply(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t k, int w, int which, bool conj) {
+void diag_apply(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t k, int w, int which, bool conj,
+                int64_t ncols) {
   const int64_t ld = h->ldc;
-  ZgemmArgs p{w, h->mr, w, inv_ptr(v, k / 64, which), 64, h->inv_stride, Y + k, ld, sy, Y + k, ld, sy,
+  ZgemmArgs p{w, ncols, w, inv_ptr(v, k / 64, which), 64, h->inv_stride, Y + k, ld, sy, Y + k, ld, sy,
               make_double2(1, 0), make_double2(0, 0), v.nbat, 1};
   feast::zgemm_launch(p, conj, feast::ZG_GEN, v.sm);
 }
 
 // Y <- L^-1 Y (Y already row-permuted): used when the factors are cached (no augmented LU)
-void solve_right_fwd(feast_ctx* h, const Lu& v, double2* Y, int64_t sy) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), m = h->mr;
+void solve_right_fwd(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t m) {
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr);
   double2* C = v.Cw;
   for (int64_t k = 0; k < n; k += h->nb) {
     const int w = (int)std::min<int64_t>(h->nb, n - k);
-    diag_apply(h, v, Y, sy, k, w, 0, false);
+    diag_apply(h, v, Y, sy, k, w, 0, false, m);
     const int64_t rest = n - k - w;
     if (rest > 0) {
       ZgemmArgs p{rest, m, w, C + (k + w) + k * ld, ld, st, Y + k, ld, sy, Y + k + w, ld, sy,
@@ -446,13 +448,13 @@ void solve_right_fwd(feast_ctx* h, const Lu& v, double2* Y, int64_t sy) {
 }
 
 // Y <- U^-1 Y  (Y = L^-1 P R already: the forward substitution ran inside the augmented LU)
-void solve_right_back(feast_ctx* h, const Lu& v, double2* Y, int64_t sy) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), m = h->mr;
+void solve_right_back(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t m) {
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr);
   double2* C = v.Cw;
   const int64_t last = ((n - 1) / h->nb) * h->nb;
   for (int64_t k = last; k >= 0; k -= h->nb) {
     const int w = (int)std::min<int64_t>(h->nb, n - k);
-    diag_apply(h, v, Y, sy, k, w, 1, false);
+    diag_apply(h, v, Y, sy, k, w, 1, false, m);
     if (k > 0) {
       ZgemmArgs p{k, m, w, C + k * ld, ld, st, Y + k, ld, sy, Y, ld, sy, make_double2(-1, 0), make_double2(1, 0),
                   v.nbat};
@@ -467,7 +469,7 @@ void solve_left(feast_ctx* h, const Lu& v, double2* Y) {
   double2* C = v.Cw;
   for (int64_t k = 0; k < n; k += h->nb) {  // U^H: lower, non-unit
     const int w = (int)std::min<int64_t>(h->nb, n - k);
-    diag_apply(h, v, Y, sy, k, w, 1, true);      // (U_kk^H)^-1 = (U_kk^-1)^H
+    diag_apply(h, v, Y, sy, k, w, 1, true, m);   // (U_kk^H)^-1 = (U_kk^-1)^H
     const int64_t rest = n - k - w;
     if (rest > 0) {
       // Y[k+w:] -= (U[k:k+w, k+w:])^H Y[k:k+w]
@@ -479,7 +481,7 @@ void solve_left(feast_ctx* h, const Lu& v, double2* Y) {
   const int64_t last = ((n - 1) / h->nb) * h->nb;
   for (int64_t k = last; k >= 0; k -= h->nb) {  // L^H: upper, unit
     const int w = (int)std::min<int64_t>(h->nb, n - k);
-    diag_apply(h, v, Y, sy, k, w, 0, true);      // (L_kk^H)^-1 = (L_kk^-1)^H
+    diag_apply(h, v, Y, sy, k, w, 0, true, m);   // (L_kk^H)^-1 = (L_kk^-1)^H
     if (k > 0) {
       // Y[0:k] -= (L[k:k+w, 0:k])^H Y[k:k+w]
       ZgemmArgs p{k, m, w, C + k, ld, st, Y + k, ld, sy, Y, ld, sy, make_double2(-1, 0), make_double2(1, 0), v.nbat};
@@ -517,6 +519,11 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
   const int64_t mr = h->mr, st = ld * (n + mr);
   const bool pair = h->real;          // units are conjugate-pole orbits: RHS [R | conj R]
   const double2* wp = pair ? h->wpd : nullptr;
+  // complex-symmetric pencil (C_j^T = C_j): Z_j = C_j^-H RL = conj(C_j^-1 conj(RL)), so the left
+  // block rides along the right solves as extra columns conj(RL) of the augmented system
+  const bool csl = h->csym && doL && !reuse;
+  const int64_t ncr = pair ? mr : (csl && doR ? 2 * m : m);   // right-hand-side columns solved
+  const bool solve = doR || csl;
   if (pair && owned > 0) {            // the real-pencil premise, checked on the device
     cudaMemsetAsync(h->realviol, 0, 4, h->stream);
     feast::imag_check_launch(A, lda, n, h->realviol, h->stream);
@@ -538,21 +545,26 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
         feast::stats_init_launch(v.stats, v.info, v.nbat, v.sm);
         // a2: C_j = z_j B - A ; R appended as extra columns (augmented system [C_j | R])
         feast::shift_launch(bat(v.Cw, ld, st), A, lda, B, ldb, h->zd + j + b0, n, v.nbat, v.sm);
-        if (doR) feast::broadcast_copy_launch(bat(v.Cw + n * ld, ld, st), Rr, ldr, n, m, v.nbat, pair, v.sm);
+        if (doR)
+          feast::broadcast_copy_launch(bat(v.Cw + n * ld, ld, st), Rr, ldr, n, m, v.nbat,
+                                       pair ? feast::BC_PAIR : feast::BC_COPY, v.sm);
+        if (csl)
+          feast::broadcast_copy_launch(bat(v.Cw + (n + (doR ? m : 0)) * ld, ld, st), Rl, ldrl, n, m, v.nbat,
+                                       feast::BC_CONJ, v.sm);
         // a3 (+ forward substitution of a4): P_j [C_j | R] -> [U_j | L_j^-1 P_j R]
-        lu_batched(h, v, doR ? mr : 0);
+        lu_batched(h, v, solve ? ncr : 0);
         if (doL || h->cache_on)
           feast::perm_launch(v.ipiv, h->perm + (int64_t)b0 * n, h->iperm + (int64_t)b0 * n, n, v.nbat, v.sm);
         // a4: Y_j = U_j^-1 (L_j^-1 P_j R)
-        if (doR) solve_right_back(h, v, v.Cw + n * ld, st);
+        if (solve) solve_right_back(h, v, v.Cw + n * ld, st, ncr);
       } else if (doR) {
         // cached factors (NEXT-1, "factored just once"): Y_j = U^-1 L^-1 P_j R
         double2* Yg = h->Y + b0 * ld * mr;   // (factor cache and real-pencil mode are exclusive: mr = m)
         feast::gather_rows_launch(bat(Yg, ld, ld * mr), Rr, ldr, 0, h->perm + (int64_t)b0 * n, n, m, v.nbat, v.sm);
-        solve_right_fwd(h, v, Yg, ld * mr);
-        solve_right_back(h, v, Yg, ld * mr);
+        solve_right_fwd(h, v, Yg, ld * mr, m);
+        solve_right_back(h, v, Yg, ld * mr, m);
       }
-      if (doL) {
+      if (doL && !csl) {
         // Z_j = P^T L^-H U^-H RL  (P^T folded into the accumulate below)
         double2* Yg = h->YL + b0 * ld * mr;
         feast::broadcast_copy_launch(bat(Yg, ld, ld * mr), Rl, ldrl, n, m, v.nbat, pair, v.sm);
@@ -573,7 +585,10 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
         feast::accum_launch(Q, ldq, bat(h->Y, ld, ld * mr), h->wd + j, wpj, nullptr, n, m, nbat, false, jb > 0,
                             h->stream);
     }
-    if (doL)
+    if (csl)   // QL (+)= sum_j conj(w_j) conj(C_j^-1 conj RL) = conj(sum_j w_j C_j^-1 conj RL)
+      feast::accum_launch(QL, ldql, bat(h->Cw + (n + (doR ? m : 0)) * ld, ld, st), h->wd + j, nullptr, nullptr, n, m,
+                          nbat, false, jb > 0, h->stream, true);
+    else if (doL)
       feast::accum_launch(QL, ldql, bat(h->YL, ld, ld * mr), h->wd + j, wpj, h->iperm, n, m, nbat, true, jb > 0,
                           h->stream);
   }
@@ -748,7 +763,7 @@ int setup_units(feast_ctx* h) {
   h->j1 = (h->rank + 1) * (h->nu / h->world);
   const int owned = h->j1 - h->j0;
   h->batch = std::max(1, h->max_batch == 0 ? owned : std::min<int>(h->max_batch, owned));
-  h->mr = h->real ? 2 * h->m0 : h->m0;
+  h->mr = (h->real || (h->csym && h->mode == FEAST_BI)) ? 2 * h->m0 : h->m0;
   return 0;
 }
 
@@ -1091,11 +1106,21 @@ int feast_factor_cache(feast_handle h, int32_t enable) {
   return FEAST_OK;
 }
 
+int feast_set_complex_symmetric(feast_handle h, int32_t enable) {
+  if (!h) return FEAST_E_ARG;
+  if (h->ws) return fail(h, FEAST_E_STATE, "feast_set_complex_symmetric must precede feast_workspace_bytes/bind%s");
+  if (enable && h->real) return fail(h, FEAST_E_STATE, "complex-symmetric and real-pencil modes are exclusive%s");
+  h->csym = enable != 0;
+  setup_units(h);
+  return FEAST_OK;
+}
+
 int feast_set_real_pencil(feast_handle h, int32_t enable) {
   if (!h) return FEAST_E_ARG;
   if (h->ws) return fail(h, FEAST_E_STATE, "feast_set_real_pencil must precede feast_workspace_bytes/bind%s");
   if (enable && h->cache_on) return fail(h, FEAST_E_STATE, "factor cache is not combined with real-pencil mode%s");
   if (enable && h->c_im != 0.0) return fail(h, FEAST_E_ARG, "real-pencil mode needs a contour centre on the real axis%s");
+  if (enable && h->csym) return fail(h, FEAST_E_STATE, "complex-symmetric and real-pencil modes are exclusive%s");
   h->real = enable != 0;
   if (setup_units(h) != 0) {
     h->real = false;

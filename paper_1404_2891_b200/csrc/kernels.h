@@ -69,16 +69,18 @@ void gather_rows_launch(Batched Y, const double2* R, int64_t ldr, int64_t sR, co
 // scatter: Out_b[perm_b[i]][c] = Y_b[i][c]
 void scatter_rows_launch(Batched Out, const double2* Y, int64_t ldy, int64_t sY, const int32_t* perm,
                          int64_t n, int64_t m, int batch, cudaStream_t s);
-// copy R (shared) into every Y_b (pair_conj: and conj(R) into Y_b's columns [m, 2m))
-void broadcast_copy_launch(Batched Y, const double2* R, int64_t ldr, int64_t n, int64_t m, int batch, bool pair_conj,
+// copy R (shared) into every Y_b; BC_PAIR: and conj(R) into Y_b's columns [m, 2m); BC_CONJ: conj(R)
+enum { BC_COPY = 0, BC_PAIR = 1, BC_CONJ = 2 };
+void broadcast_copy_launch(Batched Y, const double2* R, int64_t ldr, int64_t n, int64_t m, int batch, int mode,
                            cudaStream_t s);
 // flag |= 1 if M (n x n) has any nonzero imaginary part
 void imag_check_launch(const double2* M, int64_t ld, int64_t n, int32_t* flag, cudaStream_t s);
 
 // Q (+)= sum_b w_b Y_b[iperm_b[i]] (+ wp_b conj(Y_b[iperm_b[i], m + c]) when wp != null) with
-// conj(w), conj(wp) if conjw; iperm null = identity; b increasing; accumulate=false overwrites Q.
+// conj(w), conj(wp) if conjw; iperm null = identity; b increasing; accumulate=false overwrites Q;
+// conj_out: Q = conj(conj(Q_old) + sum) (the left block of a complex-symmetric pencil).
 void accum_launch(double2* Q, int64_t ldq, Batched Y, const double2* w, const double2* wp, const int32_t* iperm,
-                  int64_t n, int64_t m, int batch, bool conjw, bool accumulate, cudaStream_t s);
+                  int64_t n, int64_t m, int batch, bool conjw, bool accumulate, cudaStream_t s, bool conj_out = false);
 // C = alpha * sum_s P_s + beta C, P_s = M x N (ld M) partials at P + s*M*N
 void splitk_reduce_launch(double2* C, int64_t ldc, const double2* P, int64_t M, int64_t N, int splits,
                           double2 alpha, double2 beta, cudaStream_t s);

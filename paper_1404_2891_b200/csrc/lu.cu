@@ -464,13 +464,15 @@ void scatter_rows_launch(Batched Out, const double2* Y, int64_t ldy, int64_t sY,
   count_launch();
 }
 
-// Y_b[:, c] = R[:, c] (c < m) and, with pair_conj, Y_b[:, m + c] = conj(R[:, c]): the
-// right-hand sides [R | conj(R)] of a conjugate-pole pair of a real pencil (one LU, both poles).
-__global__ void broadcast_copy_kernel(Batched Y, const double2* __restrict__ R, int64_t ldr, int64_t n, int64_t m) {
+// Y_b[:, c] = R[:, c] (c < m) and, with mode BC_PAIR, Y_b[:, m + c] = conj(R[:, c]): the
+// right-hand sides [R | conj(R)] of a conjugate-pole pair of a real pencil (one LU, both poles);
+// mode BC_CONJ copies conj(R) (the left block of a complex-symmetric pencil).
+__global__ void broadcast_copy_kernel(Batched Y, const double2* __restrict__ R, int64_t ldr, int64_t n, int64_t m,
+                                      int mode) {
   const int b = blockIdx.z;
   const int64_t cc = blockIdx.y;
-  const bool cj = cc >= m;
-  const int64_t c = cj ? cc - m : cc;
+  const bool cj = cc >= m || mode == BC_CONJ;
+  const int64_t c = cc >= m ? cc - m : cc;
   const double2* Rc = R + c * ldr;
   double2* Yc = Y.p + (int64_t)b * Y.stride + cc * Y.ld;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -479,13 +481,13 @@ __global__ void broadcast_copy_kernel(Batched Y, const double2* __restrict__ R, 
   }
 }
 
-void broadcast_copy_launch(Batched Y, const double2* R, int64_t ldr, int64_t n, int64_t m, int batch, bool pair_conj,
+void broadcast_copy_launch(Batched Y, const double2* R, int64_t ldr, int64_t n, int64_t m, int batch, int mode,
                            cudaStream_t s) {
-  const int64_t cols = pair_conj ? 2 * m : m;
+  const int64_t cols = mode == BC_PAIR ? 2 * m : m;
   ProfScope ps_(K_PERM, 0.0, (double)batch * n * cols * 32.0, s);
   unsigned gx = (unsigned)((n + 255) / 256);
   if (gx > 16) gx = 16;
-  broadcast_copy_kernel<<<dim3(gx, (unsigned)cols, (unsigned)batch), 256, 0, s>>>(Y, R, ldr, n, m);
+  broadcast_copy_kernel<<<dim3(gx, (unsigned)cols, (unsigned)batch), 256, 0, s>>>(Y, R, ldr, n, m, mode);
   count_launch();
 }
 
@@ -515,10 +517,11 @@ __device__ __forceinline__ double2 cfma(double2 w, double2 y, double2 acc) {
 }
 __global__ void accum_kernel(double2* __restrict__ Q, int64_t ldq, Batched Y, const double2* __restrict__ w,
                              const double2* __restrict__ wp, const int32_t* __restrict__ iperm, int64_t n, int64_t m,
-                             int batch, bool conjw, bool accumulate) {
+                             int batch, bool conjw, bool accumulate, bool conj_out) {
   const int64_t c = blockIdx.y;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double2 acc = accumulate ? Q[i + c * ldq] : make_double2(0.0, 0.0);
+    if (conj_out) acc = cconj(acc);
     for (int b = 0; b < batch; ++b) {
       double2 wb = w[b];
       if (conjw) wb = cconj(wb);
@@ -531,18 +534,19 @@ __global__ void accum_kernel(double2* __restrict__ Q, int64_t ldq, Batched Y, co
         acc = cfma(wq, cconj(Yb[(m + c) * Y.ld]), acc);
       }
     }
-    Q[i + c * ldq] = acc;
+    Q[i + c * ldq] = conj_out ? cconj(acc) : acc;
   }
 }
 
 void accum_launch(double2* Q, int64_t ldq, Batched Y, const double2* w, const double2* wp, const int32_t* iperm,
-                  int64_t n, int64_t m, int batch, bool conjw, bool accumulate, cudaStream_t s) {
+                  int64_t n, int64_t m, int batch, bool conjw, bool accumulate, cudaStream_t s, bool conj_out) {
   const int parts = wp ? 2 : 1;
   ProfScope ps_(K_ACCUM, (double)batch * parts * n * m * 8.0,
                 (double)(batch * parts + (accumulate ? 2 : 1)) * n * m * 16.0, s);
   unsigned gx = (unsigned)((n + 255) / 256);
   if (gx > 16) gx = 16;
-  accum_kernel<<<dim3(gx, (unsigned)m), 256, 0, s>>>(Q, ldq, Y, w, wp, iperm, n, m, batch, conjw, accumulate);
+  accum_kernel<<<dim3(gx, (unsigned)m), 256, 0, s>>>(Q, ldq, Y, w, wp, iperm, n, m, batch, conjw, accumulate,
+                                                     conj_out);
   count_launch();
 }
 

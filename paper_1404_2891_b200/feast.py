@@ -32,7 +32,8 @@ ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, c
 # every symbol include/feast.h declares (checked by tests/test_abi.py)
 EXPORTS = ["feast_init", "feast_workspace_bytes", "feast_bind_workspace", "feast_nodes", "feast_project",
            "feast_project_left", "feast_project_bi", "feast_reduce", "feast_set_allreduce", "feast_iterate",
-           "feast_node_stats", "feast_factor_cache", "feast_set_real_pencil", "feast_last_launch_count", "feast_profile", "feast_profile_summary",
+           "feast_node_stats", "feast_factor_cache", "feast_set_real_pencil",
+           "feast_set_complex_symmetric", "feast_last_launch_count", "feast_profile", "feast_profile_summary",
            "feast_profile_records", "feast_last_error",
            "feast_version", "feast_destroy"]
 K_CLASSES = ["shift", "panel", "laswp", "trsm", "zgemm", "perm", "accum", "other"]
@@ -71,6 +72,7 @@ def load_library(path: str = LIB_PATH):
     lib.feast_last_launch_count.restype = I64
     lib.feast_factor_cache.argtypes = [P, I32]
     lib.feast_set_real_pencil.argtypes = [P, I32]
+    lib.feast_set_complex_symmetric.argtypes = [P, I32]
     lib.feast_profile.argtypes = [P, I32]
     lib.feast_profile_summary.argtypes = [P, I32, P, P, P, P]
     lib.feast_profile_records.argtypes = [P, I64, P, P, P, P, P, P]
@@ -124,7 +126,8 @@ class Feast:
     """One handle of the C ABI: contour, quadrature, node ownership and workspace."""
 
     def __init__(self, n, m0, center=0j, r=1.0, aspect=1.0, n_e=8, rule=RULE_TRAPEZOID, mode=RIGHT,
-                 b_is_identity=True, rank=0, world=1, max_batch=0, device=None, group=None, real_pencil=False):
+                 b_is_identity=True, rank=0, world=1, max_batch=0, device=None, group=None, real_pencil=False,
+                 complex_symmetric=False):
         self.lib = load_library()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.stream = torch.cuda.current_stream(self.device)
@@ -141,6 +144,8 @@ class Feast:
         self.real_pencil = bool(real_pencil)
         if self.real_pencil:   # conjugate-pole pairs share one LU (NEXT-2b); before the workspace
             self._check(self.lib.feast_set_real_pencil(self.h, 1))
+        if complex_symmetric:  # A^T = A, B^T = B: left block through the right solves (NEXT-2a)
+            self._check(self.lib.feast_set_complex_symmetric(self.h, 1))
         nbytes = ctypes.c_size_t()
         self._check(self.lib.feast_workspace_bytes(self.h, ctypes.byref(nbytes)))
         self.workspace = torch.empty(int(nbytes.value) + 256, dtype=torch.uint8, device=self.device)

@@ -23,7 +23,7 @@ def _declared():
 def test_exports_every_declared_symbol():
     lib = fb.load_library()
     decl = _declared()
-    assert set(decl) == set(fb.EXPORTS)
+    assert set(decl) == set(fb.EXPORTS), set(decl) ^ set(fb.EXPORTS)
     for name in decl:
         assert hasattr(lib, name), name
     assert b"sm_100a" in lib.feast_version()

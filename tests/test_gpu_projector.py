@@ -248,3 +248,23 @@ def test_real_pencil_mode_full_size_and_guards():
         f.project(Ac, dev(P.B), dev(P.X0))
     with pytest.raises(FeastError):
         Feast(P.n, P.m0, 0.2 + 0.1j, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, False, real_pencil=True)
+
+
+@pytest.mark.parametrize("n,m0", [(160, 12), (300, 25)])
+def test_complex_symmetric_bi_parity(n, m0):
+    """NEXT-2a: C3-recipe (complex-symmetric) pencil in a Bi handle with the complex-symmetric
+    mode: the left block is computed by right solves of conj(B^H V); Q and Q_L match the oracle
+    (which runs the conjugate-transposed substitution), for project_bi and project_left."""
+    P = synth.make_pencil("C3", n=n, m0=m0)
+    assert np.abs(P.A - P.A.T).max() == 0 and np.abs(P.B - P.B.T).max() == 0
+    z, w = _oracle_nodes(P)
+    Vin = synth.random_block(P.n, P.m0, 3)
+    f = _handle(P, mode=fb.BI, complex_symmetric=True)
+    A, B = dev(P.A), dev(P.B)
+    Q, QL = f.project_bi(A, B, dev(P.X0), dev(Vin))
+    assert rel(host(Q), oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
+    assert rel(host(QL), oracle.project(P.A, P.B, Vin, z, w, left=True)) <= TOL
+    QL2 = f.project_left(A, B, dev(Vin))
+    assert rel(host(QL2), oracle.project(P.A, P.B, Vin, z, w, left=True)) <= TOL
+    Q2 = f.project(A, B, dev(P.X0))
+    assert rel(host(Q2), oracle.project(P.A, P.B, P.X0, z, w)) <= TOL

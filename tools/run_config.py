@@ -20,14 +20,18 @@ ap.add_argument("key")
 ap.add_argument("--batch", type=int, default=0)
 ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--m0", type=int, default=None)
+ap.add_argument("--bi", action="store_true", help="force a Bi-FEAST handle (left + right blocks)")
+ap.add_argument("--csym", action="store_true", help="complex-symmetric mode (NEXT-2a)")
+ap.add_argument("--real", action="store_true", help="real-pencil mode (NEXT-2b)")
 args = ap.parse_args()
 t0 = time.time()
 P = synth.make_pencil_torch(args.key, n=args.n, m0=args.m0)
 torch.cuda.synchronize()
 tgen = time.time() - t0
 s = P.spec
-bi = s.mode == "bi"
-f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.BI if bi else fb.RIGHT, P.B is None, max_batch=args.batch)
+bi = s.mode == "bi" or args.bi
+f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.BI if bi else fb.RIGHT, P.B is None, max_batch=args.batch,
+          complex_symmetric=args.csym, real_pencil=args.real)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 if bi:
     G = P.X0.conj().T @ P.X0
