@@ -155,6 +155,17 @@ int feast_reduce(feast_handle h, const void* A, int64_t lda, const void* B, int6
                  const void* Q, int64_t ldq, const void* QL, int64_t ldql,
                  void* Ahat, int64_t ldah, void* Bhat, int64_t ldbh);
 
+/* Eigenvalue-count estimate (the count m of eigenvalues inside the
+ * contour decides whether m0 >= m): Q = rho(B^-1 A) U for a caller-supplied random block U
+ * (n x m0, entries with E[u u^H] = I, e.g. CN(0,1)), then the Hutchinson trace estimate
+ *     *estimate = Re tr(U^H Q) / m0  ~  Re tr rho(B^-1 A) = Re sum_i rho(lambda_i)  ~  m,
+ * since rho ~ 1 inside and ~ 0 outside the contour (the expectation is exact; the standard
+ * deviation falls like 1/sqrt(m0)).  With world > 1, Q is all-reduced over the ranks (through
+ * the registered callback) before the trace, so every rank returns the same estimate.
+ * U, Q: device, column-major, ld >= n; estimate: host. */
+int feast_estimate_count(feast_handle h, const void* A, int64_t lda, const void* B, int64_t ldb,
+                         const void* U, int64_t ldu, void* Q, int64_t ldq, double* estimate);
+
 /* All-reduce callback for world > 1: sum `count` float64 values at device pointer `buf`
  * across ranks, in place, ordered on `cuda_stream` (the library's stream: the callback must
  * enqueue its collective there, or complete it before returning); return 0 on success. */

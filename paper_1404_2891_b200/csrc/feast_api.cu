@@ -975,6 +975,33 @@ int feast_reduce(feast_handle h, const void* A, int64_t lda, const void* B, int6
   return FEAST_OK;
 }
 
+int feast_estimate_count(feast_handle h, const void* A, int64_t lda, const void* B, int64_t ldb, const void* U,
+                         int64_t ldu, void* Q, int64_t ldq, double* estimate) {
+  int e = check_args_common(h, A, lda, B, ldb);
+  if (e) return e;
+  if (!U || !Q || !estimate || ldu < h->n || ldq < h->n) return fail(h, FEAST_E_ARG, "U/Q/estimate null or ld < n%s");
+  if (h->world > 1 && !h->ar) return fail(h, FEAST_E_COMM, "world > 1 needs feast_set_allreduce%s");
+  Join j_(h);
+  const int64_t n = h->n, m = h->m0;
+  // Q = rho(B^-1 A) U (this rank's nodes, then the node sum over ranks)
+  const int pst = project_impl(h, (const double2*)A, lda, (const double2*)B, ldb, (const double2*)U, ldu, nullptr, 0,
+                               (double2*)Q, ldq, nullptr, 0);
+  if (pst < 0) return pst;
+  if (h->world > 1)
+    for (int64_t c = 0; c < m; ++c)
+      if (h->ar((double2*)Q + c * ldq, 2 * n, h->stream, h->ar_user)) return fail(h, FEAST_E_COMM, "all-reduce failed%s");
+  // Hutchinson trace estimate: m ~ tr rho(B^-1 A) ~ Re tr(U^H Q) / m0 (deterministic block sums)
+  constexpr int NP = 64;
+  feast::cdot_launch((const double2*)U, ldu, (const double2*)Q, ldq, n, m, h->SK, NP, h->stream);
+  std::vector<double2> part(NP);
+  CUDA_TRY(h, cudaMemcpyAsync(part.data(), h->SK, NP * 16, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  double re = 0.0;
+  for (const double2& p : part) re += p.x;
+  *estimate = re / (double)m;
+  return pst;
+}
+
 int feast_set_allreduce(feast_handle h, feast_allreduce_fn fn, void* user) {
   if (!h) return FEAST_E_ARG;
   h->ar = fn;

@@ -629,6 +629,30 @@ void frob2_launch(const double2* A, int64_t lda, int64_t n, double* partial, int
   count_launch();
 }
 
+// partial[b] = sum over the columns c = b, b + nparts, ... of sum_i conj(U[i][c]) Q[i][c]
+// (re, im) — the trace tr(U^H Q) of the count estimator, summed on the host in block order.
+__global__ void cdot_kernel(const double2* U, int64_t ldu, const double2* Q, int64_t ldq, int64_t n, int64_t m,
+                            double2* partial) {
+  double re = 0.0, im = 0.0;
+  for (int64_t c = blockIdx.x; c < m; c += gridDim.x)
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const double2 u = U[i + c * ldu], q = Q[i + c * ldq];
+      re = fma(u.x, q.x, fma(u.y, q.y, re));
+      im = fma(u.x, q.y, fma(-u.y, q.x, im));
+    }
+  re = block_sum(re);
+  __syncthreads();
+  im = block_sum(im);
+  if (threadIdx.x == 0) partial[blockIdx.x] = make_double2(re, im);
+}
+
+void cdot_launch(const double2* U, int64_t ldu, const double2* Q, int64_t ldq, int64_t n, int64_t m, double2* partial,
+                 int nparts, cudaStream_t s) {
+  ProfScope ps_(K_OTHER, 8.0 * n * m, 32.0 * n * m, s);
+  cdot_kernel<<<nparts, 256, 0, s>>>(U, ldu, Q, ldq, n, m, partial);
+  count_launch();
+}
+
 __global__ void colscale_kernel(double2* X, int64_t ldx, int64_t n, double2* W, int64_t ldw, int64_t m,
                                 const double* xn) {
   const int64_t c = blockIdx.y;

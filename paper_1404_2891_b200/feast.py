@@ -33,7 +33,7 @@ ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, c
 EXPORTS = ["feast_init", "feast_workspace_bytes", "feast_bind_workspace", "feast_nodes", "feast_project",
            "feast_project_left", "feast_project_bi", "feast_reduce", "feast_set_allreduce", "feast_iterate",
            "feast_node_stats", "feast_factor_cache", "feast_set_real_pencil",
-           "feast_set_complex_symmetric", "feast_last_launch_count", "feast_profile", "feast_profile_summary",
+           "feast_set_complex_symmetric", "feast_estimate_count", "feast_last_launch_count", "feast_profile", "feast_profile_summary",
            "feast_profile_records", "feast_last_error",
            "feast_version", "feast_destroy"]
 K_CLASSES = ["shift", "panel", "laswp", "trsm", "zgemm", "perm", "accum", "other"]
@@ -73,6 +73,7 @@ def load_library(path: str = LIB_PATH):
     lib.feast_factor_cache.argtypes = [P, I32]
     lib.feast_set_real_pencil.argtypes = [P, I32]
     lib.feast_set_complex_symmetric.argtypes = [P, I32]
+    lib.feast_estimate_count.argtypes = [P, P, I64, P, I64, P, I64, P, I64, P]
     lib.feast_profile.argtypes = [P, I32]
     lib.feast_profile_summary.argtypes = [P, I32, P, P, P, P]
     lib.feast_profile_records.argtypes = [P, I64, P, P, P, P, P, P]
@@ -267,6 +268,19 @@ class Feast:
                                                          flags))
         lam = [complex(ritz[2 * i], ritz[2 * i + 1]) for i in range(m)]
         return {"lam": lam, "resid": list(res), "flags": list(flags)}
+
+    def estimate_count(self, A, B, U, Q=None):
+        """Eigenvalue-count estimate Re tr(U^H rho(B^-1 A) U) / m0 for a random block U (NEXT-3);
+        returns (estimate, Q = rho(B^-1 A) U, node-summed over ranks)."""
+        Q = empty_colmajor(self.n, self.m0, self.device) if Q is None else Q
+        pa, lda = _ptr_ld(A, self.n, "A")
+        pb, ldb = _ptr_ld(B, self.n, "B")
+        pu, ldu = _ptr_ld(U, self.n, "U")
+        pq, ldq = _ptr_ld(Q, self.n, "Q")
+        est = ctypes.c_double()
+        self.status = self._check(self.lib.feast_estimate_count(self.h, pa, lda, pb, ldb, pu, ldu, pq, ldq,
+                                                                ctypes.byref(est)))
+        return est.value, Q
 
     def node_stats(self):
         zz, _, _, _ = self.nodes()

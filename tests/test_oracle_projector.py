@@ -130,3 +130,15 @@ def test_real_pencil_conjugate_pole_symmetry():
         Yk = sla.solve(z[k] * P.B - P.A, R)
         Yj_conj = np.conj(sla.solve(zj * P.B - P.A, np.conj(R)))
         assert _rel(Yj_conj, Yk) < 1e-12
+
+
+@pytest.mark.parametrize("key", ["C1", "C2", "R2"])
+def test_count_estimator_trace_identity(key):
+    """NEXT-3 count estimate: tr(U^H rho(B^-1 A) U) with U = I equals tr rho(B^-1 A) =
+    sum_i rho(lambda_i) (similarity invariance; rho from the closed form), and for random CN(0,1)
+    U its expectation — checked here on the oracle projector at a small size."""
+    P = synth.make_pencil(key, n=48, m0=48)
+    z, w = oracle.nodes(P.spec.c, P.spec.r, P.spec.aspect, P.spec.n_e, P.spec.rule)
+    Q = oracle.project(P.A, P.B, np.eye(P.n, dtype=complex), z, w)
+    exact = np.sum(_rho_closed(P.spec, P.lam))
+    assert abs(np.trace(Q) - exact) <= 1e-11 * max(1.0, abs(exact))
