@@ -38,6 +38,7 @@ def lib():
         _lib.orc_trapezoid_endpoint.argtypes = [I32, P, P]
         _lib.orc_midpoint.argtypes = [I32, P, P]
         _lib.orc_nodes.argtypes = [D, D, D, D, I32, I32, P, P]
+        _lib.orc_contour_nodes.argtypes = [I32, P, P, I32, I32, P, P]
         _lib.orc_rho.argtypes = [I32, P, P, I32, P, P]
         _lib.orc_rho.restype = None
         _lib.orc_lu.argtypes = [I64, P, I64, P, P]
@@ -85,6 +86,24 @@ def nodes(c, R, a, n_e, rule):
     if q < 0:
         raise ValueError("bad contour/rule arguments")
     return z[:2 * q].view(np.complex128).copy(), w[:2 * q].view(np.complex128).copy()
+
+
+def contour_nodes(segments, K, rule):
+    """Composite contour: segments = [("line", a, b) | ("arc", c, R, th0, th1)], the
+    rule (0 midpoint, 2 Gauss-Legendre) with K nodes per segment.  Returns (z, w)."""
+    kind = np.array([0 if s[0] == "line" else 1 for s in segments], dtype=np.int32)
+    par = np.zeros(5 * len(segments))
+    for i, s in enumerate(segments):
+        if s[0] == "line":
+            par[5 * i:5 * i + 4] = [complex(s[1]).real, complex(s[1]).imag, complex(s[2]).real, complex(s[2]).imag]
+        else:
+            par[5 * i:5 * i + 5] = [complex(s[1]).real, complex(s[1]).imag, s[2], s[3], s[4]]
+    q = len(segments) * K
+    z = np.zeros(2 * q); w = np.zeros(2 * q)
+    r = lib().orc_contour_nodes(len(segments), _p(kind), _p(par), int(K), int(rule), _p(z), _p(w))
+    if r < 0:
+        raise ValueError("bad contour/rule arguments")
+    return z.view(np.complex128).copy(), w.view(np.complex128).copy()
 
 
 def rho(z, w, mu):

@@ -151,6 +151,50 @@ int orc_nodes(double c_re, double c_im, double R, double a, int n_e, int rule, d
   return q;
 }
 
+/* Composite ("glued") contours (§5.4 "General Domain Shapes": the region is bounded
+ * by segments of curves or lines parameterized separately and glued together; only phi(t)
+ * changes).  Segment s is parameterized on t in [-1, 1]:
+ *   kind 0, line a -> b:        phi(t) = a + (b - a)(1 + t)/2,          phi'(t) = (b - a)/2
+ *   kind 1, arc c, R, th0->th1:  phi(t) = c + R e^{i th(t)}, th(t) = th0 + (th1 - th0)(1 + t)/2,
+ *                                 phi'(t) = i R e^{i th(t)} (th1 - th0)/2
+ * params: 5 doubles per segment (line: a_re, a_im, b_re, b_im, unused; arc: c_re, c_im, R, th0, th1).
+ * The rule (0 = midpoint trapezoid, reading R18; 2 = Gauss-Legendre) with K nodes is applied on
+ * every segment: pole phi(t_k), weight sigma = w_k phi'(t_k)/(2 pi i) (eq. pi / quadrature_for_pi
+ * with one parameter interval per segment).  Returns q = nseg*K or -1. */
+static void phi_segment(int kind, const double* p, double t, cx* ph, cx* dph) {
+  if (kind == 0) {
+    const double s = 0.5 * (1.0 + t);
+    *ph = cmk(p[0] + (p[2] - p[0]) * s, p[1] + (p[3] - p[1]) * s);
+    *dph = cmk(0.5 * (p[2] - p[0]), 0.5 * (p[3] - p[1]));
+  } else {
+    const double th = p[3] + (p[4] - p[3]) * 0.5 * (1.0 + t), half = 0.5 * (p[4] - p[3]);
+    *ph = cmk(p[0] + p[2] * cos(th), p[1] + p[2] * sin(th));
+    *dph = cmk(-p[2] * sin(th) * half, p[2] * cos(th) * half);
+  }
+}
+
+int orc_contour_nodes(int nseg, const int* kind, const double* params, int K, int rule, double* z, double* w) {
+  double tk[4096], wk[4096];
+  if (nseg < 1 || K < 1 || K > 4096) return -1;
+  if (rule == 0) orc_midpoint(K, tk, wk);
+  else if (rule == 2) orc_gauss_legendre(K, tk, wk);
+  else return -1;
+  const cx two_pi_i = cmk(0.0, 2.0 * M_PI);
+  int q = 0;
+  for (int s = 0; s < nseg; ++s) {
+    if (kind[s] != 0 && kind[s] != 1) return -1;
+    for (int k = 0; k < K; ++k) {
+      cx ph, dph;
+      phi_segment(kind[s], params + 5 * s, tk[k], &ph, &dph);
+      const cx sg = cdiv(cscale(dph, wk[k]), two_pi_i);
+      z[2 * q] = ph.re; z[2 * q + 1] = ph.im;
+      w[2 * q] = sg.re; w[2 * q + 1] = sg.im;
+      ++q;
+    }
+  }
+  return q;
+}
+
 /* rho(mu) = sum_k sigma_k / (phi_k - mu)  (eq. quadrature_for_pi). */
 void orc_rho(int q, const double* z, const double* w, int nmu, const double* mu, double* out) {
   for (int i = 0; i < nmu; ++i) {

@@ -143,3 +143,44 @@ def test_bad_arguments():
         oracle.nodes(0, -1, 1, 8, 0)
     with pytest.raises(ValueError):
         oracle.nodes(0, 1, 1, 7, 0)   # midpoint needs an even pole count (two halves)
+
+
+# ---------------------------------------------------------------- composite contours (NEXT-4)
+SQUARE = [("line", 1 - 1j, 1 + 1j), ("line", 1 + 1j, -1 + 1j), ("line", -1 + 1j, -1 - 1j), ("line", -1 - 1j, 1 - 1j)]
+TRIANGLE = [("line", -1, 1), ("line", 1, 1j), ("line", 1j, -1)]
+SEMICIRCLE = [("arc", 0, 1.0, 0.0, np.pi), ("line", -1, 1)]
+
+
+@pytest.mark.parametrize("segs", [SQUARE, TRIANGLE])
+def test_composite_polygon_moments_vanish(segs):
+    """Closed polygon, Gauss-Legendre K per side: sum_j w_j z_j^k = (1/2 pi i) oint z^k dz = 0
+    exactly for k <= 2K - 2 (phi linear on each side, so z^k phi' has degree k <= 2K - 1 in t)."""
+    K = 5
+    z, w = oracle.contour_nodes(segs, K, 2)
+    for k in range(2 * K - 1):
+        assert abs(np.sum(w * z ** k)) <= 1e-13 * max(1.0, np.max(np.abs(z)) ** k)
+
+
+def test_composite_full_circle_arc_equals_midpoint_rule():
+    """One arc of angle 2 pi with the midpoint rule reproduces the midpoint trapezoid on the circle
+    (reading R1): the same poles and weights from two different constructions."""
+    c, R, q = 0.3 - 0.2j, 0.7, 12
+    z1, w1 = oracle.contour_nodes([("arc", c, R, 0.0, 2 * np.pi)], q, 0)
+    z2, w2 = oracle.nodes(c, R, 1.0, q, 0)
+    o1, o2 = np.argsort(np.angle(z1 - c)), np.argsort(np.angle(z2 - c))
+    assert np.max(np.abs(z1[o1] - z2[o2])) < 1e-14 and np.max(np.abs(w1[o1] - w2[o2])) < 1e-15
+
+
+def test_composite_spec_examples():
+    """S:210-218 examples: square inside(0); triangle (-1, 1, i) with the trapezoid (midpoint, R18)
+    K = 8 per segment: |rho(centroid) - 1| <= 0.05; semicircle (arc + diameter): rho ~ 1 at 0.5i,
+    ~ 0 at -0.5i; and the Cauchy limit rho -> 1 inside / 0 outside as K grows."""
+    z, w = oracle.contour_nodes(SQUARE, 8, 2)
+    assert abs(oracle.rho(z, w, [0.0])[0] - 1) < 1e-5 and abs(oracle.rho(z, w, [3.0])[0]) < 1e-9
+    z, w = oracle.contour_nodes(TRIANGLE, 8, 0)
+    assert abs(oracle.rho(z, w, [1j / 3])[0] - 1) <= 0.05
+    z, w = oracle.contour_nodes(SEMICIRCLE, 16, 2)
+    r_in, r_out = oracle.rho(z, w, [0.5j, -0.5j])
+    assert abs(r_in - 1) < 1e-6 and abs(r_out) < 1e-6
+    errs = [abs(oracle.rho(*oracle.contour_nodes(TRIANGLE, K, 0), [1j / 3])[0] - 1) for K in (4, 8, 16, 32)]
+    assert all(b < a for a, b in zip(errs, errs[1:]))
