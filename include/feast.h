@@ -117,6 +117,24 @@ int feast_set_real_pencil(feast_handle h, int32_t enable);
  * The symmetry is the caller's premise (not checked). */
 int feast_set_complex_symmetric(feast_handle h, int32_t enable);
 
+/* Composite ("glued") contour (§5.4 "General Domain Shapes": only the
+ * parameterization phi(t) changes).  Replaces the ellipse of feast_init by nseg segments, each on
+ * t in [-1, 1], counter-clockwise, end of segment s = start of segment s+1 (closed):
+ *   kind[s] = 0  line a -> b:        params[5s..5s+3] = a_re, a_im, b_re, b_im   (5s+4 unused)
+ *   kind[s] = 1  arc  c + R e^{i th}: params[5s..5s+4] = c_re, c_im, R, th0, th1 (th1 > th0: ccw)
+ * rule: FEAST_RULE_TRAPEZOID (composite midpoint rule, reading R18) or FEAST_RULE_GAUSS_LEGENDRE,
+ * k_per_segment nodes on every segment: poles phi(t_k), weights w_k phi'(t_k)/(2 pi i), q = nseg*k.
+ * Before the workspace is bound (FEAST_E_STATE after); FEAST_E_ARG for an open or clockwise chain,
+ * bad kinds/radii, or q % world != 0.  feast_iterate's inside flags then use the crossing number
+ * of the contour polyline. */
+int feast_set_contour(feast_handle h, int32_t nseg, const int32_t* kind, const double* params, int32_t k_per_segment,
+                      int32_t rule);
+
+/* The rational filter of the handle's quadrature, rho(mu) = sum_j w_j / (z_j - mu) (eq.
+ * quadrature_for_pi), at npts host points mu (2*npts doubles, complex interleaved)
+ * into rho (host, 2*npts doubles): the eta(r) / filter-gap diagnostics. */
+int feast_filter(feast_handle h, int64_t npts, const double* mu, double* rho);
+
 /* Device workspace size in bytes for this handle (caller allocates, e.g. with torch). */
 int feast_workspace_bytes(feast_handle h, size_t* bytes);
 

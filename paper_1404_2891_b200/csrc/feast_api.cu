@@ -35,6 +35,11 @@ struct feast_ctx {
   // conjugate poles, which share one LU (C(conj z) = conj(C(z)) for real A, B).  j0/j1 and the
   // batches index units.  Per unit: pole zu (primary node), weight wu, partner weight wpu (0 if
   // the pole is real), primary node unode, partner node upart (-1).
+  // composite contour (NEXT-4): segments replace the ellipse when non-empty
+  struct Seg { int kind; double p[5]; };
+  std::vector<Seg> segs;
+  int seg_k = 0, seg_rule = 0;
+  std::vector<double2> poly;          // closed polyline of the contour (inside test)
   bool real = false;
   bool csym = false;                  // A^T = A, B^T = B: left block through the right solves (NEXT-2a)
   int nu = 0;
@@ -203,6 +208,67 @@ bool legendre_rule(int K, std::vector<double>& t, std::vector<double>& wt) {
     wt[K - i] = 2.0 / ((1.0 - x * x) * d * d);
   }
   return true;
+}
+
+// Composite contour: segment s on t in [-1, 1] (line a -> b, or arc c + R e^{i th}, th0 -> th1),
+// the rule (midpoint trapezoid, reading R18, or Gauss-Legendre) with seg_k nodes on every
+// segment: pole phi(t_k), weight w_k phi'(t_k) / (2 pi i) (eq. pi with one interval per segment).
+void seg_phi(const feast_ctx::Seg& g, double t, double2& ph, double2& dph) {
+  if (g.kind == 0) {
+    const double s = 0.5 * (1.0 + t);
+    ph = make_double2(g.p[0] + (g.p[2] - g.p[0]) * s, g.p[1] + (g.p[3] - g.p[1]) * s);
+    dph = make_double2(0.5 * (g.p[2] - g.p[0]), 0.5 * (g.p[3] - g.p[1]));
+  } else {
+    const double half = 0.5 * (g.p[4] - g.p[3]), th = g.p[3] + half * (1.0 + t);
+    ph = make_double2(g.p[0] + g.p[2] * std::cos(th), g.p[1] + g.p[2] * std::sin(th));
+    dph = make_double2(-g.p[2] * std::sin(th) * half, g.p[2] * std::cos(th) * half);
+  }
+}
+
+int make_segment_nodes(feast_ctx* h) {
+  std::vector<double> t, wt;
+  const int K = h->seg_k;
+  if (K < 1) return -1;
+  if (h->seg_rule == FEAST_RULE_TRAPEZOID) {
+    for (int k = 0; k < K; ++k) { t.push_back(-1.0 + (2.0 * k + 1.0) / K); wt.push_back(2.0 / K); }
+  } else if (h->seg_rule == FEAST_RULE_GAUSS_LEGENDRE) {
+    legendre_rule(K, t, wt);
+  } else {
+    return -1;
+  }
+  h->z.clear(); h->w.clear(); h->poly.clear();
+  for (const auto& g : h->segs) {
+    for (int k = 0; k < K; ++k) {
+      double2 ph, dph;
+      seg_phi(g, t[k], ph, dph);
+      h->z.push_back(ph);
+      // w phi' / (2 pi i) = (w / 2 pi) (Im phi', -Re phi')
+      h->w.push_back(make_double2(wt[k] * dph.y / (2.0 * M_PI), -wt[k] * dph.x / (2.0 * M_PI)));
+    }
+    for (int i = 0; i < 256; ++i) {   // polyline for the inside test
+      double2 ph, dph;
+      seg_phi(g, -1.0 + 2.0 * i / 256.0, ph, dph);
+      h->poly.push_back(ph);
+    }
+  }
+  h->q = (int)h->z.size();
+  return 0;
+}
+
+// Is mu inside the contour?  Ellipse: the analytic test (R2); composite contour:
+// crossing number of the closed polyline (256 points per segment).
+bool inside_contour(const feast_ctx* h, double x, double y) {
+  if (h->segs.empty()) {
+    const double u = (x - h->c_re) / h->r, v = (y - h->c_im) / (h->r * h->aspect);
+    return u * u + v * v < 1.0;
+  }
+  bool in = false;
+  const size_t np = h->poly.size();
+  for (size_t i = 0, j = np - 1; i < np; j = i++) {
+    const double2 a = h->poly[i], b = h->poly[j];
+    if ((a.y > y) != (b.y > y) && x < (b.x - a.x) * (y - a.y) / (b.y - a.y) + a.x) in = !in;
+  }
+  return in;
 }
 
 int make_nodes(feast_ctx* h) {
@@ -1104,8 +1170,7 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
     if (ritz) { ritz[2 * c] = lam[c].x; ritz[2 * c + 1] = lam[c].y; }
     const double rp = rn[c];  // ||x|| = 1
     if (resid) resid[c] = an > 0 ? rp / an : rp;
-    const double u = (lam[c].x - h->c_re) / h->r, v = (lam[c].y - h->c_im) / (h->r * h->aspect);
-    const bool inside = u * u + v * v < 1.0;
+    const bool inside = inside_contour(h, lam[c].x, lam[c].y);
     if (flags) flags[c] = (inside ? 1 : 0) | ((inside && rp <= 1e-4) ? 2 : 0);
   }
   return pst;
@@ -1133,6 +1198,69 @@ int feast_factor_cache(feast_handle h, int32_t enable) {
   return FEAST_OK;
 }
 
+int feast_set_contour(feast_handle h, int32_t nseg, const int32_t* kind, const double* params, int32_t k_per_segment,
+                      int32_t rule) {
+  if (!h) return FEAST_E_ARG;
+  if (h->ws) return fail(h, FEAST_E_STATE, "feast_set_contour must precede feast_workspace_bytes/bind%s");
+  if (nseg < 1 || !kind || !params || k_per_segment < 1 || k_per_segment > 2048 ||
+      (rule != FEAST_RULE_TRAPEZOID && rule != FEAST_RULE_GAUSS_LEGENDRE))
+    return fail(h, FEAST_E_ARG, "feast_set_contour: bad segment count, rule or nodes per segment%s");
+  std::vector<feast_ctx::Seg> segs(nseg);
+  for (int s = 0; s < nseg; ++s) {
+    if (kind[s] != 0 && kind[s] != 1) return fail(h, FEAST_E_ARG, "segment kind must be 0 (line) or 1 (arc)%s");
+    segs[s].kind = kind[s];
+    for (int i = 0; i < 5; ++i) segs[s].p[i] = params[5 * s + i];
+    if (kind[s] == 1 && !(segs[s].p[2] > 0)) return fail(h, FEAST_E_ARG, "arc radius must be > 0%s");
+  }
+  // closure and orientation (counter-clockwise: positive signed area of the polyline)
+  auto ends = [](const feast_ctx::Seg& g, double t) { double2 a, b; seg_phi(g, t, a, b); return a; };
+  double diam = 0.0, area = 0.0;
+  for (int s = 0; s < nseg; ++s) {
+    const double2 a = ends(segs[s], -1.0), b = ends(segs[(s + 1) % nseg], -1.0);
+    diam = std::max(diam, std::hypot(a.x - b.x, a.y - b.y));
+  }
+  for (int s = 0; s < nseg; ++s) {
+    const double2 e = ends(segs[s], 1.0), b = ends(segs[(s + 1) % nseg], -1.0);
+    if (std::hypot(e.x - b.x, e.y - b.y) > 1e-10 * std::max(diam, 1e-300))
+      return fail(h, FEAST_E_ARG, "contour segments do not close (end of segment s != start of s+1)%s");
+    for (int i = 0; i < 64; ++i) {
+      const double2 p0 = ends(segs[s], -1.0 + 2.0 * i / 64), p1 = ends(segs[s], -1.0 + 2.0 * (i + 1) / 64);
+      area += p0.x * p1.y - p1.x * p0.y;
+    }
+  }
+  if (!(area > 0)) return fail(h, FEAST_E_ARG, "contour must be counter-clockwise%s");
+  const auto old_segs = h->segs;
+  const int old_k = h->seg_k, old_rule = h->seg_rule;
+  h->segs = segs; h->seg_k = k_per_segment; h->seg_rule = rule;
+  if (make_segment_nodes(h) != 0 || h->q % h->world != 0 || setup_units(h) != 0) {
+    h->segs = old_segs; h->seg_k = old_k; h->seg_rule = old_rule;
+    if (h->segs.empty()) make_nodes(h); else make_segment_nodes(h);
+    setup_units(h);
+    return fail(h, FEAST_E_ARG, "contour: nodes do not divide over the ranks (or do not pair in real mode)%s");
+  }
+  // c_re, c_im: the centroid of the polyline (used only by diagnostics); r: half the diameter
+  double cx = 0, cy = 0;
+  for (const auto& p : h->poly) { cx += p.x; cy += p.y; }
+  h->c_re = cx / h->poly.size(); h->c_im = cy / h->poly.size(); h->r = 0.5 * diam;
+  return FEAST_OK;
+}
+
+int feast_filter(feast_handle h, int64_t npts, const double* mu, double* rho) {
+  if (!h || npts < 0 || (npts > 0 && (!mu || !rho))) return FEAST_E_ARG;
+  for (int64_t i = 0; i < npts; ++i) {
+    double sr = 0.0, si = 0.0;
+    for (int j = 0; j < h->q; ++j) {   // w_j / (z_j - mu)  (eq. quadrature_for_pi)
+      const double dr = h->z[j].x - mu[2 * i], di = h->z[j].y - mu[2 * i + 1];
+      const double d2 = dr * dr + di * di;
+      sr += (h->w[j].x * dr + h->w[j].y * di) / d2;
+      si += (h->w[j].y * dr - h->w[j].x * di) / d2;
+    }
+    rho[2 * i] = sr;
+    rho[2 * i + 1] = si;
+  }
+  return FEAST_OK;
+}
+
 int feast_set_complex_symmetric(feast_handle h, int32_t enable) {
   if (!h) return FEAST_E_ARG;
   if (h->ws) return fail(h, FEAST_E_STATE, "feast_set_complex_symmetric must precede feast_workspace_bytes/bind%s");
@@ -1146,7 +1274,8 @@ int feast_set_real_pencil(feast_handle h, int32_t enable) {
   if (!h) return FEAST_E_ARG;
   if (h->ws) return fail(h, FEAST_E_STATE, "feast_set_real_pencil must precede feast_workspace_bytes/bind%s");
   if (enable && h->cache_on) return fail(h, FEAST_E_STATE, "factor cache is not combined with real-pencil mode%s");
-  if (enable && h->c_im != 0.0) return fail(h, FEAST_E_ARG, "real-pencil mode needs a contour centre on the real axis%s");
+  if (enable && h->segs.empty() && h->c_im != 0.0)
+    return fail(h, FEAST_E_ARG, "real-pencil mode needs a contour centre on the real axis%s");
   if (enable && h->csym) return fail(h, FEAST_E_STATE, "complex-symmetric and real-pencil modes are exclusive%s");
   h->real = enable != 0;
   if (setup_units(h) != 0) {

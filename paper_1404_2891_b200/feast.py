@@ -33,7 +33,7 @@ ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, c
 EXPORTS = ["feast_init", "feast_workspace_bytes", "feast_bind_workspace", "feast_nodes", "feast_project",
            "feast_project_left", "feast_project_bi", "feast_reduce", "feast_set_allreduce", "feast_iterate",
            "feast_node_stats", "feast_factor_cache", "feast_set_real_pencil",
-           "feast_set_complex_symmetric", "feast_estimate_count", "feast_last_launch_count", "feast_profile", "feast_profile_summary",
+           "feast_set_complex_symmetric", "feast_estimate_count", "feast_set_contour", "feast_filter", "feast_last_launch_count", "feast_profile", "feast_profile_summary",
            "feast_profile_records", "feast_last_error",
            "feast_version", "feast_destroy"]
 K_CLASSES = ["shift", "panel", "laswp", "trsm", "zgemm", "perm", "accum", "other"]
@@ -74,6 +74,8 @@ def load_library(path: str = LIB_PATH):
     lib.feast_set_real_pencil.argtypes = [P, I32]
     lib.feast_set_complex_symmetric.argtypes = [P, I32]
     lib.feast_estimate_count.argtypes = [P, P, I64, P, I64, P, I64, P, I64, P]
+    lib.feast_set_contour.argtypes = [P, I32, P, P, I32, I32]
+    lib.feast_filter.argtypes = [P, I64, P, P]
     lib.feast_profile.argtypes = [P, I32]
     lib.feast_profile_summary.argtypes = [P, I32, P, P, P, P]
     lib.feast_profile_records.argtypes = [P, I64, P, P, P, P, P, P]
@@ -128,7 +130,7 @@ class Feast:
 
     def __init__(self, n, m0, center=0j, r=1.0, aspect=1.0, n_e=8, rule=RULE_TRAPEZOID, mode=RIGHT,
                  b_is_identity=True, rank=0, world=1, max_batch=0, device=None, group=None, real_pencil=False,
-                 complex_symmetric=False):
+                 complex_symmetric=False, segments=None, k_per_segment=8, segment_rule=RULE_TRAPEZOID):
         self.lib = load_library()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.stream = torch.cuda.current_stream(self.device)
@@ -142,6 +144,17 @@ class Feast:
         if rc != OK:
             raise FeastError(rc, "feast_init rejected the arguments")
         self.h = h
+        if segments is not None:   # composite contour (NEXT-4): [("line", a, b) | ("arc", c, R, th0, th1)]
+            kind = (ctypes.c_int32 * len(segments))()
+            par = (ctypes.c_double * (5 * len(segments)))()
+            for i, sg in enumerate(segments):
+                kind[i] = 0 if sg[0] == "line" else 1
+                vals = ([complex(sg[1]).real, complex(sg[1]).imag, complex(sg[2]).real, complex(sg[2]).imag, 0.0]
+                        if sg[0] == "line" else [complex(sg[1]).real, complex(sg[1]).imag, sg[2], sg[3], sg[4]])
+                for k, v in enumerate(vals):
+                    par[5 * i + k] = float(v)
+            self._check(self.lib.feast_set_contour(self.h, len(segments), kind, par, int(k_per_segment),
+                                                   int(segment_rule)))
         self.real_pencil = bool(real_pencil)
         if self.real_pencil:   # conjugate-pole pairs share one LU (NEXT-2b); before the workspace
             self._check(self.lib.feast_set_real_pencil(self.h, 1))
@@ -268,6 +281,15 @@ class Feast:
                                                          flags))
         lam = [complex(ritz[2 * i], ritz[2 * i + 1]) for i in range(m)]
         return {"lam": lam, "resid": list(res), "flags": list(flags)}
+
+    def filter(self, mu):
+        """rho(mu) = sum_j w_j / (z_j - mu) of this handle's quadrature at host points mu."""
+        import numpy as np
+        mu = np.ascontiguousarray(np.atleast_1d(mu), dtype=np.complex128)
+        out = np.zeros_like(mu)
+        self._check(self.lib.feast_filter(self.h, len(mu), mu.ctypes.data_as(ctypes.c_void_p),
+                                          out.ctypes.data_as(ctypes.c_void_p)))
+        return out
 
     def estimate_count(self, A, B, U, Q=None):
         """Eigenvalue-count estimate Re tr(U^H rho(B^-1 A) U) / m0 for a random block U (NEXT-3);

@@ -126,3 +126,58 @@ def test_real_pencil_units_and_guards():
     lib.feast_nodes(h, ctypes.byref(q), None, None, ctypes.byref(j0), ctypes.byref(j1))
     assert (q.value, j1.value - j0.value) == (4, 3)          # {1}, {i, -i}, {-1}
     lib.feast_destroy(h)
+
+
+def _contour(lib, h, segs, K, rule):
+    kind = (ctypes.c_int32 * len(segs))(*[0 if s[0] == "line" else 1 for s in segs])
+    par = (ctypes.c_double * (5 * len(segs)))()
+    for i, s in enumerate(segs):
+        vals = ([complex(s[1]).real, complex(s[1]).imag, complex(s[2]).real, complex(s[2]).imag, 0.0]
+                if s[0] == "line" else [complex(s[1]).real, complex(s[1]).imag, s[2], s[3], s[4]])
+        for k, v in enumerate(vals):
+            par[5 * i + k] = v
+    return lib.feast_set_contour(h, len(segs), kind, par, K, rule)
+
+
+@pytest.mark.parametrize("rule", [0, 2])
+def test_composite_contour_nodes_match_oracle(rule):
+    """NEXT-4: the library's glued-contour poles/weights (host code, written independently) equal
+    the oracle's; feast_filter equals the oracle's rho; open / clockwise chains are refused."""
+    lib = fb.load_library()
+    tri = [("line", -1, 1), ("line", 1, 1j), ("line", 1j, -1)]
+    semi = [("arc", 0.1, 0.8, 0.0, np.pi), ("line", 0.1 - 0.8, 0.1 + 0.8)]
+    for segs, K in ((tri, 8), (semi, 12)):
+        rc, h = _init(n=64, m0=8)
+        assert _contour(lib, h, segs, K, rule) == 0
+        q = ctypes.c_int32()
+        lib.feast_nodes(h, ctypes.byref(q), None, None, None, None)
+        z = (ctypes.c_double * (2 * q.value))()
+        w = (ctypes.c_double * (2 * q.value))()
+        lib.feast_nodes(h, None, z, w, None, None)
+        zl = np.frombuffer(z, dtype=np.complex128)
+        wl = np.frombuffer(w, dtype=np.complex128)
+        zo, wo = oracle.contour_nodes(segs, K, rule)
+        assert np.max(np.abs(zl - zo)) < 1e-14 and np.max(np.abs(wl - wo)) < 1e-14
+        mu = np.array([0.3j, 0.1 + 0.2j, 2.0, -0.5 - 0.5j], dtype=np.complex128)
+        out = np.zeros_like(mu)
+        assert lib.feast_filter(h, len(mu), mu.ctypes.data_as(ctypes.c_void_p), out.ctypes.data_as(ctypes.c_void_p)) == 0
+        assert np.max(np.abs(out - oracle.rho(zo, wo, mu))) < 1e-13
+        lib.feast_destroy(h)
+    rc, h = _init(n=64, m0=8)
+    assert _contour(lib, h, [("line", -1, 1), ("line", 1, 1j)], 4, rule) == -1          # open
+    assert _contour(lib, h, [("line", -1, 1j), ("line", 1j, 1), ("line", 1, -1)], 4, rule) == -1   # clockwise
+    lib.feast_destroy(h)
+
+
+def test_filter_endpoint_trapezoid_closed_forms():
+    """feast_filter on the paper's endpoint trapezoid K = 3 (q = 4) unit circle:
+    rho(0) = 1, rho(2) = -1/15, and max over |mu| = 2 of |rho| = 1/15 (the eta(2) of S:207)."""
+    lib = fb.load_library()
+    rc, h = _init(n=64, m0=8, c=0j, r=1.0, n_e=4, rule=1)
+    th = np.linspace(0, 2 * np.pi, 1024, endpoint=False)
+    mu = np.concatenate([[0.0, 2.0], 2 * np.exp(1j * th)]).astype(np.complex128)
+    out = np.zeros_like(mu)
+    lib.feast_filter(h, len(mu), mu.ctypes.data_as(ctypes.c_void_p), out.ctypes.data_as(ctypes.c_void_p))
+    assert abs(out[0] - 1) < 1e-14 and abs(out[1] + 1 / 15) < 1e-14
+    assert abs(np.max(np.abs(out[2:])) - 1 / 15) < 1e-12
+    lib.feast_destroy(h)

@@ -293,3 +293,20 @@ def test_count_estimate():
     est, _ = f.estimate_count(dev(P.A), dev(P.B), dev(P.X0))
     true_m = int(np.sum(np.abs(P.lam - P.spec.c) < P.spec.r))
     assert abs(est - true_m) <= 0.25 * true_m, (est, true_m)
+
+
+@pytest.mark.parametrize("segs,K,rule", [
+    ([("line", -0.4 - 0.4j, 0.4 - 0.4j), ("line", 0.4 - 0.4j, 0.4 + 0.4j), ("line", 0.4 + 0.4j, -0.4 + 0.4j),
+      ("line", -0.4 + 0.4j, -0.4 - 0.4j)], 8, synth.RULE_TRAPEZOID),
+    ([("arc", 0.0, 0.5, 0.0, np.pi), ("line", -0.5, 0.5)], 8, synth.RULE_GAUSS_LEGENDRE)])
+def test_composite_contour_projector(segs, K, rule):
+    """NEXT-4: square / semicircle contours glued from segments; Q matches the oracle
+    with the oracle's own contour nodes, and the spectral identity with rho evaluated by the oracle."""
+    P = synth.make_pencil("C1", n=150, m0=20)
+    zo, wo = oracle.contour_nodes(segs, K, rule)
+    f = Feast(P.n, P.m0, 0j, 1.0, 1.0, 8, 0, fb.RIGHT, True, segments=segs, k_per_segment=K, segment_rule=rule)
+    Q = host(f.project(dev(P.A), None, dev(P.X0)))
+    assert rel(Q, oracle.project(P.A, None, P.X0, zo, wo)) <= TOL
+    Qs = P.V @ (oracle.rho(zo, wo, P.lam)[:, None] * np.linalg.solve(P.V, P.X0))
+    assert rel(Q, Qs) <= TOL
+    assert np.max(np.abs(f.filter(P.lam[:5]) - oracle.rho(zo, wo, P.lam[:5]))) < 1e-12
