@@ -168,7 +168,10 @@ int feast_project_bi(feast_handle h, const void* A, int64_t lda, const void* B, 
 
 /* Reduced matrices (R-FEAST step 4; Bi-FEAST step 6):
  *   Ahat = QL^H A Q,  Bhat = QL^H B Q      (QL = Q in R-FEAST: pass QL = NULL)
- * Ahat, Bhat: m0 x m0 device, ld >= m0.  B = NULL when b_is_identity. */
+ * Ahat, Bhat: m0 x m0 device, ld >= m0.  B = NULL when b_is_identity.  Q (QL) must be the
+ * node-summed block.  With world > 1 and an all-reduce callback registered, the rows are
+ * sharded: rank r multiplies rows [r n/P, (r+1) n/P) of A (B) and the m0 x m0 partials are
+ * all-reduced through the callback, so every rank returns the complete Ahat, Bhat. */
 int feast_reduce(feast_handle h, const void* A, int64_t lda, const void* B, int64_t ldb,
                  const void* Q, int64_t ldq, const void* QL, int64_t ldql,
                  void* Ahat, int64_t ldah, void* Bhat, int64_t ldbh);

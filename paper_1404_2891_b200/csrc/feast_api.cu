@@ -568,7 +568,7 @@ int check_args_common(feast_ctx* h, const void* A, int64_t lda, const void* B, i
 // per node.  Pure enqueue (no host synchronisation), so it can be captured into a CUDA graph.
 void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2* B, int64_t ldb, const double2* X,
                      int64_t ldx, const double2* V, int64_t ldv, double2* Q, int64_t ldq, double2* QL, int64_t ldql,
-                     bool reuse) {
+                     bool reuse, bool rhs_ready) {
   const bool doR = X != nullptr, doL = V != nullptr;
   const int64_t n = h->n, m = h->m0, ld = h->ldc;
   const double2 one = make_double2(1, 0), zero = make_double2(0, 0);
@@ -577,9 +577,15 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
   int64_t ldr = ldx;
   const double2* Rl = V;
   int64_t ldrl = ldv;
-  if (!h->b_id) {
-    if (doR) { gemm_gen(h, n, m, n, false, B, ldb, X, ldx, h->R, ld, one, zero); Rr = h->R; ldr = ld; }
-    if (doL) { gemm_gen(h, n, m, n, true, B, ldb, V, ldv, h->RL, ld, one, zero); Rl = h->RL; ldrl = ld; }
+  if (!h->b_id) {   // (rhs_ready: formed row-sharded and all-reduced by project_impl)
+    if (doR) {
+      if (!rhs_ready) gemm_gen(h, n, m, n, false, B, ldb, X, ldx, h->R, ld, one, zero);
+      Rr = h->R; ldr = ld;
+    }
+    if (doL) {
+      if (!rhs_ready) gemm_gen(h, n, m, n, true, B, ldb, V, ldv, h->RL, ld, one, zero);
+      Rl = h->RL; ldrl = ld;
+    }
   }
   const int owned = h->j1 - h->j0;
   const int64_t mr = h->mr, st = ld * (n + mr);
@@ -673,6 +679,23 @@ int project_impl(feast_ctx* h, const double2* A, int64_t lda, const double2* B, 
   const int owned = h->j1 - h->j0;
   const bool reuse = h->cache_on && h->cache_valid && h->batch >= owned && h->cache_A == A && h->cache_B == B;
   const feast_ctx::GraphKey key{A, B, X, V, Q, QL, lda, ldb, ldx, ldv, ldq, ldql, reuse};
+  // a1 with world > 1: rank r forms rows [r n/P, (r+1) n/P) of R = B X (R_L = B^H V), the rest
+  // zero, and the all-reduce (sum) through the callback assembles the full block on every rank
+  // (an all-gather), before the (graph-captured) node loop reads it
+  const bool rhs_ready = !h->b_id && h->world > 1 && h->ar != nullptr && owned > 0;
+  if (rhs_ready) {
+    const int64_t n = h->n, m = h->m0, ld = h->ldc;
+    const int64_t r0 = h->rank * n / h->world, r1 = (h->rank + 1) * n / h->world;
+    const double2 one = make_double2(1, 0), zero = make_double2(0, 0);
+    for (int k = 0; k < 2; ++k) {
+      if (k == 0 ? X == nullptr : V == nullptr) continue;
+      double2* R = k == 0 ? h->R : h->RL;
+      CUDA_TRY(h, cudaMemsetAsync(R, 0, (size_t)ld * m * 16, h->stream));
+      if (k == 0) gemm_gen(h, r1 - r0, m, n, false, B + r0, ldb, X, ldx, R + r0, ld, one, zero);
+      else gemm_gen(h, r1 - r0, m, n, true, B + r0 * ldb, ldb, V, ldv, R + r0, ld, one, zero);
+      if (h->ar(R, 2 * ld * m, h->stream, h->ar_user)) return fail(h, FEAST_E_COMM, "all-reduce failed%s");
+    }
+  }
   const bool use_graph = h->graphs && !feast::prof().on;
   if (use_graph && h->gexec && h->gkey == key) {
     CUDA_TRY(h, cudaGraphLaunch(h->gexec, h->stream));
@@ -683,7 +706,7 @@ int project_impl(feast_ctx* h, const double2* A, int64_t lda, const double2* B, 
     cudaGraph_t g = nullptr;
     const int64_t c0 = feast::g_launches;
     CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-    project_enqueue(h, A, lda, B, ldb, X, ldx, V, ldv, Q, ldq, QL, ldql, reuse);
+    project_enqueue(h, A, lda, B, ldb, X, ldx, V, ldv, Q, ldq, QL, ldql, reuse, rhs_ready);
     const cudaError_t ce = cudaStreamEndCapture(h->stream, &g);
     h->glaunches = feast::g_launches - c0;
     feast::g_launches = c0;
@@ -693,7 +716,7 @@ int project_impl(feast_ctx* h, const double2* A, int64_t lda, const double2* B, 
       if (g) cudaGraphDestroy(g);
       h->gexec = nullptr;
       h->graphs = false;   // capture unsupported here: keep launching the same kernels eagerly
-      project_enqueue(h, A, lda, B, ldb, X, ldx, V, ldv, Q, ldq, QL, ldql, reuse);
+      project_enqueue(h, A, lda, B, ldb, X, ldx, V, ldv, Q, ldq, QL, ldql, reuse, rhs_ready);
     } else {
       cudaGraphDestroy(g);
       h->gkey = key;
@@ -701,7 +724,7 @@ int project_impl(feast_ctx* h, const double2* A, int64_t lda, const double2* B, 
       feast::count_launch((int)h->glaunches);
     }
   } else {
-    project_enqueue(h, A, lda, B, ldb, X, ldx, V, ldv, Q, ldq, QL, ldql, reuse);
+    project_enqueue(h, A, lda, B, ldb, X, ldx, V, ldv, Q, ldq, QL, ldql, reuse, rhs_ready);
     h->gseen = key;
     h->gseen_valid = true;
   }
@@ -1013,6 +1036,54 @@ int feast_project_bi(feast_handle h, const void* A, int64_t lda, const void* B, 
                       (double2*)Q, ldq, (double2*)QL, ldql);
 }
 
+}  // extern "C"
+
+namespace {
+// a7 with the rows of A Q (B Q) split over the ranks when `shard` (world > 1 and an all-reduce
+// callback): rank r forms AQ for rows [r n/P, (r+1) n/P) and the partial QL_r^H AQ_r; one
+// all-reduce of the two m0 x m0 partials completes Ahat, Bhat ("must be
+// row-sharded across ranks").  Without sharding every rank forms the whole product (AQ / BQ
+// stay complete in the workspace, as feast_iterate's residuals need).
+int reduce_impl(feast_ctx* h, const void* A, int64_t lda, const void* B, int64_t ldb, const void* Q, int64_t ldq,
+                const void* QL, int64_t ldql, void* Ahat, int64_t ldah, void* Bhat, int64_t ldbh, bool shard) {
+  const int64_t n = h->n, m = h->m0, ld = h->ldc;
+  const double2 one = make_double2(1, 0), zero = make_double2(0, 0);
+  const double2* Qr = (const double2*)Q;
+  const double2* Ql = QL ? (const double2*)QL : Qr;
+  if (!QL) ldql = ldq;
+  const int64_t t0 = feast::g_launches;
+  shard = shard && h->world > 1 && h->ar != nullptr;
+  const int64_t r0 = shard ? h->rank * n / h->world : 0, r1 = shard ? (h->rank + 1) * n / h->world : n, nr = r1 - r0;
+  // a7: AQ = A Q, BQ = B Q, Ahat = QL^H AQ, Bhat = QL^H BQ  (rows [r0, r1) when sharded)
+  gemm_gen(h, nr, m, n, false, (const double2*)A + r0, lda, Qr, ldq, h->AQ + r0, ld, one, zero);
+  gemm_gen(h, m, m, nr, true, Ql + r0, ldql, h->AQ + r0, ld, (double2*)Ahat, ldah, one, zero);
+  if (!h->b_id) {
+    gemm_gen(h, nr, m, n, false, (const double2*)B + r0, ldb, Qr, ldq, h->BQ + r0, ld, one, zero);
+    gemm_gen(h, m, m, nr, true, Ql + r0, ldql, h->BQ + r0, ld, (double2*)Bhat, ldbh, one, zero);
+  } else {
+    gemm_gen(h, m, m, nr, true, Ql + r0, ldql, Qr + r0, ldq, (double2*)Bhat, ldbh, one, zero);
+  }
+  CUDA_TRY(h, cudaGetLastError());
+  if (shard) {
+    for (int k = 0; k < 2; ++k) {
+      double2* M = (double2*)(k ? Bhat : Ahat);
+      const int64_t ldm = k ? ldbh : ldah;
+      if (ldm == m) {
+        if (h->ar(M, 2 * m * m, h->stream, h->ar_user)) return fail(h, FEAST_E_COMM, "all-reduce failed%s");
+      } else {
+        for (int64_t c = 0; c < m; ++c)
+          if (h->ar(M + c * ldm, 2 * m, h->stream, h->ar_user)) return fail(h, FEAST_E_COMM, "all-reduce failed%s");
+      }
+    }
+  }
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  h->launches = feast::g_launches - t0;
+  return FEAST_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int feast_reduce(feast_handle h, const void* A, int64_t lda, const void* B, int64_t ldb, const void* Q, int64_t ldq,
                  const void* QL, int64_t ldql, void* Ahat, int64_t ldah, void* Bhat, int64_t ldbh) {
   int e = check_args_common(h, A, lda, B, ldb);
@@ -1020,25 +1091,7 @@ int feast_reduce(feast_handle h, const void* A, int64_t lda, const void* B, int6
   if (!Q || !Ahat || !Bhat || ldq < h->n || ldah < h->m0 || ldbh < h->m0 || (QL && ldql < h->n))
     return fail(h, FEAST_E_ARG, "reduce: null pointer or bad ld%s");
   Join j_(h);
-  const int64_t n = h->n, m = h->m0, ld = h->ldc;
-  const double2 one = make_double2(1, 0), zero = make_double2(0, 0);
-  const double2* Qr = (const double2*)Q;
-  const double2* Ql = QL ? (const double2*)QL : Qr;
-  if (!QL) ldql = ldq;
-  const int64_t t0 = feast::g_launches;
-  // a7: AQ = A Q, BQ = B Q, Ahat = QL^H AQ, Bhat = QL^H BQ
-  gemm_gen(h, n, m, n, false, (const double2*)A, lda, Qr, ldq, h->AQ, ld, one, zero);
-  gemm_gen(h, m, m, n, true, Ql, ldql, h->AQ, ld, (double2*)Ahat, ldah, one, zero);
-  if (!h->b_id) {
-    gemm_gen(h, n, m, n, false, (const double2*)B, ldb, Qr, ldq, h->BQ, ld, one, zero);
-    gemm_gen(h, m, m, n, true, Ql, ldql, h->BQ, ld, (double2*)Bhat, ldbh, one, zero);
-  } else {
-    gemm_gen(h, m, m, n, true, Ql, ldql, Qr, ldq, (double2*)Bhat, ldbh, one, zero);
-  }
-  CUDA_TRY(h, cudaGetLastError());
-  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-  h->launches = feast::g_launches - t0;
-  return FEAST_OK;
+  return reduce_impl(h, A, lda, B, ldb, Q, ldq, QL, ldql, Ahat, ldah, Bhat, ldbh, true);
 }
 
 int feast_estimate_count(feast_handle h, const void* A, int64_t lda, const void* B, int64_t ldb, const void* U,
@@ -1109,7 +1162,7 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
   if ((e = orth(it.Qr))) return e;
   if (bi && (e = orth(it.Ql))) return e;
   // step 4 / 6: reduced matrices
-  e = feast_reduce(h, A, lda, B, ldb, it.Qr, n, bi ? it.Ql : nullptr, n, it.Ah, m, it.Bh, m);
+  e = reduce_impl(h, A, lda, B, ldb, it.Qr, n, bi ? it.Ql : nullptr, n, it.Ah, m, it.Bh, m, false);
   if (e) return e;
   // step 5 / 7 (outside the hot path): M = Bh^-1 Ah, eig(M) -> lam, W
   CUDA_TRY(h, cudaMemcpyAsync(it.T, it.Bh, m * m * 16, cudaMemcpyDeviceToDevice, h->stream));

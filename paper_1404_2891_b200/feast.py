@@ -117,6 +117,13 @@ def allreduce_node_sum(t: torch.Tensor, group=None) -> torch.Tensor:
     return t
 
 
+def _dist_world(group=None) -> int:
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group)
+    return 1
+
+
 class _CudaPtr:
     """__cuda_array_interface__ shim so the all-reduce callback can wrap a raw buffer."""
 
@@ -167,7 +174,10 @@ class Feast:
         aligned = (base + 255) // 256 * 256
         self._check(self.lib.feast_bind_workspace(self.h, ctypes.c_void_p(aligned), int(nbytes.value)))
         self._ar = None
-        if self.world > 1:
+        if self.world > 1 and _dist_world(group) == self.world:
+            # node sums (and the row-sharded a1 / a7 assemblies) through torch.distributed (NCCL);
+            # without an initialised process group of this size (e.g. virtual ranks in one
+            # process) no callback is registered and calls return this rank's partials
             self._ar = ALLREDUCE_FN(self._allreduce_cb)
             self._check(self.lib.feast_set_allreduce(self.h, self._ar, None))
 

@@ -310,3 +310,62 @@ def test_composite_contour_projector(segs, K, rule):
     Qs = P.V @ (oracle.rho(zo, wo, P.lam)[:, None] * np.linalg.solve(P.V, P.X0))
     assert rel(Q, Qs) <= TOL
     assert np.max(np.abs(f.filter(P.lam[:5]) - oracle.rho(zo, wo, P.lam[:5]))) < 1e-12
+
+
+def test_row_sharded_reduce_partials():
+    """a7 row-sharded over ranks: each virtual rank's m0 x m0 partial
+    (rows [r n/P, (r+1) n/P) of A Q and B Q) is handed to the all-reduce callback; the partials
+    of all ranks sum to QL^H A Q and QL^H B Q (checked against the unsharded product)."""
+    import ctypes
+    P = synth.make_pencil("C2", n=230, m0=18)
+    world = 4                # q = 16 nodes over 4 ranks; 230 rows split 57/58 (ragged)
+    A, B, Q = dev(P.A), dev(P.B), dev(synth.random_block(P.n, P.m0, 5))
+    full = _handle(P)
+    Ah, Bh = full.reduce(A, B, Q)
+    Ah, Bh = host(Ah), host(Bh)
+    got = {"A": 0, "B": 0}
+    for r in range(world):
+        f = _handle(P, rank=r, world=world)
+        seen = []
+
+        def cb(buf, count, stream, user, seen=seen):
+            torch.cuda.synchronize()
+            t = torch.as_tensor(fb._CudaPtr(buf, count), device="cuda")
+            seen.append(t.clone().view(torch.complex128).cpu().numpy())
+            return 0
+
+        f._ar = fb.ALLREDUCE_FN(cb)
+        assert f.lib.feast_set_allreduce(f.h, f._ar, None) == 0
+        pa, pb = f.reduce(A, B, Q)
+        assert len(seen) == 2   # Ahat, Bhat partials (ld = m0: one call each)
+        got["A"] = got["A"] + seen[0].reshape(P.m0, P.m0).T
+        got["B"] = got["B"] + seen[1].reshape(P.m0, P.m0).T
+    assert rel(got["A"], Ah) <= 1e-12 and rel(got["B"], Bh) <= 1e-12
+
+
+def test_row_sharded_rhs_partials():
+    """a1 row-sharded over ranks: rank r forms rows [r n/P, (r+1) n/P) of R = B X (zeros
+    elsewhere) and hands the block to the all-reduce callback, whose sum over ranks must be B X."""
+    P = synth.make_pencil("C2", n=230, m0=18)
+    world = 4
+    A, B, X = dev(P.A), dev(P.B), dev(P.X0)
+    total = 0
+    for r in range(world):
+        f = _handle(P, rank=r, world=world)
+        seen = []
+
+        def cb(buf, count, stream, user, seen=seen):
+            torch.cuda.synchronize()
+            t = torch.as_tensor(fb._CudaPtr(buf, count), device="cuda")
+            seen.append(t.clone().view(torch.complex128).cpu().numpy())
+            return 0
+
+        f._ar = fb.ALLREDUCE_FN(cb)
+        assert f.lib.feast_set_allreduce(f.h, f._ar, None) == 0
+        f.project(A, B, X, allreduce=False)
+        ld = seen[0].size // P.m0
+        part = seen[0].reshape(P.m0, ld).T[:P.n]
+        r0, r1 = r * P.n // world, (r + 1) * P.n // world
+        assert np.all(part[:r0] == 0) and np.all(part[r1:] == 0)
+        total = total + part
+    assert rel(total, P.B @ P.X0) <= 1e-13
