@@ -52,7 +52,8 @@ struct feast_ctx {
   bool own_stream = false;
   int nb = 64;
   feast::PanelCfg pcfg{};
-  int smem_cs = 0;   // cluster size of the shared-memory panel kernel (0: register-chunk kernel)
+  int smem_cs = 0;   // cluster size of the shared-memory panel kernel for the full height (0: too tall)
+  int smem_cs_max = 16;  // largest cluster the shared-memory panel may use (FEAST_CS_MAX)
   bool lookahead = true;
   bool cache_on = false, cache_valid = false;   // factor-once reuse across calls
   const void *cache_A = nullptr, *cache_B = nullptr;
@@ -370,10 +371,17 @@ void gemm_gen(feast_ctx* h, int64_t M, int64_t N, int64_t K, bool conjA, const d
 }
 
 // ---------------------------------------------------------------- blocked LU (batched)
+// The cluster panel with the panel in shared memory whenever the remaining height L = n - k fits
+// clusters of <= smem_cs_max CTAs x 256 rows (the launch shrinks the cluster further as L falls);
+// the register-chunk panel (64 wide, rows swapped in global memory) for taller panels.
+bool smem_panel_for(const feast_ctx* h, int64_t k) {
+  return h->smem_cs_max > 0 && (h->n - k + h->smem_cs_max - 1) / h->smem_cs_max <= 256;
+}
+
 void panel_at(feast_ctx* h, const Lu& v, int64_t k, int w, cudaStream_t s) {
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr);
-  if (h->smem_cs)
-    feast::panel_smem_launch(bat(v.Cw, ld, st), n, k, w, v.ipiv, v.stats, v.info, v.nbat, h->smem_cs, s);
+  if (smem_panel_for(h, k))
+    feast::panel_smem_launch(bat(v.Cw, ld, st), n, k, w, v.ipiv, v.stats, v.info, v.nbat, h->smem_cs_max, s);
   else
     feast::panel_launch(bat(v.Cw, ld, st), n, k, w, v.ipiv, v.stats, v.info, v.nbat, h->pcfg, s);
 }
@@ -393,15 +401,16 @@ void factor_block(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, cudaStream_
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr);
   double2* C = v.Cw;
   const int nbat = v.nbat;
-  const int64_t wp = h->smem_cs ? h->wp : 64;
   for (int64_t ki = K0; ki < K0 + Wo; ki += 64) {
     const int wi = (int)std::min<int64_t>(64, K0 + Wo - ki);
+    const bool smem = smem_panel_for(h, ki);
+    const int64_t wp = smem ? h->wp : 64;
     // the 64-block is factored as narrow cluster panels of wp columns (small SM footprint), with
     // the in-block U12 (warp TRSM) and update (DMMA) between them
     for (int64_t kp = ki; kp < ki + wi; kp += wp) {
       const int wpp = (int)std::min<int64_t>(wp, ki + wi - kp);
       panel_at(h, v, kp, wpp, s);
-      if (h->smem_cs) {
+      if (smem) {
         feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, K0 + Wo, nbat, s);
       } else {   // the register-chunk panel already swapped its own columns
         feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, kp, nbat, s);
@@ -894,8 +903,13 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
     const int v = atoi(e);
     if (v >= 1 && v <= 16 && feast::panel_smem_fits(n, (int)h->wp, v)) h->smem_cs = v;
   }
+  h->smem_cs_max = std::max(h->smem_cs, 16);
+  if (const char* e = getenv("FEAST_CS_MAX")) {
+    const int v = atoi(e);
+    if (v == 0 || v == 1 || v == 2 || v == 4 || v == 8 || v == 16) h->smem_cs_max = v;
+  }
   if (const char* e = getenv("FEAST_PANEL")) {   // debugging override: "reg" = register-chunk kernel
-    if (e[0] == 'r') { h->smem_cs = 0; h->nb = 64; }
+    if (e[0] == 'r') { h->smem_cs = 0; h->smem_cs_max = 0; h->nb = 64; }
   }
   if (const char* e = getenv("FEAST_LOOKAHEAD")) h->lookahead = e[0] != '0';
   if (const char* e = getenv("FEAST_GRAPH")) h->graphs = e[0] != '0';

@@ -122,8 +122,10 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
   __shared__ double2 L11s[WC][WC];               // chunk pivot rows' chunk values
   __shared__ __align__(16) double2 U12s[WC][WMAX];   // chunk pivot rows' rest-of-panel values
   __shared__ int pvt[WMAX];                      // pivot (panel row index) per column
-  __shared__ unsigned long long wkey[PT / 32];
-  __shared__ double2 wrow[PT / 32][WC + 1];
+  // per-warp candidates, double-buffered by column parity (a single-CTA "cluster" decides the
+  // pivot straight from them: one __syncthreads per column, no DSMEM exchange)
+  __shared__ unsigned long long wkey[2][PT / 32];
+  __shared__ double2 wrow[2][PT / 32][WC + 1];
   __shared__ __align__(8) unsigned long long mbar[4];   // slots[0], slots[1], U12s, load
   __shared__ int pos2row[WMAX], cur[WMAX];
 
@@ -191,7 +193,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
       const int buf = col & 1;
       const uint32_t bar = saddr(&mbar[buf]);
       PTRACE(8 + 4 * col);
-      if (tid == 0) mbar_arm(bar, (uint32_t)(CS * SLOT_BYTES));
+      if (tid == 0 && CS > 1) mbar_arm(bar, (uint32_t)(CS * SLOT_BYTES));
       unsigned long long bk = 0ull;
       int bs = -1;
 #pragma unroll
@@ -225,42 +227,52 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
         for (int s = 0; s < S; ++s)
           if (s == bs) {
 #pragma unroll
-            for (int q = 0; q < WC; ++q) wrow[warp][q] = a[s][q];
-            wrow[warp][WC] = myrcp;
+            for (int q = 0; q < WC; ++q) wrow[buf][warp][q] = a[s][q];
+            wrow[buf][warp][WC] = myrcp;
           }
       }
-      if (lane == 0) wkey[warp] = wk;
+      if (lane == 0) wkey[buf][warp] = wk;
       __syncthreads();
-      unsigned long long ck = wkey[0];
+      unsigned long long ck = wkey[buf][0];
       int cw = 0;
 #pragma unroll
       for (int q = 1; q < PT / 32; ++q)
-        if (wkey[q] > ck) { ck = wkey[q]; cw = q; }
+        if (wkey[buf][q] > ck) { ck = wkey[buf][q]; cw = q; }
       PTRACE(9 + 4 * col);
-      // push {row[WC], key, 1/pivot} into slot [buf][crank] of every CTA (st.async -> its mbarrier)
-      for (int t = tid; t < CS * (WC + 2); t += PT) {
-        const int dcta = t / (WC + 2), e = t - dcta * (WC + 2);
-        const uint32_t rslot = mapa(saddr(&slots[buf][crank]), dcta);
-        const uint32_t rbar = mapa(bar, dcta);
-        double2 v;
-        if (e < WC) v = ck ? wrow[cw][e] : make_double2(0.0, 0.0);
-        else if (e == WC) v = make_double2(__longlong_as_double((long long)ck), 0.0);
-        else v = ck ? wrow[cw][WC] : make_double2(0.0, 0.0);
-        st_async16(rslot + e * 16, v, rbar);
+      unsigned long long gk;
+      const double2* prow;
+      double2 pinv;
+      if (CS == 1) {
+        // single CTA: the CTA winner is the pivot
+        gk = ck;
+        prow = wrow[buf][cw];
+        pinv = wrow[buf][cw][WC];
+      } else {
+        // push {row[WC], key, 1/pivot} into slot [buf][crank] of every CTA (st.async -> its mbarrier)
+        for (int t = tid; t < CS * (WC + 2); t += PT) {
+          const int dcta = t / (WC + 2), e = t - dcta * (WC + 2);
+          const uint32_t rslot = mapa(saddr(&slots[buf][crank]), dcta);
+          const uint32_t rbar = mapa(bar, dcta);
+          double2 v;
+          if (e < WC) v = ck ? wrow[buf][cw][e] : make_double2(0.0, 0.0);
+          else if (e == WC) v = make_double2(__longlong_as_double((long long)ck), 0.0);
+          else v = ck ? wrow[buf][cw][WC] : make_double2(0.0, 0.0);
+          st_async16(rslot + e * 16, v, rbar);
+        }
+        mbar_wait(bar, (uint32_t)((col >> 1) & 1));
+        PTRACE(10 + 4 * col);
+        // global pivot: lanes read the CS keys, 64-bit max by REDUX (every warp, same result)
+        const unsigned long long lk = lane < CS ? slots[buf][lane].key : 0ull;
+        gk = warp_max_key(lk);
+        const int gb = __ffs(__ballot_sync(0xffffffffu, lane < CS && lk == gk)) - 1;
+        prow = slots[buf][gb].row;
+        pinv = slots[buf][gb].pinv;
       }
-      mbar_wait(bar, (uint32_t)((col >> 1) & 1));
-      PTRACE(10 + 4 * col);
-      // global pivot: lanes read the CS keys, 64-bit max by REDUX (every warp, same result)
-      const unsigned long long lk = lane < CS ? slots[buf][lane].key : 0ull;
-      const unsigned long long gk = warp_max_key(lk);
-      const int gb = __ffs(__ballot_sync(0xffffffffu, lane < CS && lk == gk)) - 1;
       const int gi = key_row(gk);
-      const double2* prow = slots[buf][gb].row;
       if (tid < WC) L11s[jj][tid] = prow[tid];
       if (tid == 0) pvt[col] = gi;
       const double2 p = prow[jj];
       const bool pzero = (p.x == 0.0 && p.y == 0.0);
-      const double2 pinv = slots[buf][gb].pinv;
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const int r = tid + s * PT;
@@ -296,20 +308,23 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
     if (c1 < w) {
       const int rem = w - c1;
       const uint32_t ubar = saddr(&mbar[2]);
-      if (tid == 0) mbar_arm(ubar, (uint32_t)(wc * rem * 16));
+      if (tid == 0 && CS > 1) mbar_arm(ubar, (uint32_t)(wc * rem * 16));
       __syncthreads();
-      // owners push the chunk pivot rows' rest-of-panel values to every CTA
+      // owners push the chunk pivot rows' rest-of-panel values to every CTA (single CTA: plain
+      // shared-memory copies and a barrier)
       for (int jj = 0; jj < wc; ++jj) {
         const int pr = pvt[j0 + jj] - rbeg;
         if (pr >= 0 && pr < nrow) {
           for (int idx = tid; idx < rem * CS; idx += PT) {
             const int dcta = idx / rem, c = idx - dcta * rem;
-            st_async16(mapa(saddr(&U12s[jj][c]), dcta), P[(c1 - WC + c) * PLD + pr], mapa(ubar, dcta));
+            if (CS == 1) U12s[jj][c] = P[(c1 - WC + c) * PLD + pr];
+            else st_async16(mapa(saddr(&U12s[jj][c]), dcta), P[(c1 - WC + c) * PLD + pr], mapa(ubar, dcta));
           }
         }
       }
       PTRACE(300 + 4 * chunk);
-      mbar_wait(ubar, (uint32_t)(chunk & 1));
+      if (CS == 1) __syncthreads();
+      else mbar_wait(ubar, (uint32_t)(chunk & 1));
       PTRACE(301 + 4 * chunk);
       // U12 = L11^-1 (pivot rows), unit lower L11 (chunk multipliers of the pivot rows)
       for (int c = tid; c < rem; c += PT) {

@@ -11,16 +11,18 @@ namespace feast { inline void panel_trace_read(unsigned long long*) {} }
 #endif
 int main(int argc, char** argv) {
   int W = argc > 1 ? atoi(argv[1]) : 64, CS = argc > 2 ? atoi(argv[2]) : 16;
-  int n = 2048; int64_t ld = n;
-  std::vector<double2> h((size_t)n * n);
+  int n = argc > 3 ? atoi(argv[3]) : 2048; int64_t ld = n;
+  int batch = argc > 4 ? atoi(argv[4]) : 1;
+  std::vector<double2> h((size_t)n * n * batch);
   srand(1);
   for (auto& v : h) { v.x = rand() / (double)RAND_MAX - 0.5; v.y = rand() / (double)RAND_MAX - 0.5; }
   double2* d; cudaMalloc(&d, h.size() * 16); cudaMemcpy(d, h.data(), h.size() * 16, cudaMemcpyHostToDevice);
-  int32_t* ipiv; cudaMalloc(&ipiv, n * 4); double* st; cudaMalloc(&st, 16); int32_t* inf; cudaMalloc(&inf, 4);
-  feast::stats_init_launch(st, inf, 1, 0);
+  int32_t* ipiv; cudaMalloc(&ipiv, (size_t)n * 4 * batch); double* st; cudaMalloc(&st, 16 * batch);
+  int32_t* inf; cudaMalloc(&inf, 4 * batch);
+  feast::stats_init_launch(st, inf, batch, 0);
   for (int rep = 0; rep < 3; ++rep) {
     cudaMemcpy(d, h.data(), h.size() * 16, cudaMemcpyHostToDevice);
-    feast::panel_smem_launch(feast::Batched{d, ld, ld * n}, n, 0, W, ipiv, st, inf, 1, CS, 0);
+    feast::panel_smem_launch(feast::Batched{d, ld, ld * n}, n, 0, W, ipiv, st, inf, batch, CS, 0);
     cudaDeviceSynchronize();
   }
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
