@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
 #include <string>
 #include <vector>
 
@@ -1166,6 +1167,19 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
     if (bi && h->ar(it.Ql, 2 * n * m, h->stream, h->ar_user)) return fail(h, FEAST_E_COMM, "all-reduce failed%s");
   }
   // orthonormalise U^ (and V^) (reading R13), cuSOLVER Householder QR
+  // FEAST_TIMING=1: host wall time of the iteration phases (stream-synchronised), to stderr
+  static const bool timing = getenv("FEAST_TIMING") != nullptr;
+  auto tmark = [&](const char* what) {
+    if (!timing) return;
+    static double last = 0.0;
+    cudaStreamSynchronize(h->stream);
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    const double now = ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+    if (what) fprintf(stderr, "feast_iterate %-12s %8.3f ms\n", what, now - last);
+    last = now;
+  };
+  tmark(nullptr);
   auto orth = [&](double2* Qb) -> int {
     SOL_TRY(h, cusolverDnZgeqrf(h->sol, (int)n, (int)m, (cuDoubleComplex*)Qb, (int)n, (cuDoubleComplex*)it.tau,
                                 (cuDoubleComplex*)it.sw, (int)(it.sw_bytes / 16), it.info));
@@ -1173,11 +1187,13 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
                                 (cuDoubleComplex*)it.sw, (int)(it.sw_bytes / 16), it.info));
     return 0;
   };
+  tmark("project");
   if ((e = orth(it.Qr))) return e;
   if (bi && (e = orth(it.Ql))) return e;
   // step 4 / 6: reduced matrices
   e = reduce_impl(h, A, lda, B, ldb, it.Qr, n, bi ? it.Ql : nullptr, n, it.Ah, m, it.Bh, m, false);
   if (e) return e;
+  tmark("qr+reduce");
   // step 5 / 7 (outside the hot path): M = Bh^-1 Ah, eig(M) -> lam, W
   CUDA_TRY(h, cudaMemcpyAsync(it.T, it.Bh, m * m * 16, cudaMemcpyDeviceToDevice, h->stream));
   CUDA_TRY(h, cudaMemcpyAsync(it.M, it.Ah, m * m * 16, cudaMemcpyDeviceToDevice, h->stream));
@@ -1196,6 +1212,7 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
     snprintf(b, sizeof b, "%d", hinfo);
     return fail(h, FEAST_E_REDUCED, "reduced eigensolver info = %s", b);
   }
+  tmark("reduced-eig");
   // step 6 / 8: X = U^ W with unit columns (scale folded into W)
   gemm_gen(h, n, m, m, false, it.Qr, n, it.W, m, (double2*)X, ldx, one, zero);
   feast::resid_launch((double2*)X, (double2*)X, (double2*)X, ldx, it.lam, n, m, it.rn, it.xn, h->stream);
@@ -1233,6 +1250,7 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
   double an = 0.0;
   for (double v : fr) an += v;
   an = std::sqrt(an);
+  tmark("ritz+resid");
   for (int64_t c = 0; c < m; ++c) {
     if (ritz) { ritz[2 * c] = lam[c].x; ritz[2 * c + 1] = lam[c].y; }
     const double rp = rn[c];  // ||x|| = 1
