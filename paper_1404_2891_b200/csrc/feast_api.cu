@@ -9,6 +9,7 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -463,14 +464,27 @@ void outer_update(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, int64_t c0,
   }
 }
 
-void lu_batched(feast_ctx* h, const Lu& v, int64_t aug) {
+// rest(s): enqueues the formation of the columns beyond the first outer block on stream s
+void lu_batched(feast_ctx* h, const Lu& v, int64_t aug, const std::function<void(cudaStream_t)>& rest = nullptr) {
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), ntot = n + aug;
   double2* C = v.Cw;
   const int nbat = v.nbat;
   cudaStream_t sm = v.sm, sp = v.sp;
   const int64_t NBO = h->nbo;
   int64_t Wo = std::min<int64_t>(NBO, n);
-  factor_block(h, v, 0, Wo, sm);
+  if (rest && h->lookahead && !h->prof_serial && Wo < n) {
+    // the first block is factored on the high-priority side stream while the main stream forms
+    // the rest of [C_j | R] (HBM-bound, needed only once the block is done)
+    cudaEventRecord(v.ev_a, sm);
+    cudaStreamWaitEvent(sp, v.ev_a, 0);
+    factor_block(h, v, 0, Wo, sp);
+    cudaEventRecord(v.ev_p, sp);
+    rest(sm);
+    cudaStreamWaitEvent(sm, v.ev_p, 0);
+  } else {
+    if (rest) rest(sm);
+    factor_block(h, v, 0, Wo, sm);
+  }
   if (v.ev_first) cudaEventRecord(v.ev_first, sm);   // releases the next (staggered) group
   feast::laswp_launch(bat(C, ld, st), n, 0, (int)Wo, v.ipiv, Wo, ntot, nbat, sm);
   for (int64_t K0 = 0; K0 < n; K0 += Wo, Wo = std::min<int64_t>(NBO, n - K0)) {
@@ -625,16 +639,23 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
       if (g) cudaStreamWaitEvent(v.sm, (h->stagger && g > 0) ? h->gev_first[g - 1] : h->ev_fork, 0);
       if (!reuse) {
         feast::stats_init_launch(v.stats, v.info, v.nbat, v.sm);
-        // a2: C_j = z_j B - A ; R appended as extra columns (augmented system [C_j | R])
-        feast::shift_launch(bat(v.Cw, ld, st), A, lda, B, ldb, h->zd + j + b0, n, v.nbat, v.sm);
-        if (doR)
-          feast::broadcast_copy_launch(bat(v.Cw + n * ld, ld, st), Rr, ldr, n, m, v.nbat,
-                                       pair ? feast::BC_PAIR : feast::BC_COPY, v.sm);
-        if (csl)
-          feast::broadcast_copy_launch(bat(v.Cw + (n + (doR ? m : 0)) * ld, ld, st), Rl, ldrl, n, m, v.nbat,
-                                       feast::BC_CONJ, v.sm);
+        // a2: C_j = z_j B - A ; R appended as extra columns (augmented system [C_j | R]).  Only the
+        // first outer block's columns are formed before its factorisation starts; lu_batched
+        // forms the rest underneath it (needed only once the block is factored).
+        const int64_t w0 = std::min<int64_t>(h->nbo, n);
+        const double2* zj = h->zd + j + b0;
+        feast::shift_launch(bat(v.Cw, ld, st), A, lda, B, ldb, zj, n, v.nbat, v.sm, 0, w0);
+        auto rest = [&, zj](cudaStream_t sr) {
+          feast::shift_launch(bat(v.Cw, ld, st), A, lda, B, ldb, zj, n, v.nbat, sr, w0, n);
+          if (doR)
+            feast::broadcast_copy_launch(bat(v.Cw + n * ld, ld, st), Rr, ldr, n, m, v.nbat,
+                                         pair ? feast::BC_PAIR : feast::BC_COPY, sr);
+          if (csl)
+            feast::broadcast_copy_launch(bat(v.Cw + (n + (doR ? m : 0)) * ld, ld, st), Rl, ldrl, n, m, v.nbat,
+                                         feast::BC_CONJ, sr);
+        };
         // a3 (+ forward substitution of a4): P_j [C_j | R] -> [U_j | L_j^-1 P_j R]
-        lu_batched(h, v, solve ? ncr : 0);
+        lu_batched(h, v, solve ? ncr : 0, rest);
         if (doL || h->cache_on)
           feast::perm_launch(v.ipiv, h->perm + (int64_t)b0 * n, h->iperm + (int64_t)b0 * n, n, v.nbat, v.sm);
         // a4: Y_j = U_j^-1 (L_j^-1 P_j R)

@@ -28,9 +28,10 @@ struct Batched {
   int64_t ld, stride;
 };
 
-// C_b = z_b B - A   (B == nullptr: B = I).  z: device array of batch poles.
+// C_b = z_b B - A   (B == nullptr: B = I).  z: device array of batch poles.  Columns [c0, c1)
+// only (c1 < 0: to n).
 void shift_launch(Batched C, const double2* A, int64_t lda, const double2* B, int64_t ldb,
-                  const double2* z, int64_t n, int batch, cudaStream_t s);
+                  const double2* z, int64_t n, int batch, cudaStream_t s, int64_t c0 = 0, int64_t c1 = -1);
 
 // Panel factorisation with partial pivoting of columns [k, k+w) (rows k..n-1) of each matrix.
 // ipiv: batch x n int32 (absolute row index swapped with row k+i), stats: batch x 2 doubles

@@ -27,9 +27,9 @@ Prof& prof() {
 // C_b = z_b B - A  (HBM-bound: reads A (+B), writes C_b).
 __global__ void shift_kernel(Batched C, const double2* __restrict__ A, int64_t lda,
                              const double2* __restrict__ B, int64_t ldb, const double2* __restrict__ z,
-                             int64_t n) {
+                             int64_t n, int64_t c0) {
   const int b = blockIdx.z;
-  const int64_t col = blockIdx.y;
+  const int64_t col = c0 + blockIdx.y;
   const double2 zb = z[b];
   double2* Cc = C.p + b * C.stride + col * C.ld;
   const double2* Ac = A + col * lda;
@@ -43,13 +43,15 @@ __global__ void shift_kernel(Batched C, const double2* __restrict__ A, int64_t l
 }
 
 void shift_launch(Batched C, const double2* A, int64_t lda, const double2* B, int64_t ldb,
-                  const double2* z, int64_t n, int batch, cudaStream_t s) {
-  ProfScope ps_(K_SHIFT, 0.0, (double)batch * n * n * 16.0 * (B ? 3 : 2), s);
+                  const double2* z, int64_t n, int batch, cudaStream_t s, int64_t c0, int64_t c1) {
+  if (c1 < 0) c1 = n;
+  if (c1 <= c0) return;
+  ProfScope ps_(K_SHIFT, 0.0, (double)batch * n * (c1 - c0) * 16.0 * (B ? 3 : 2), s);
   const int threads = 256;
   unsigned gx = (unsigned)((n + threads - 1) / threads);
   if (gx > 8) gx = 8;
-  dim3 grid(gx, (unsigned)n, (unsigned)batch);
-  shift_kernel<<<grid, threads, 0, s>>>(C, A, lda, B, ldb, z, n);
+  dim3 grid(gx, (unsigned)(c1 - c0), (unsigned)batch);
+  shift_kernel<<<grid, threads, 0, s>>>(C, A, lda, B, ldb, z, n, c0);
   count_launch();
 }
 
