@@ -235,8 +235,9 @@ enum { FEAST_K_SHIFT = 0, FEAST_K_PANEL = 1, FEAST_K_LASWP = 2, FEAST_K_TRSM = 3
 int feast_profile(feast_handle h, int32_t enable);
 int feast_profile_summary(feast_handle h, int32_t kclass, int64_t* launches, double* ms, double* flops,
                           double* bytes);
-/* The recorded launches one by one (a timeline; tools/timeline.py): class, stream (0 = the
- * handle's stream, 1 = its lookahead side stream), start / end in ms relative to the first
+/* The recorded launches one by one (a timeline; tools/timeline.py): class, stream (2g = node
+ * group g's main stream, 2g + 1 its lookahead side stream; group 0 = the handle's own stream
+ * pair; -1 other), start / end in ms relative to the first
  * record's start, algorithmic flops.  Host arrays of max_records entries (any may be NULL);
  * *count = number of records.  Synchronises the device. */
 int feast_profile_records(feast_handle h, int64_t max_records, int32_t* kclass, int32_t* stream, double* t0_ms,

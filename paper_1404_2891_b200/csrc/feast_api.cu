@@ -1435,7 +1435,12 @@ int feast_profile_records(feast_handle h, int64_t max_records, int32_t* kclass, 
     CUDA_TRY(h, cudaEventElapsedTime(&e0, recs[0].a, r.a));
     CUDA_TRY(h, cudaEventElapsedTime(&e1, recs[0].a, r.b));
     if (kclass) kclass[i] = r.cls;
-    if (stream) stream[i] = r.s == h->stream ? 0 : (r.s == h->side ? 1 : 2);
+    if (stream) {
+      int tag = r.s == h->stream ? 0 : (r.s == h->side ? 1 : -1);
+      for (int g = 1; g < feast_ctx::GMAX && tag < 0; ++g)
+        if (r.s == h->gs[g]) tag = 2 * g; else if (r.s == h->gside[g]) tag = 2 * g + 1;
+      stream[i] = tag;
+    }
     if (t0_ms) t0_ms[i] = e0;
     if (t1_ms) t1_ms[i] = e1;
     if (flops) flops[i] = r.flops;

@@ -354,6 +354,20 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
         if (r < nrow && !used[s]) {
           double2* colp = P + (c1 - WC) * PLD + r;
           int c = 0;
+          // 8 independent accumulation chains per pass (ILP: one warp per SM sub-partition)
+          for (; c + 8 <= rem; c += 8) {
+            double2 v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = colp[(c + e) * PLD];
+#pragma unroll
+            for (int jj = 0; jj < WC; ++jj)
+              if (jj < wc) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[e] = cfms(v[e], a[s][jj], U12s[jj][c + e]);
+              }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) colp[(c + e) * PLD] = v[e];
+          }
           for (; c + 4 <= rem; c += 4) {
             double2 v0 = colp[(c + 0) * PLD], v1 = colp[(c + 1) * PLD], v2 = colp[(c + 2) * PLD], v3 = colp[(c + 3) * PLD];
 #pragma unroll
