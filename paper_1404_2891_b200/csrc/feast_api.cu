@@ -65,6 +65,7 @@ struct feast_ctx {
   cudaEvent_t ev_a = nullptr, ev_p = nullptr;
   // concurrent node groups (group 0 uses stream / side / ev_a / ev_p)
   static constexpr int GMAX = 4;
+  bool laswp_perm = false;            // FEAST_LASWP=perm: permutation-gather row swaps
   bool prof_serial = false;           // feast_profile(h, 2): one stream, no lookahead / groups
   int groups = 4;                     // concurrent node groups per batch (FEAST_GROUPS)
   bool group_streams = false;
@@ -413,10 +414,10 @@ void factor_block(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, cudaStream_
       const int wpp = (int)std::min<int64_t>(wp, ki + wi - kp);
       panel_at(h, v, kp, wpp, s);
       if (smem) {
-        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, K0 + Wo, nbat, s);
+        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, K0 + Wo, nbat, s, h->laswp_perm);
       } else {   // the register-chunk panel already swapped its own columns
-        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, kp, nbat, s);
-        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, kp + wpp, K0 + Wo, nbat, s);
+        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, kp, nbat, s, h->laswp_perm);
+        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, kp + wpp, K0 + Wo, nbat, s, h->laswp_perm);
       }
       const int64_t cp = kp + wpp, remb = ki + wi - cp;
       if (remb > 0) {
@@ -486,7 +487,7 @@ void lu_batched(feast_ctx* h, const Lu& v, int64_t aug, const std::function<void
     factor_block(h, v, 0, Wo, sm);
   }
   if (v.ev_first) cudaEventRecord(v.ev_first, sm);   // releases the next (staggered) group
-  feast::laswp_launch(bat(C, ld, st), n, 0, (int)Wo, v.ipiv, Wo, ntot, nbat, sm);
+  feast::laswp_launch(bat(C, ld, st), n, 0, (int)Wo, v.ipiv, Wo, ntot, nbat, sm, h->laswp_perm);
   for (int64_t K0 = 0; K0 < n; K0 += Wo, Wo = std::min<int64_t>(NBO, n - K0)) {
     const int64_t K1 = K0 + Wo;
     if (K1 >= n) {
@@ -507,8 +508,8 @@ void lu_batched(feast_ctx* h, const Lu& v, int64_t aug, const std::function<void
       factor_block(h, v, K1, Wo1, sm);
     }
     // block K1's swaps on every column outside it
-    feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, 0, K1, nbat, sm);
-    feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, K1 + Wo1, ntot, nbat, sm);
+    feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, 0, K1, nbat, sm, h->laswp_perm);
+    feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, K1 + Wo1, ntot, nbat, sm, h->laswp_perm);
   }
 }
 
@@ -935,6 +936,7 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   }
   if (const char* e = getenv("FEAST_LOOKAHEAD")) h->lookahead = e[0] != '0';
   if (const char* e = getenv("FEAST_GRAPH")) h->graphs = e[0] != '0';
+  if (const char* e = getenv("FEAST_LASWP")) h->laswp_perm = e[0] == 'p';
   if (const char* e = getenv("FEAST_STAGGER")) h->stagger = e[0] != '0';
   if (const char* e = getenv("FEAST_GROUPS")) {
     const int v = atoi(e);

@@ -42,8 +42,10 @@ void panel_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double*
                   int batch, const PanelCfg& cfg, cudaStream_t s);
 
 // Apply the cnt (<= 1024) sequential swaps ipiv[k..k+cnt) to the columns [c0, c1).
+// use_perm: one composed permutation per CTA, gather + scatter per column (coalesced writes of
+// the rows k..k+cnt-1) instead of the per-column swap chain.
 void laswp_launch(Batched C, int64_t n, int64_t k, int cnt, const int32_t* ipiv, int64_t c0, int64_t c1, int batch,
-                  cudaStream_t s);
+                  cudaStream_t s, bool use_perm = false);
 // Cluster panel with the panel resident in shared memory (rows never moved; see panel_smem.cu).
 bool panel_smem_fits(int64_t n, int w, int cs);
 int panel_smem_max_clusters(int64_t L, int w, int cs);

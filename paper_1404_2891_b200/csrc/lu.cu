@@ -8,6 +8,7 @@
 // across the nodes a rank owns (parallelism over the linear systems).
 #include <cooperative_groups.h>
 #include <float.h>
+#include <cstdlib>
 #include <limits.h>
 
 #include "common.cuh"
@@ -379,13 +380,89 @@ __global__ void laswp_kernel(Batched C, int64_t n, int64_t k, int cnt, const int
   }
 }
 
+// Row swaps as ONE permutation (SURVEY G3 "row-swap kernel with coalesced 16-byte access"):
+// thread 0 of every CTA composes the cnt sequential swaps into the map of the touched rows
+// (positions k..k+cnt-1 and the pivot rows below), using a dense row -> slot table in shared
+// memory; then each warp moves whole columns with one gather and one scatter: lane j reads the
+// source row of touched slot j and writes the destination row, so the writes to the contiguous
+// rows k..k+cnt-1 of a column coalesce, and no swap waits on another (a sequential swap chain
+// is cnt dependent global round trips).
+constexpr int LP_COLS = 1;          // columns per warp (one gather/scatter round trip each)
+constexpr int LP_WARPS = 8;
+__global__ void __launch_bounds__(32 * LP_WARPS) laswp_perm_kernel(Batched C, int64_t n, int64_t k, int cnt,
+                                                                    const int32_t* __restrict__ ipiv_all,
+                                                                    int64_t c0, int64_t c1) {
+  extern __shared__ int32_t lsm[];
+  const int L = (int)(n - k);
+  int32_t* slot_of = lsm;                 // [L]: slot of relative row r, -1 if untouched
+  int32_t* row_at = lsm + L;              // [2 cnt]: relative row of slot t (destination)
+  int32_t* src_of = row_at + 2 * cnt;     // [2 cnt]: relative source row whose value ends in slot t
+  __shared__ int nt_s;
+  const int b = blockIdx.y;
+  const int32_t* ipiv = ipiv_all + (int64_t)b * n + k;
+  for (int r = threadIdx.x; r < L; r += blockDim.x) slot_of[r] = r < cnt ? r : -1;
+  for (int t = threadIdx.x; t < cnt; t += blockDim.x) { row_at[t] = t; src_of[t] = t; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int nt = cnt;
+    for (int i = 0; i < cnt; ++i) {
+      const int p = ipiv[i] - (int)k;   // >= i (partial pivoting picks from rows i..)
+      if (p == i) continue;
+      int sp = slot_of[p];
+      if (sp < 0) { sp = nt++; slot_of[p] = sp; row_at[sp] = p; src_of[sp] = p; }
+      const int tmp = src_of[i];
+      src_of[i] = src_of[sp];
+      src_of[sp] = tmp;
+    }
+    nt_s = nt;
+  }
+  __syncthreads();
+  const int nt = nt_s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* base = C.p + (int64_t)b * C.stride + k;
+  for (int q = 0; q < LP_COLS; ++q) {
+    const int64_t col = c0 + ((int64_t)blockIdx.x * LP_WARPS + warp) * LP_COLS + q;
+    if (col >= c1) break;
+    double2* Cc = base + col * C.ld;
+    // gather every touched slot's new value first, then scatter (a bijection on the slots)
+    double2 v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int t = lane + 32 * u;
+      if (t < nt) v[u] = Cc[src_of[t]];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int t = lane + 32 * u;
+      if (t < nt) Cc[row_at[t]] = v[u];
+    }
+  }
+}
+
 void laswp_launch(Batched C, int64_t n, int64_t k, int cnt, const int32_t* ipiv, int64_t c0, int64_t c1, int batch,
-                  cudaStream_t s) {
+                  cudaStream_t s, bool use_perm) {
   if (c1 <= c0 || cnt <= 0) return;
   ProfScope ps_(K_LASWP, 0.0, (double)batch * (c1 - c0) * cnt * 64.0, s);
-  const int threads = 128;
-  dim3 grid((unsigned)((c1 - c0 + threads - 1) / threads), (unsigned)batch);
-  laswp_kernel<<<grid, threads, 0, s>>>(C, n, k, cnt, ipiv, c0, c1);
+  const int64_t L = n - k;
+  const size_t smem = (size_t)(L + 4 * cnt) * sizeof(int32_t);
+  // Default: the per-column swap chain.  Measured on B200 (C2 project 17.9 vs 18.9 ms, C3 1710 vs
+  // 1730 ms) the permutation kernel loses in the overlapped schedule: its many CTAs and row tables
+  // compete with the trailing-update GEMMs more than the short chain kernel does.
+  if (use_perm && 2 * cnt <= 32 * 16 && smem <= 96 * 1024) {
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(laswp_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      configured = true;
+    }
+    const int64_t per_cta = (int64_t)LP_WARPS * LP_COLS;
+    dim3 grid((unsigned)((c1 - c0 + per_cta - 1) / per_cta), (unsigned)batch);
+    laswp_perm_kernel<<<grid, 32 * LP_WARPS, smem, s>>>(C, n, k, cnt, ipiv, c0, c1);
+  } else {   // very tall trailing matrices (row table > 96 KB) or > 256 swaps: the swap chain per column
+    const int threads = 128;
+    dim3 grid((unsigned)((c1 - c0 + threads - 1) / threads), (unsigned)batch);
+    laswp_kernel<<<grid, threads, 0, s>>>(C, n, k, cnt, ipiv, c0, c1);
+  }
   count_launch();
 }
 

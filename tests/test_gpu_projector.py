@@ -369,3 +369,14 @@ def test_row_sharded_rhs_partials():
         assert np.all(part[:r0] == 0) and np.all(part[r1:] == 0)
         total = total + part
     assert rel(total, P.B @ P.X0) <= 1e-13
+
+
+def test_permutation_laswp_variant(monkeypatch):
+    """The permutation-gather row-swap kernel (FEAST_LASWP=perm, coalesced writes of the panel
+    rows) gives the same projector as the default per-column swap chain."""
+    monkeypatch.setenv("FEAST_LASWP", "perm")
+    P = synth.make_pencil("C2", n=300, m0=20)
+    z, w = _oracle_nodes(P)
+    f = _handle(P)
+    Q = host(f.project(dev(P.A), dev(P.B), dev(P.X0)))
+    assert rel(Q, oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
