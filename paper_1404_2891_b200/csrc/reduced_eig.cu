@@ -1,0 +1,299 @@
+// reduced_eig.cu — the m0 x m0 reduced eigenproblem of a FEAST iteration on one CTA (SURVEY §8(a)
+// "outside the timed path": R-FEAST step 5; Bi-FEAST step 7), for
+// m0 <= RE_MAXM.  cuSOLVER's Xgeev (a hybrid host/device solver) takes ~25 ms at m0 = 128 on
+// B200 — longer than the projector of C2 — so small reduced problems are solved here:
+//
+//   1. Householder reduction to upper Hessenberg form, in global memory (L2-resident):
+//      H = P^H M P, P = P_1 ... P_{m-2}, P_j = I - 2 u u^H (||u|| = 1); Z = P.
+//   2. Complex single-shift QR iteration (Wilkinson shift, exceptional shifts every 10
+//      iterations, deflation |h_{l,l-1}| <= eps (|h_ll| + |h_{l-1,l-1}|)) on the Hessenberg
+//      matrix held PACKED in shared memory (column j keeps rows 0..j+1: ~m^2/2 entries), the
+//      bulge as a separate scalar; Givens rotations (zlartg convention) applied to whole rows /
+//      columns (wantt: the full Schur form T = Z^H M Z), recorded per sweep and applied to Z in
+//      global memory after the sweep (one thread per row of Z, coalesced column accesses).
+//   3. Eigenvectors of T by back-substitution (one thread per eigenvector):
+//      y_i = e_i, y_j = -(sum_{l=j+1..i} t_jl y_l) / (t_jj - t_ii), j < i.
+//   The caller forms W = Z Y (a DMMA ZGEMM).  info = 0, or 1 if the QR iteration did not
+//   converge within 30 m sweeps (the caller then falls back to cuSOLVER).
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "prof.h"
+
+namespace feast {
+namespace {
+
+constexpr int RE_T = 256;   // threads
+
+__device__ double block_sum_re(double v, double* red) {
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < RE_T / 32; ++i) s += red[i];
+  return s;
+}
+
+__device__ __forceinline__ double cabs2d(double2 a) { return hypot(a.x, a.y); }
+
+// packed Hessenberg: column j holds rows 0 .. min(j+1, m-1)
+__host__ __device__ __forceinline__ int poff(int j, int m) {
+  // sum_{l<j} min(l+2, m): for l <= m-2 the length is l+2
+  const int jj = min(j, m - 1);
+  int o = jj * (jj + 3) / 2;            // sum_{l<jj} (l + 2)
+  if (j > m - 1) o += (j - (m - 1)) * m;
+  return o;
+}
+
+__global__ void __launch_bounds__(RE_T) reduced_eig_kernel(double2* __restrict__ H, int m, int64_t ldh,
+                                                           double2* __restrict__ Z, int64_t ldz,
+                                                           double2* __restrict__ lam, double2* __restrict__ Y,
+                                                           int64_t ldy, int32_t* __restrict__ info) {
+  extern __shared__ __align__(16) double2 S[];   // packed Hessenberg / Schur form
+  __shared__ double red[RE_T / 32];
+  __shared__ double2 rot_c[RE_MAXM], rot_s[RE_MAXM];   // c (real, in .x) and s per sweep step
+  __shared__ double2 u_s[RE_MAXM], w_s[RE_MAXM];
+  __shared__ int lo_s, conv_s;
+  __shared__ double2 bulge_s, x_s, y_s;
+  const int tid = threadIdx.x;
+
+  // ---- 1. Householder Hessenberg reduction in global memory; Z = I then Z <- Z P_j
+  for (int idx = tid; idx < m * m; idx += RE_T) {
+    const int i = idx % m, j = idx / m;
+    Z[i + j * ldz] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  for (int j = 0; j + 2 < m; ++j) {
+    const int len = m - j - 1;   // x = H[j+1 : m, j]
+    double part = 0.0;
+    for (int i = tid; i < len; i += RE_T) {
+      const double2 v = H[(j + 1 + i) + j * ldh];
+      part += v.x * v.x + v.y * v.y;
+    }
+    const double xn2 = block_sum_re(part, red);
+    const double2 x0 = H[(j + 1) + j * ldh];
+    const double xn = sqrt(xn2), ax0 = cabs2d(x0);
+    if (xn == 0.0 || xn2 - ax0 * ax0 <= 1e-300 * xn2) { __syncthreads(); continue; }   // already reduced
+    // alpha = -e^{i arg x0} ||x||;  u = (x - alpha e1) / ||x - alpha e1||
+    const double2 ph = ax0 > 0 ? make_double2(x0.x / ax0, x0.y / ax0) : make_double2(1.0, 0.0);
+    const double2 alpha = make_double2(-ph.x * xn, -ph.y * xn);
+    const double2 u0 = make_double2(x0.x - alpha.x, x0.y - alpha.y);
+    const double un = sqrt(xn2 - ax0 * ax0 + u0.x * u0.x + u0.y * u0.y);
+    for (int i = tid; i < len; i += RE_T) {
+      const double2 v = i == 0 ? u0 : H[(j + 1 + i) + j * ldh];
+      u_s[i] = make_double2(v.x / un, v.y / un);
+    }
+    __syncthreads();
+    // left: rows j+1.., columns j..m-1:  H <- H - 2 u (u^H H); w = u^H H by one warp per column
+    // (lanes over rows: coalesced column reads, shuffle reduction)
+    {
+      const int warp = tid >> 5, lane = tid & 31;
+      for (int c = j + warp; c < m; c += RE_T / 32) {
+        double sx = 0.0, sy = 0.0;
+        for (int i = lane; i < len; i += 32) {
+          const double2 uh = cconj(u_s[i]), hv = H[(j + 1 + i) + c * ldh];
+          sx += uh.x * hv.x - uh.y * hv.y;
+          sy += uh.x * hv.y + uh.y * hv.x;
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+          sx += __shfl_xor_sync(0xffffffffu, sx, off);
+          sy += __shfl_xor_sync(0xffffffffu, sy, off);
+        }
+        if (lane == 0) w_s[c - j] = make_double2(sx, sy);
+      }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < len * (m - j); idx += RE_T) {
+      const int i = idx % len, c = j + idx / len;
+      const double2 t = cmul(u_s[i], w_s[c - j]);
+      double2* hp = H + (j + 1 + i) + c * ldh;
+      *hp = make_double2(hp->x - 2.0 * t.x, hp->y - 2.0 * t.y);
+    }
+    __syncthreads();
+    // right: all rows, columns j+1..:  H <- H - 2 (H u) u^H ;  same for Z
+    for (int pass = 0; pass < 2; ++pass) {
+      double2* A = pass ? Z : H;
+      const int64_t lda = pass ? ldz : ldh;
+      for (int r = tid; r < m; r += RE_T) {   // consecutive rows per thread: coalesced
+        double2 s0 = make_double2(0.0, 0.0), s1 = s0, s2 = s0, s3 = s0;
+        int i = 0;
+        for (; i + 4 <= len; i += 4) {        // four independent chains, loads in flight
+          s0 = cadd(s0, cmul(A[r + (j + 1 + i) * lda], u_s[i]));
+          s1 = cadd(s1, cmul(A[r + (j + 2 + i) * lda], u_s[i + 1]));
+          s2 = cadd(s2, cmul(A[r + (j + 3 + i) * lda], u_s[i + 2]));
+          s3 = cadd(s3, cmul(A[r + (j + 4 + i) * lda], u_s[i + 3]));
+        }
+        for (; i < len; ++i) s0 = cadd(s0, cmul(A[r + (j + 1 + i) * lda], u_s[i]));
+        w_s[r] = cadd(cadd(s0, s1), cadd(s2, s3));
+      }
+      __syncthreads();
+      for (int idx = tid; idx < m * len; idx += RE_T) {
+        const int r = idx % m, i = idx / m;
+        const double2 t = cmul(w_s[r], cconj(u_s[i]));
+        double2* ap = A + r + (j + 1 + i) * lda;
+        *ap = make_double2(ap->x - 2.0 * t.x, ap->y - 2.0 * t.y);
+      }
+      __syncthreads();
+    }
+  }
+  // ---- 2. packed copy into shared memory (entries below the subdiagonal are zero)
+  for (int j = 0; j < m; ++j)
+    for (int i = tid; i <= min(j + 1, m - 1); i += RE_T) S[poff(j, m) + i] = H[i + j * ldh];
+  __syncthreads();
+  auto at = [&](int i, int j) -> double2& { return S[poff(j, m) + i]; };
+
+  const double eps = DBL_EPSILON;
+  int hi = m - 1, its = 0, total = 0;
+  const int maxit = 30 * m;
+  while (hi > 0) {
+    // deflation scan (thread 0): lo = largest l in (0, hi] with negligible h_{l,l-1}
+    if (tid == 0) {
+      int l = hi;
+      for (; l > 0; --l) {
+        const double2 sub = at(l, l - 1);
+        const double tst = cabs1(at(l, l)) + cabs1(at(l - 1, l - 1));
+        if (cabs1(sub) <= eps * tst) { at(l, l - 1) = make_double2(0.0, 0.0); break; }
+      }
+      lo_s = l;
+    }
+    __syncthreads();
+    const int lo = lo_s;
+    if (lo == hi) { --hi; its = 0; __syncthreads(); continue; }
+    if (++total > maxit) break;
+    ++its;
+    // shift (thread 0): Wilkinson (eigenvalue of the trailing 2x2 closest to h_hh), or an
+    // exceptional shift every 10 iterations without deflation
+    if (tid == 0) {
+      double2 mu;
+      const double2 a = at(hi - 1, hi - 1), b = at(hi - 1, hi), c = at(hi, hi - 1), d = at(hi, hi);
+      if (its % 10 == 0) {
+        const double e = cabs1(c) + (hi - 2 >= lo ? cabs1(at(hi - 1, hi - 2)) : 0.0);
+        mu = make_double2(d.x + 0.75 * e, d.y);
+      } else {
+        // eigenvalues of [[a, b], [c, d]]: tr/2 +- sqrt((a - d)^2/4 + b c)
+        const double2 hf = make_double2(0.5 * (a.x - d.x), 0.5 * (a.y - d.y));
+        const double2 disc = cadd(cmul(hf, hf), cmul(b, c));
+        // principal complex square root of disc
+        const double r = cabs2d(disc);
+        const double t = sqrt(0.5 * (r + fabs(disc.x)));
+        double2 sq = make_double2(0.0, 0.0);
+        if (t > 0.0)
+          sq = disc.x >= 0.0 ? make_double2(t, disc.y / (2.0 * t)) : make_double2(fabs(disc.y) / (2.0 * t), copysign(t, disc.y));
+        const double2 mid = make_double2(0.5 * (a.x + d.x), 0.5 * (a.y + d.y));
+        const double2 l1 = cadd(mid, sq), l2 = csub(mid, sq);
+        mu = cabs1(csub(l1, d)) <= cabs1(csub(l2, d)) ? l1 : l2;
+      }
+      x_s = csub(at(lo, lo), mu);
+      y_s = at(lo + 1, lo);
+      bulge_s = make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    for (int k = lo; k < hi; ++k) {
+      // rotation G = [[c, s], [-conj(s), c]] with G [x; y] = [r; 0]  (zlartg convention)
+      if (tid == 0) {
+        const double2 f = x_s, g = y_s;
+        const double af = cabs2d(f), ag = cabs2d(g);
+        double c;
+        double2 s;
+        if (ag == 0.0) { c = 1.0; s = make_double2(0.0, 0.0); }
+        else if (af == 0.0) { c = 0.0; s = make_double2(g.x / ag, -g.y / ag); }
+        else {
+          const double nrm = hypot(af, ag);
+          c = af / nrm;
+          const double2 fs = make_double2(f.x / af, f.y / af);
+          s = make_double2((fs.x * g.x + fs.y * g.y) / nrm, (fs.y * g.x - fs.x * g.y) / nrm);   // fs conj(g) / nrm
+        }
+        rot_c[k] = make_double2(c, 0.0);
+        rot_s[k] = s;
+      }
+      __syncthreads();
+      const double c = rot_c[k].x;
+      const double2 s = rot_s[k];
+      // rows k, k+1, columns (k-1 or lo) .. m-1: [hk; hk1] <- [c hk + s hk1; -conj(s) hk + c hk1]
+      const int c0 = k > lo ? k - 1 : lo;
+      for (int col = c0 + tid; col < m; col += RE_T) {
+        double2 hk = at(k, col);
+        double2 hk1 = (k + 1 <= col + 1) ? at(k + 1, col) : bulge_s;   // (k+1, k-1) is the bulge
+        const double2 nk = cadd(make_double2(c * hk.x, c * hk.y), cmul(s, hk1));
+        const double2 nk1 = csub(make_double2(c * hk1.x, c * hk1.y), cmul(cconj(s), hk));
+        at(k, col) = nk;
+        if (k + 1 <= col + 1) at(k + 1, col) = nk1;   // the bulge entry becomes 0 (annihilated)
+      }
+      __syncthreads();
+      // columns k, k+1, rows 0 .. min(k+2, hi): [hik, hik1] <- [c hik + conj(s) hik1, -s hik + c hik1]
+      const int r1 = min(k + 2, hi);
+      for (int row = tid; row <= r1; row += RE_T) {
+        // (k+2, k) is below the Hessenberg profile: zero before this rotation, the new bulge after
+        const double2 hik = (row <= k + 1) ? at(row, k) : make_double2(0.0, 0.0);
+        const double2 hik1 = at(row, k + 1);
+        const double2 nk = cadd(make_double2(c * hik.x, c * hik.y), cmul(cconj(s), hik1));
+        const double2 nk1 = csub(make_double2(c * hik1.x, c * hik1.y), cmul(s, hik));
+        if (row <= k + 1) at(row, k) = nk;
+        at(row, k + 1) = nk1;
+        if (row == k + 2) bulge_s = nk;   // new bulge at (k+2, k)
+      }
+      __syncthreads();
+      if (tid == 0 && k + 1 < hi) { x_s = at(k + 1, k); y_s = bulge_s; }
+      __syncthreads();
+    }
+    // Z <- Z G_k^H for k = lo..hi-1 (one thread per row of Z)
+    for (int row = tid; row < m; row += RE_T) {
+      double2 zk = Z[row + (int64_t)lo * ldz];
+      for (int k = lo; k < hi; ++k) {
+        const double c = rot_c[k].x;
+        const double2 s = rot_s[k];
+        const double2 zk1 = Z[row + (int64_t)(k + 1) * ldz];
+        const double2 nk = cadd(make_double2(c * zk.x, c * zk.y), cmul(cconj(s), zk1));
+        const double2 nk1 = csub(make_double2(c * zk1.x, c * zk1.y), cmul(s, zk));
+        Z[row + (int64_t)k * ldz] = nk;
+        zk = nk1;
+      }
+      Z[row + (int64_t)hi * ldz] = zk;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) conv_s = hi <= 0 ? 1 : 0;
+  __syncthreads();
+  if (!conv_s) {
+    if (tid == 0) info[0] = 1;
+    return;
+  }
+  // ---- 3. eigenvalues and eigenvectors of T (upper triangular part of S)
+  for (int i = tid; i < m; i += RE_T) lam[i] = at(i, i);
+  const double smlnum = DBL_MIN * (double)m / eps;
+  for (int i = tid; i < m; i += RE_T) {
+    const double2 ti = at(i, i);
+    double2* y = Y + (int64_t)i * ldy;
+    for (int j = i + 1; j < m; ++j) y[j] = make_double2(0.0, 0.0);
+    y[i] = make_double2(1.0, 0.0);
+    for (int j = i - 1; j >= 0; --j) {
+      double2 sacc = make_double2(0.0, 0.0);
+      for (int l = j + 1; l <= i; ++l) sacc = cadd(sacc, cmul(at(j, l), y[l]));
+      double2 den = csub(at(j, j), ti);
+      if (cabs1(den) < smlnum) den = make_double2(smlnum, 0.0);
+      y[j] = cdiv(make_double2(-sacc.x, -sacc.y), den);
+    }
+  }
+  if (tid == 0) info[0] = 0;
+}
+
+}  // namespace
+
+bool reduced_eig_launch(double2* H, int m, int64_t ldh, double2* Z, int64_t ldz, double2* lam, double2* Y, int64_t ldy,
+                        int32_t* info, cudaStream_t s) {
+  if (m < 1 || m > RE_MAXM) return false;
+  ProfScope ps_(K_OTHER, 0.0, 0.0, s);
+  const size_t smem = (size_t)poff(m, m) * sizeof(double2);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(reduced_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    configured = true;
+  }
+  reduced_eig_kernel<<<1, RE_T, smem, s>>>(H, m, ldh, Z, ldz, lam, Y, ldy, info);
+  count_launch();
+  return true;
+}
+
+}  // namespace feast
