@@ -196,7 +196,7 @@ int feast_estimate_count(feast_handle h, const void* A, int64_t lda, const void*
  * FEAST_E_ARG for m > 160 or bad arguments, FEAST_E_REDUCED if the QR iteration does not
  * converge (30 m sweeps; feast_iterate then falls back to cuSOLVER Xgeev).  Synchronises.
  * Device-resident (no host round trips), but measured slower than cuSOLVER Xgeev on B200
- * (m = 64 / 128 / 160: 8.8 / 38.6 / 63 ms vs 5.8 / 25 / - ms): the default stays cuSOLVER. */
+ * (m = 64 / 128 / 160: 5.6 / 28 / 49 ms vs 5.8 / 26 / - ms): the default stays cuSOLVER. */
 int feast_small_eig(int64_t m, const void* M, int64_t ldm, void* lam, void* W, int64_t ldw, void* work,
                     size_t work_bytes, void* cuda_stream);
 
