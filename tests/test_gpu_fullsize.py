@@ -67,3 +67,30 @@ def test_c5_full_spectral():
     Q = f.project(P.A, P.B, P.X0)
     Qs = P.V @ (_rho(P)[:, None] * torch.linalg.solve(P.V, P.X0))
     assert _rel(Q, Qs) <= TOL
+
+
+def test_c4_full_bifeast_converged_pairs_match_truth():
+    """Parity protocol P3 at full C4 size (n = 16384, m0 = 512, 32 poles, Bi-FEAST, 5 iterations):
+    every converged pair inside the contour (residual <= 1e-10) is a true eigenvalue (known by
+    construction) to 1e-10 x R, one-to-one; and (P4) the converged inside pairs are all of them."""
+    import numpy as np
+    P = synth.make_pencil_torch("C4")
+    s = P.spec
+    f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.BI, True)
+    X = P.X0.clone()
+    G = X.conj().T @ X
+    V = torch.linalg.solve(G, X.conj().T).conj().T.contiguous().t().contiguous().t()   # X0 G^-H (R6)
+    for _ in range(s.iters):
+        out = f.iterate(P.A, None, X, V)
+    lam = np.asarray(out["lam"])
+    ok = (np.asarray(out["flags"]) & 1).astype(bool) & (np.asarray(out["resid"]) <= 1e-10)
+    true = P.lam.cpu().numpy()
+    inside = true[np.abs(true - s.c) < s.r]
+    got = lam[ok]
+    assert len(got) == len(inside) > 0, (len(got), len(inside))
+    rem = list(inside)
+    for l in got:
+        d = np.abs(np.asarray(rem) - l)
+        i = int(np.argmin(d))
+        assert d[i] <= 1e-10 * s.r, (l, rem[i])
+        rem.pop(i)

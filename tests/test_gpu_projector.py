@@ -380,3 +380,35 @@ def test_permutation_laswp_variant(monkeypatch):
     f = _handle(P)
     Q = host(f.project(dev(P.A), dev(P.B), dev(P.X0)))
     assert rel(Q, oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
+
+
+@pytest.mark.parametrize("key,n,m0", [("C2", 220, 24), ("C4", 200, 30)])
+def test_projector_parity_at_later_iterations(key, n, m0):
+    """Parity protocol P1 at k > 1: the GPU projector applied to the ORACLE's
+    iterate X^(k-1) (after two oracle R-FEAST iterations) matches the oracle's projector."""
+    P = synth.make_pencil(key, n=n, m0=m0)
+    s = P.spec
+    z, w = _oracle_nodes(P)
+    X = P.X0
+    for _ in range(2):
+        X = oracle.feast_iterate(P.A, P.B, X, None, z, w, s.c, s.r, s.aspect)["X"]
+    f = _handle(P)
+    Q = host(f.project(dev(P.A), dev(P.B), dev(X)))
+    assert rel(Q, oracle.project(P.A, P.B, X, z, w)) <= TOL
+
+
+def test_worst_pivot_node_solution():
+    """Parity protocol P2: the per-node solve Y_j = (z_j B - A)^-1 B X of the node with the
+    smallest pivot ratio (feast_node_stats), isolated as a one-node virtual rank (its partial is
+    w_j Y_j), matches the oracle's naive-LU solve of that node."""
+    P = synth.make_pencil("C2", n=240, m0=12)
+    z, w = _oracle_nodes(P)
+    f = _handle(P)
+    f.project(dev(P.A), dev(P.B), dev(P.X0))
+    stats, worst = f.node_stats()
+    assert worst == int(np.argmin(stats))
+    g = _handle(P, rank=worst, world=P.q)                       # owns exactly node `worst`
+    part = host(g.project(dev(P.A), dev(P.B), dev(P.X0), allreduce=False))
+    Yj = part / w[worst]
+    Yo = oracle.project(P.A, P.B, P.X0, z, np.ones_like(w), worst, worst + 1)
+    assert rel(Yj, Yo) <= TOL
