@@ -412,3 +412,26 @@ def test_worst_pivot_node_solution():
     Yj = part / w[worst]
     Yo = oracle.project(P.A, P.B, P.X0, z, np.ones_like(w), worst, worst + 1)
     assert rel(Yj, Yo) <= TOL
+
+
+@pytest.mark.parametrize("n,m0", [(257, 9), (513, 17), (1000, 31), (2049, 8)])
+def test_ragged_sizes_across_panel_paths(n, m0):
+    """Heights around the panel-kernel boundaries: 1 -> 2 -> 4 -> 8 -> 16 CTAs per cluster as
+    L = n - k falls (256 rows per CTA), ragged last blocks; oracle parity."""
+    P = synth.make_pencil("C2", n=n, m0=m0)
+    z, w = _oracle_nodes(P)
+    f = _handle(P)
+    Q = host(f.project(dev(P.A), dev(P.B), dev(P.X0)))
+    assert rel(Q, oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
+
+
+def test_register_panel_height_spectral():
+    """n = 4200 > 16 x 256: the first panels take the register-chunk kernel, later ones the
+    shared-memory cluster kernel; checked with the spectral identity (closed-form filter)."""
+    P = synth.make_pencil_torch("C2", n=4200, m0=16)
+    s = P.spec
+    f = _handle(P)
+    Q = f.project(P.A, P.B, P.X0)
+    rho = 1.0 / (1.0 + ((P.lam - s.c) / s.r) ** P.q)
+    Qs = P.V @ (rho[:, None] * torch.linalg.solve(P.V, P.X0))
+    assert float(torch.linalg.norm(Q - Qs) / torch.linalg.norm(Qs)) <= TOL
