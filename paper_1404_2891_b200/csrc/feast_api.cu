@@ -61,6 +61,7 @@ struct feast_ctx {
   const void *cache_A = nullptr, *cache_B = nullptr;
   int64_t nbo = 256;                  // outer block (trailing-update K); multiple of 64
   int64_t wp = 32;                    // cluster-panel width (divides 64)
+  int64_t wide_panel_rows = 768;      // 64-wide cluster panels once n - k <= this (FEAST_WIDE_ROWS)
   cudaStream_t side = nullptr;        // high-priority stream for the lookahead panel
   cudaEvent_t ev_a = nullptr, ev_p = nullptr;
   // concurrent node groups (group 0 uses stream / side / ev_a / ev_p)
@@ -409,7 +410,9 @@ void factor_block(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, cudaStream_
   for (int64_t ki = K0; ki < K0 + Wo; ki += 64) {
     const int wi = (int)std::min<int64_t>(64, K0 + Wo - ki);
     const bool smem = smem_panel_for(h, ki);
-    const int64_t wp = smem ? h->wp : 64;
+    // once the panel is short (L <= wide_panel_rows: clusters of <= 8 CTAs x 128 rows), a 64-wide
+    // block is one cluster panel: no in-block trsm / update / second swap launch on the chain
+    const int64_t wp = !smem ? 64 : ((h->n - ki <= h->wide_panel_rows) ? 64 : h->wp);
     // the 64-block is factored as narrow cluster panels of wp columns (small SM footprint), with
     // the in-block U12 (warp TRSM) and update (DMMA) between them
     for (int64_t kp = ki; kp < ki + wi; kp += wp) {
@@ -941,6 +944,7 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   if (const char* e = getenv("FEAST_LASWP")) h->laswp_perm = e[0] == 'p';
   if (const char* e = getenv("FEAST_EIG")) h->own_eig = e[0] == 'o';
   if (const char* e = getenv("FEAST_STAGGER")) h->stagger = e[0] != '0';
+  if (const char* e = getenv("FEAST_WIDE_ROWS")) h->wide_panel_rows = atol(e);
   if (const char* e = getenv("FEAST_GROUPS")) {
     const int v = atoi(e);
     if (v >= 1 && v <= feast_ctx::GMAX) h->groups = v;

@@ -489,7 +489,10 @@ void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, do
   // Shrink the cluster as the panel gets shorter (L = n - k): the smallest cluster that keeps
   // <= 2*PT rows per CTA.  Fewer CTAs per column exchange (cs = 1: no DSMEM at all) and fewer SMs
   // held while the latency-bound panel runs next to the trailing-update GEMMs.
-  while (cs > 1 && (n - k + cs / 2 - 1) / (cs / 2) <= 2 * PT) cs /= 2;
+  // rows per CTA: <= 2 PT (two per thread) for panels up to 32 wide; <= PT for wider ones so the
+  // w - 8 shared-memory columns stay within ~112 KB
+  const int rowcap = w > 32 ? PT : 2 * PT;
+  while (cs > 1 && (n - k + cs / 2 - 1) / (cs / 2) <= rowcap) cs /= 2;
   const int64_t Lc = (n - k + cs - 1) / cs;
   // register chunk: 8 columns (a 16-column chunk spills at 2 rows per thread)
   if (Lc <= PT) launch_s<1, 8>(C, n, k, w, ipiv, stats, info, batch, cs, s);
