@@ -76,6 +76,8 @@ struct feast_ctx {
   cudaEvent_t gev_a[GMAX] = {}, gev_p[GMAX] = {}, gev_done[GMAX] = {};
   cudaEvent_t ev_fork = nullptr;
   cudaEvent_t gev_first[GMAX] = {};
+  cudaStream_t gx[GMAX] = {};         // per group: the stream of the diagonal-block inverses
+  cudaEvent_t gev_t[GMAX] = {}, gev_x[GMAX] = {};
   bool stagger = false;  // true: group g starts once group g-1 has factored its first block
   int64_t ldc = 0;
   // workspace
@@ -337,6 +339,8 @@ struct Lu {
   cudaStream_t sm, sp;  // main / high-priority lookahead stream
   cudaEvent_t ev_a, ev_p;
   cudaEvent_t ev_first;  // recorded after the first block is factored (nullptr: none)
+  cudaStream_t sx;       // diagonal-block inverses off the panel chain (nullptr: on the chain)
+  cudaEvent_t ev_t, ev_x;
 };
 const double2* inv_ptr(const Lu& v, int64_t kb, int which) { return v.Inv + (kb * 2 + which) * 4096; }
 
@@ -433,16 +437,28 @@ void factor_block(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, cudaStream_
         feast::zgemm_launch(p, false, feast::ZG_SUB, s);
       }
     }
-    feast::trtri_launch(bat(C, ld, st), n, ki / 64, 1, v.Inv, h->inv_stride, 2, nbat, s);
+    // the 64x64 inverses (needed by the outer U12 and the substitutions, not by this block's
+    // chain) run on their own stream, joined at the end of the block
     const int64_t c1 = ki + wi, rem = K0 + Wo - c1;
+    cudaStream_t st_inv = s;
+    if (v.sx) {
+      cudaEventRecord(v.ev_t, s);
+      cudaStreamWaitEvent(v.sx, v.ev_t, 0);
+      st_inv = v.sx;
+    }
+    feast::trtri_launch(bat(C, ld, st), n, ki / 64, 1, v.Inv, h->inv_stride, 2, nbat, st_inv);
     if (rem > 0) {
-      ZgemmArgs u{wi, rem, wi, inv_ptr(v, ki / 64, 0), 64, h->inv_stride, C + ki + c1 * ld, ld, st, C + ki + c1 * ld,
-                  ld, st, make_double2(1, 0), make_double2(0, 0), nbat, 1};
-      feast::zgemm_launch(u, false, feast::ZG_GEN, s);
+      // in-block U12 = L11^-1 A12 (warp TRSM on the chain), then A22 -= L21 U12 (DMMA)
+      feast::trsm_launch(bat(C + ki + ki * ld, ld, st), bat(C + ki + c1 * ld, ld, st), wi, rem, true, true, false,
+                         nbat, s);
       ZgemmArgs p{n - c1, rem, wi, C + c1 + ki * ld, ld, st, C + ki + c1 * ld, ld, st, C + c1 + c1 * ld, ld, st,
                   make_double2(-1, 0), make_double2(1, 0), nbat};
       feast::zgemm_launch(p, false, feast::ZG_SUB, s);
     }
+  }
+  if (v.sx) {   // the block's inverses complete before anything downstream of this stream
+    cudaEventRecord(v.ev_x, v.sx);
+    cudaStreamWaitEvent(s, v.ev_x, 0);
   }
 }
 
@@ -641,7 +657,8 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
       const int b0 = g * nbat / G, b1 = (g + 1) * nbat / G;
       Lu v{h->Cw + b0 * st, h->Inv + b0 * h->inv_stride, h->ipiv + (int64_t)b0 * n, h->stats + 2 * (j + b0),
            h->info + (j + b0), b1 - b0, g ? h->gs[g] : h->stream, g ? h->gside[g] : h->side, g ? h->gev_a[g] : h->ev_a,
-           g ? h->gev_p[g] : h->ev_p, (h->stagger && g + 1 < G) ? h->gev_first[g] : nullptr};
+           g ? h->gev_p[g] : h->ev_p, (h->stagger && g + 1 < G) ? h->gev_first[g] : nullptr,
+           h->prof_serial ? nullptr : h->gx[g], h->gev_t[g], h->gev_x[g]};
       if (g) cudaStreamWaitEvent(v.sm, (h->stagger && g > 0) ? h->gev_first[g - 1] : h->ev_fork, 0);
       if (!reuse) {
         feast::stats_init_launch(v.stats, v.info, v.nbat, v.sm);
@@ -973,7 +990,10 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
              cudaEventCreateWithFlags(&h->gev_p[g], cudaEventDisableTiming) == cudaSuccess &&
              cudaEventCreateWithFlags(&h->gev_done[g], cudaEventDisableTiming) == cudaSuccess;
       for (int g = 0; g < feast_ctx::GMAX && ok; ++g)
-        ok = cudaEventCreateWithFlags(&h->gev_first[g], cudaEventDisableTiming) == cudaSuccess;
+        ok = cudaEventCreateWithFlags(&h->gev_first[g], cudaEventDisableTiming) == cudaSuccess &&
+             cudaStreamCreateWithFlags(&h->gx[g], cudaStreamNonBlocking) == cudaSuccess &&
+             cudaEventCreateWithFlags(&h->gev_t[g], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&h->gev_x[g], cudaEventDisableTiming) == cudaSuccess;
       if (!ok) { cudaGetLastError(); h->groups = 1; h->group_streams = false; }
       else h->group_streams = true;
     } else {
@@ -1511,8 +1531,12 @@ void feast_destroy(feast_handle h) {
     if (h->gev_done[g]) cudaEventDestroy(h->gev_done[g]);
   }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
-  for (int g = 0; g < feast_ctx::GMAX; ++g)
+  for (int g = 0; g < feast_ctx::GMAX; ++g) {
     if (h->gev_first[g]) cudaEventDestroy(h->gev_first[g]);
+    if (h->gx[g]) cudaStreamDestroy(h->gx[g]);
+    if (h->gev_t[g]) cudaEventDestroy(h->gev_t[g]);
+    if (h->gev_x[g]) cudaEventDestroy(h->gev_x[g]);
+  }
   if (h->own_stream) {
     cudaStreamSynchronize(h->stream);
     cudaStreamDestroy(h->stream);
