@@ -75,6 +75,8 @@ struct feast_ctx {
   cudaStream_t gs[GMAX] = {}, gside[GMAX] = {};
   cudaEvent_t gev_a[GMAX] = {}, gev_p[GMAX] = {}, gev_done[GMAX] = {};
   cudaEvent_t ev_fork = nullptr;
+  cudaStream_t s_rhs = nullptr;       // a1 (R = B X) concurrently with the first panels
+  cudaEvent_t ev_a1 = nullptr, ev_rhs = nullptr;
   cudaEvent_t gev_first[GMAX] = {};
   cudaStream_t gx[GMAX] = {};         // per group: the stream of the diagonal-block inverses
   cudaEvent_t gev_t[GMAX] = {}, gev_x[GMAX] = {};
@@ -348,7 +350,9 @@ const double2* inv_ptr(const Lu& v, int64_t kb, int which) { return v.Inv + (kb 
 // C = alpha op(A) B + beta C (single), with split-K when the output tile grid is too small
 // to fill the GPU (the reduced matrices Q^H (A Q) are m0 x m0 with K = n).
 void gemm_gen(feast_ctx* h, int64_t M, int64_t N, int64_t K, bool conjA, const double2* A, int64_t lda,
-              const double2* B, int64_t ldb, double2* C, int64_t ldc, double2 alpha, double2 beta) {
+              const double2* B, int64_t ldb, double2* C, int64_t ldc, double2 alpha, double2 beta,
+              cudaStream_t s = nullptr) {
+  if (!s) s = h->stream;
   // 32x32 CTA tiles, 3 resident per SM: fewer than 444 tiles leave the GPU under-filled
   const int64_t tiles = ((M + 31) / 32) * ((N + 31) / 32);
   int splits = 1;
@@ -358,7 +362,7 @@ void gemm_gen(feast_ctx* h, int64_t M, int64_t N, int64_t K, bool conjA, const d
   }
   if (splits <= 1) {
     ZgemmArgs p{M, N, K, A, lda, 0, B, ldb, 0, C, ldc, 0, alpha, beta, 1};
-    feast::zgemm_launch(p, conjA, feast::ZG_GEN, h->stream);
+    feast::zgemm_launch(p, conjA, feast::ZG_GEN, s);
     return;
   }
   const int64_t kc = ((K + splits - 1) / splits + 15) / 16 * 16;
@@ -369,15 +373,15 @@ void gemm_gen(feast_ctx* h, int64_t M, int64_t N, int64_t K, bool conjA, const d
   const int64_t sA = conjA ? kc : kc * lda;
   if (full > 0) {
     ZgemmArgs p{M, N, kc, A, lda, sA, B, ldb, kc, h->SK, M, M * N, make_double2(1, 0), make_double2(0, 0), full};
-    feast::zgemm_launch(p, conjA, feast::ZG_GEN, h->stream);
+    feast::zgemm_launch(p, conjA, feast::ZG_GEN, s);
   }
   if (full < splits) {
     const int64_t k0 = (int64_t)full * kc;
     ZgemmArgs p{M, N, K - k0, A + (conjA ? k0 : k0 * lda), lda, 0, B + k0, ldb, 0, h->SK + (int64_t)full * M * N, M, 0,
                 make_double2(1, 0), make_double2(0, 0), 1};
-    feast::zgemm_launch(p, conjA, feast::ZG_GEN, h->stream);
+    feast::zgemm_launch(p, conjA, feast::ZG_GEN, s);
   }
-  feast::splitk_reduce_launch(C, ldc, h->SK, M, N, splits, alpha, beta, h->stream);
+  feast::splitk_reduce_launch(C, ldc, h->SK, M, N, splits, alpha, beta, s);
 }
 
 // ---------------------------------------------------------------- blocked LU (batched)
@@ -623,14 +627,28 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
   int64_t ldr = ldx;
   const double2* Rl = V;
   int64_t ldrl = ldv;
+  // a1 on its own stream when possible: the node groups start their shifts and first panels at
+  // once, and wait for R only where they copy it into the augmented columns
+  cudaEvent_t rhs_wait = nullptr;
   if (!h->b_id) {   // (rhs_ready: formed row-sharded and all-reduced by project_impl)
+    const bool side_a1 = !rhs_ready && h->s_rhs && !h->prof_serial;
+    cudaStream_t sa = h->stream;
+    if (side_a1) {
+      cudaEventRecord(h->ev_a1, h->stream);
+      cudaStreamWaitEvent(h->s_rhs, h->ev_a1, 0);
+      sa = h->s_rhs;
+    }
     if (doR) {
-      if (!rhs_ready) gemm_gen(h, n, m, n, false, B, ldb, X, ldx, h->R, ld, one, zero);
+      if (!rhs_ready) gemm_gen(h, n, m, n, false, B, ldb, X, ldx, h->R, ld, one, zero, sa);
       Rr = h->R; ldr = ld;
     }
     if (doL) {
-      if (!rhs_ready) gemm_gen(h, n, m, n, true, B, ldb, V, ldv, h->RL, ld, one, zero);
+      if (!rhs_ready) gemm_gen(h, n, m, n, true, B, ldb, V, ldv, h->RL, ld, one, zero, sa);
       Rl = h->RL; ldrl = ld;
+    }
+    if (side_a1) {
+      cudaEventRecord(h->ev_rhs, sa);
+      rhs_wait = h->ev_rhs;
     }
   }
   const int owned = h->j1 - h->j0;
@@ -670,6 +688,7 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
         feast::shift_launch(bat(v.Cw, ld, st), A, lda, B, ldb, zj, n, v.nbat, v.sm, 0, w0);
         auto rest = [&, zj](cudaStream_t sr) {
           feast::shift_launch(bat(v.Cw, ld, st), A, lda, B, ldb, zj, n, v.nbat, sr, w0, n);
+          if (rhs_wait) cudaStreamWaitEvent(sr, rhs_wait, 0);
           if (doR)
             feast::broadcast_copy_launch(bat(v.Cw + n * ld, ld, st), Rr, ldr, n, m, v.nbat,
                                          pair ? feast::BC_PAIR : feast::BC_COPY, sr);
@@ -686,6 +705,7 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
       } else if (doR) {
         // cached factors (NEXT-1, "factored just once"): Y_j = U^-1 L^-1 P_j R
         double2* Yg = h->Y + b0 * ld * mr;   // (factor cache and real-pencil mode are exclusive: mr = m)
+        if (rhs_wait) cudaStreamWaitEvent(v.sm, rhs_wait, 0);
         feast::gather_rows_launch(bat(Yg, ld, ld * mr), Rr, ldr, 0, h->perm + (int64_t)b0 * n, n, m, v.nbat, v.sm);
         solve_right_fwd(h, v, Yg, ld * mr, m);
         solve_right_back(h, v, Yg, ld * mr, m);
@@ -693,6 +713,7 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
       if (doL && !csl) {
         // Z_j = P^T L^-H U^-H RL  (P^T folded into the accumulate below)
         double2* Yg = h->YL + b0 * ld * mr;
+        if (rhs_wait) cudaStreamWaitEvent(v.sm, rhs_wait, 0);
         feast::broadcast_copy_launch(bat(Yg, ld, ld * mr), Rl, ldrl, n, m, v.nbat, pair, v.sm);
         solve_left(h, v, Yg);
       }
@@ -982,7 +1003,10 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
                cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming) == cudaSuccess &&
                cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming) == cudaSuccess) {
       h->own_stream = true;
-      bool ok = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) == cudaSuccess;
+      bool ok = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+                cudaStreamCreateWithFlags(&h->s_rhs, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaEventCreateWithFlags(&h->ev_a1, cudaEventDisableTiming) == cudaSuccess &&
+                cudaEventCreateWithFlags(&h->ev_rhs, cudaEventDisableTiming) == cudaSuccess;
       for (int g = 1; g < feast_ctx::GMAX && ok; ++g)
         ok = cudaStreamCreateWithFlags(&h->gs[g], cudaStreamNonBlocking) == cudaSuccess &&
              cudaStreamCreateWithPriority(&h->gside[g], cudaStreamNonBlocking, hi) == cudaSuccess &&
@@ -1531,6 +1555,9 @@ void feast_destroy(feast_handle h) {
     if (h->gev_done[g]) cudaEventDestroy(h->gev_done[g]);
   }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->s_rhs) cudaStreamDestroy(h->s_rhs);
+  if (h->ev_a1) cudaEventDestroy(h->ev_a1);
+  if (h->ev_rhs) cudaEventDestroy(h->ev_rhs);
   for (int g = 0; g < feast_ctx::GMAX; ++g) {
     if (h->gev_first[g]) cudaEventDestroy(h->gev_first[g]);
     if (h->gx[g]) cudaStreamDestroy(h->gx[g]);
