@@ -245,11 +245,12 @@ def run_gpu(args):
     zg = prof["zgemm"]
     achieved = zg["flops"] / (zg["ms"] * 1e-3) / 1e12 if zg["ms"] > 0 else 0.0
     total_prof_ms = sum(v["ms"] for v in prof.values())
-    traffic = None
-    try:
+    traffic, traffic_src = None, None
+    try:  # committed ncu capture of the same serialised step (tools/zgemm_traffic.py)
         tr = json.load(open(os.path.join(ROOT, "profiles", "zgemm_traffic.json")))
         if tr.get("config") == args.config:
             traffic = tr.get("dram_bytes_per_launch")
+            traffic_src = "profiles/zgemm_traffic.json: " + tr.get("source", "")
     except Exception:  # noqa: BLE001
         pass
     roofline = {"bound": "tensor", "kernel": "zgemm_dmma_kernel (FP64 DMMA.8x8x4)", "achieved": achieved,
@@ -257,6 +258,8 @@ def run_gpu(args):
                 "traffic": traffic, "peak_source": FP64_PEAK_NOTE,
                 "launches_per_step": zg["launches"] / prof_steps,
                 "algorithmic_flops_per_launch": zg["flops"] / max(1, zg["launches"]),
+                "algorithmic_bytes_per_launch": zg["bytes"] / max(1, zg["launches"]),
+                "traffic_source": traffic_src,
                 "share_of_serialised_step": zg["ms"] / total_prof_ms if total_prof_ms > 0 else None,
                 "serialised_step_ms": total_prof_ms / prof_steps,
                 "timing": "CUDA events per launch on its stream, serialised pass after the timed region",

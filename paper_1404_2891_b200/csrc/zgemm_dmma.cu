@@ -260,9 +260,18 @@ void launch_variant(const ZgemmArgs& p, int v, cudaStream_t s) {
 
 }  // namespace
 
+// Algorithmic HBM bytes of one launch: op(A), B read once (once for the whole batch when the
+// batch stride is 0), C read (beta != 0 or SUB) and written once.
+static double zgemm_bytes(const ZgemmArgs& p, int mode) {
+  const double b = p.batch;
+  const bool readC = mode == ZG_SUB || p.beta.x != 0.0 || p.beta.y != 0.0;
+  return 16.0 * ((p.sA ? b : 1.0) * p.M * p.K + (p.sB ? b : 1.0) * p.K * p.N +
+                 b * p.M * p.N * (readC ? 2.0 : 1.0));
+}
+
 void zgemm_launch_variant(const ZgemmArgs& p, bool conjA, int mode, int variant, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.batch <= 0) return;
-  ProfScope ps_(K_ZGEMM, 8.0 * (double)p.M * (double)p.N * (double)p.K * p.batch, 0.0, s);
+  ProfScope ps_(K_ZGEMM, 8.0 * (double)p.M * (double)p.N * (double)p.K * p.batch, zgemm_bytes(p, mode), s);
   if (conjA) {
     if (mode == ZG_SUB) launch_variant<true, ZG_SUB>(p, variant, s); else launch_variant<true, ZG_GEN>(p, variant, s);
   } else {
@@ -281,7 +290,7 @@ void zgemm_launch(const ZgemmArgs& p, bool conjA, int mode, cudaStream_t s) {
     zgemm_launch_variant(p, conjA, mode, env_variant, s);
     return;
   }
-  ProfScope ps_(K_ZGEMM, 8.0 * (double)p.M * (double)p.N * (double)p.K * p.batch, 0.0, s);
+  ProfScope ps_(K_ZGEMM, 8.0 * (double)p.M * (double)p.N * (double)p.K * p.batch, zgemm_bytes(p, mode), s);
   if (conjA) {
     if (mode == ZG_SUB) launch_t<true, ZG_SUB>(p, s); else launch_t<true, ZG_GEN>(p, s);
   } else {

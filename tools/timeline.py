@@ -17,23 +17,25 @@ ap.add_argument("key", nargs="?", default="C2")
 ap.add_argument("--out", default=None)
 ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--batch", type=int, default=0)
+ap.add_argument("--world", type=int, default=1, help="time rank 0's node share of a P-rank job")
 args = ap.parse_args()
 P = synth.make_pencil(args.key, n=args.n)
 s = P.spec
-f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, P.B is None, max_batch=args.batch)
+f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, P.B is None, max_batch=args.batch,
+          world=args.world)
 d = lambda a: None if a is None else torch.from_numpy(np.asfortranarray(a)).to("cuda")
 A, B, X = d(P.A), d(P.B), d(P.X0)
-Q = f.project(A, B, X)
-f.project(A, B, X, Q)
+Q = f.project(A, B, X, allreduce=False)
+f.project(A, B, X, Q, allreduce=False)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(f.stream)
-f.project(A, B, X, Q)
+f.project(A, B, X, Q, allreduce=False)
 e1.record(f.stream)
 torch.cuda.synchronize()
 print(f"{args.key}: project without events {e0.elapsed_time(e1):.3f} ms")
 f.profile(True)
-f.project(A, B, X, Q)
+f.project(A, B, X, Q, allreduce=False)
 recs = f.profile_records()
 f.profile(False)
 wall = max(r[3] for r in recs)

@@ -1,0 +1,103 @@
+"""DRAM traffic of the dominant kernel (zgemm_dmma_kernel) per launch vs its algorithmic bytes.
+
+Two passes over the SAME bench step (C2 project + reduce, serialised profile mode, the launch
+sequence bench.py's roofline pass times):
+
+    python tools/zgemm_traffic.py alg  gpurun_out/zg_alg.json     # algorithmic bytes / flops
+    ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+        -k regex:zgemm_dmma --profile-from-start off --csv --log-file gpurun_out/zg_ncu.csv \
+        python tools/zgemm_traffic.py ncu
+    python tools/zgemm_traffic.py merge gpurun_out/zg_alg.json gpurun_out/zg_ncu.csv profiles/zgemm_traffic.json
+
+ncu flushes L2 before every replayed launch (--cache-control all), so the DRAM bytes are the
+cold-cache figure: every operand tile the kernel touches comes from HBM once if the tiling
+re-reads nothing."""
+import csv
+import json
+import sys
+
+sys.path.insert(0, ".")
+
+
+def run_step(mode):
+    import numpy as np
+    import torch
+    import synth
+    from paper_1404_2891_b200 import Feast, feast as fb
+    P = synth.make_pencil("C2")
+    s = P.spec
+    f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, P.B is None)
+    d = lambda a: None if a is None else torch.from_numpy(np.asfortranarray(a)).to("cuda")
+    A, B, X = d(P.A), d(P.B), d(P.X0)
+    Q = torch.empty_like(X)
+    Ah = torch.empty((P.m0, P.m0), dtype=torch.complex128, device="cuda").t()
+    Bh = torch.empty_like(Ah)
+
+    def step():
+        f.project(A, B, X, Q, allreduce=False)
+        f.reduce(A, B, Q, None, Ah, Bh)
+
+    f.profile(True, serial=True)
+    step()                      # warm-up: lazy init, workspace, kernel attributes
+    torch.cuda.synchronize()
+    f.profile(True, serial=True)
+    if mode == "ncu":
+        torch.cuda.profiler.start()
+    step()
+    torch.cuda.synchronize()
+    if mode == "ncu":
+        torch.cuda.profiler.stop()
+    zg = f.profile_summary()["zgemm"]
+    f.profile(False)
+    return zg
+
+
+def merge(alg_path, ncu_path, out_path):
+    alg = json.load(open(alg_path))
+    rows = []
+    with open(ncu_path) as fh:
+        lines = [l for l in fh if l.startswith('"')]
+    for r in csv.DictReader(lines):
+        if "zgemm_dmma" not in r["Kernel Name"]:
+            continue
+        rows.append(r)
+    per = {}
+    for r in rows:
+        v = float(r["Metric Value"].replace(",", ""))
+        unit = r["Metric Unit"]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3,
+                 "msecond": 1e6}.get(unit, 1)
+        per.setdefault(r["ID"], {})[r["Metric Name"]] = v * scale
+    n = len(per)
+    dram = sum(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0) for m in per.values())
+    rd = sum(m.get("dram__bytes_read.sum", 0) for m in per.values())
+    ns = sum(m.get("gpu__time_duration.sum", 0) for m in per.values())
+    out = {
+        "config": "C2",
+        "kernel": "zgemm_dmma_kernel",
+        "launches": n,
+        "launches_alg": alg["launches"],
+        "dram_bytes_per_launch": dram / n,
+        "dram_read_bytes_per_launch": rd / n,
+        "algorithmic_bytes_per_launch": alg["bytes"] / alg["launches"],
+        "traffic_over_algorithmic": dram / alg["bytes"] if alg["bytes"] else None,
+        "ncu_cold_cache_ms_per_step": ns * 1e-6,
+        "ncu_tflops_cold_serialised": alg["flops"] / (ns * 1e-9) / 1e12 if ns else None,
+        "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
+                  "--clock-control none -k regex:zgemm_dmma over one serialised C2 bench step "
+                  "(tools/zgemm_traffic.py)",
+    }
+    json.dump(out, open(out_path, "w"), indent=1)
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    mode = sys.argv[1]
+    if mode == "alg":
+        zg = run_step("alg")
+        json.dump(zg, open(sys.argv[2], "w"), indent=1)
+        print(zg)
+    elif mode == "ncu":
+        run_step("ncu")
+    elif mode == "merge":
+        merge(sys.argv[2], sys.argv[3], sys.argv[4])
