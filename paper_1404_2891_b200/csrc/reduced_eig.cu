@@ -8,18 +8,21 @@
 //   2. Complex single-shift QR iteration (Wilkinson shift, exceptional shifts every 10
 //      iterations, deflation |h_{l,l-1}| <= eps (|h_ll| + |h_{l-1,l-1}|)) on the Hessenberg
 //      matrix held PACKED in shared memory (column j keeps rows 0..j+1: ~m^2/2 entries), the
-//      bulge as a separate scalar; Givens rotations (zlartg convention) applied to whole rows /
-//      columns (wantt: the full Schur form T = Z^H M Z) by ONE warp (lanes over rows / columns,
-//      __syncwarp between the dependent passes), recorded per sweep and applied to Z in global
-//      memory after the sweep by the whole CTA (one thread per row of Z, 8-deep prefetch).
-//   Measured on B200 (m = 64 / 128 / 160): 5.6 / 28 / 49 ms, of which the QR sweeps are 23.5 ms
-//   at m = 128 (~16k dependent Givens steps at ~1.2 us): cuSOLVER Xgeev (26 ms at m = 128) stays
-//   the default; this solver is device-resident (FEAST_EIG=own, feast_small_eig).
+//      bulge as a separate scalar.  Each step's rotation G = [[a, b], [-conj(b), conj(a)]]
+//      (a = conj(f)/r, b = conj(g)/r, one reciprocal square root) is chased by ONE warp inside a
+//      sliding window of RE_W steps (one lane per row / column of the window); the CTA applies
+//      the window's rotations to the rest of H after each window and to Z after each sweep.
+//   Measured on B200 (m = 64 / 128 / 160): 6.1 / 26 / 42 ms; at m = 128 the chase is ~28k
+//   dependent steps of ~1.1k cycles (single-warp latency: rsqrt, shared-memory round trips),
+//   the Householder phase 4.4 ms.  cuSOLVER Xgeev (26 ms at m = 128) stays the default; this
+//   solver is device-resident (FEAST_EIG=own, feast_small_eig).  FEAST_RE_DEBUG=1 prints the
+//   per-phase cycle counts.
 //   3. Eigenvectors of T by back-substitution (one thread per eigenvector):
 //      y_i = e_i, y_j = -(sum_{l=j+1..i} t_jl y_l) / (t_jj - t_ii), j < i.
 //   The caller forms W = Z Y (a DMMA ZGEMM).  info = 0, or 1 if the QR iteration did not
 //   converge within 30 m sweeps (the caller then falls back to cuSOLVER).
 #include <cfloat>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -30,6 +33,7 @@ namespace feast {
 namespace {
 
 constexpr int RE_T = 256;   // threads
+constexpr int RE_W = 29;    // chase window: rows k0-1 .. k1+1 and columns k0-1 .. k1+1 fit 32 lanes
 
 __device__ double block_sum_re(double v, double* red) {
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
@@ -55,14 +59,16 @@ __host__ __device__ __forceinline__ int poff(int j, int m) {
 __global__ void __launch_bounds__(RE_T) reduced_eig_kernel(double2* __restrict__ H, int m, int64_t ldh,
                                                            double2* __restrict__ Z, int64_t ldz,
                                                            double2* __restrict__ lam, double2* __restrict__ Y,
-                                                           int64_t ldy, int32_t* __restrict__ info) {
+                                                           int64_t ldy, int32_t* __restrict__ info, int dbg) {
   extern __shared__ __align__(16) double2 S[];   // packed Hessenberg / Schur form
   __shared__ double red[RE_T / 32];
-  __shared__ double2 rot_c[RE_MAXM], rot_s[RE_MAXM];   // c (real, in .x) and s per sweep step
+  __shared__ double2 rot_c[RE_MAXM], rot_s[RE_MAXM];   // a and b of each sweep step's rotation
   __shared__ double2 u_s[RE_MAXM], w_s[RE_MAXM];
   __shared__ int lo_s, conv_s, hi_s;
-  __shared__ double2 bulge_s, x_s, y_s;
   const int tid = threadIdx.x;
+  const long long t_begin = clock64();
+  long long t_hess = 0, t_qr = 0;
+  long long nsteps = 0, c_defl = 0, c_chase = 0, c_defer = 0, c_z = 0, cA;
 
   // ---- 1. Householder Hessenberg reduction in global memory; Z = I then Z <- Z P_j
   for (int idx = tid; idx < m * m; idx += RE_T) {
@@ -143,6 +149,7 @@ __global__ void __launch_bounds__(RE_T) reduced_eig_kernel(double2* __restrict__
       __syncthreads();
     }
   }
+  t_hess = clock64();
   // ---- 2. packed copy into shared memory (entries below the subdiagonal are zero)
   for (int j = 0; j < m; ++j)
     for (int i = tid; i <= min(j + 1, m - 1); i += RE_T) S[poff(j, m) + i] = H[i + j * ldh];
@@ -151,13 +158,20 @@ __global__ void __launch_bounds__(RE_T) reduced_eig_kernel(double2* __restrict__
 
   const double eps = DBL_EPSILON;
   const int warp = tid >> 5, lane = tid & 31;
-  // The QR sweeps run on WARP 0 alone (lanes over rows / columns, __syncwarp between the
-  // dependent passes: no CTA barrier per rotation); after each sweep all warps apply the sweep's
-  // rotations to Z in global memory.
+  // The bulge of a sweep is chased by WARP 0 alone inside a sliding window of RE_W steps
+  // (lanes over the window's rows / columns, __syncwarp between the dependent passes): step k
+  // updates rows k, k+1 only up to column cmax = k1 + 1 and columns k, k+1 only from row
+  // k0 - 1, so each step touches <= 32 entries per pass whatever m is.  Left and right
+  // rotations commute, and columns right of the window / rows above it never feed back into
+  // it, so after each window the whole CTA applies the window's rotations to those parts
+  // (one thread per column: the left chain down rows k0..k1; one thread per row: the right
+  // chain across columns k0..k1) and, after the sweep, to Z.
   int hi = m - 1, its = 0, total = 0;
   const int maxit = 30 * m;
   bool failed = false;
+  double2 f = make_double2(0.0, 0.0), g = f, bulge = f;   // warp 0: the chase state
   while (true) {
+    cA = clock64();
     if (warp == 0) {
       int lo = 0;
       bool sweep = false;
@@ -204,59 +218,109 @@ __global__ void __launch_bounds__(RE_T) reduced_eig_kernel(double2* __restrict__
             mu = cabs1(csub(l1, d)) <= cabs1(csub(l2, d)) ? l1 : l2;
           }
         }
-        double2 f = csub(at(lo, lo), mu), g = at(lo + 1, lo), bulge = make_double2(0.0, 0.0);
-        for (int k = lo; k < hi; ++k) {
-          // rotation G = [[c, s], [-conj(s), c]] with G [f; g] = [r; 0] (zlartg), every lane
-          const double af2 = f.x * f.x + f.y * f.y, ag2 = g.x * g.x + g.y * g.y;
-          double c;
-          double2 sr;
-          if (ag2 == 0.0) { c = 1.0; sr = make_double2(0.0, 0.0); }
-          else if (af2 == 0.0) { const double ig = rsqrt(ag2); c = 0.0; sr = make_double2(g.x * ig, -g.y * ig); }
-          else {
-            const double inrm = rsqrt(af2 + ag2), iaf = rsqrt(af2);
-            c = af2 * iaf * inrm;                                    // |f| / nrm
-            const double2 fs = make_double2(f.x * iaf, f.y * iaf);   // f / |f|
-            sr = make_double2((fs.x * g.x + fs.y * g.y) * inrm, (fs.y * g.x - fs.x * g.y) * inrm);
-          }
-          if (lane == 0) { rot_c[k] = make_double2(c, 0.0); rot_s[k] = sr; }
-          // rows k, k+1, columns (k-1 or lo) .. m-1
-          const int c0 = k > lo ? k - 1 : lo;
-          for (int col = c0 + lane; col < m; col += 32) {
-            const double2 hk = at(k, col);
-            const double2 hk1 = (k + 1 <= col + 1) ? at(k + 1, col) : bulge;
-            const double2 nk = cadd(make_double2(c * hk.x, c * hk.y), cmul(sr, hk1));
-            const double2 nk1 = csub(make_double2(c * hk1.x, c * hk1.y), cmul(cconj(sr), hk));
-            at(k, col) = nk;
-            if (k + 1 <= col + 1) at(k + 1, col) = nk1;
-          }
-          __syncwarp();
-          // columns k, k+1, rows 0 .. min(k+2, hi); (k+2, k) is zero before, the new bulge after
-          const int r1 = min(k + 2, hi);
-          double2 nb = make_double2(0.0, 0.0);
-          for (int row = lane; row <= r1; row += 32) {
-            const double2 hik = (row <= k + 1) ? at(row, k) : make_double2(0.0, 0.0);
-            const double2 hik1 = at(row, k + 1);
-            const double2 nk = cadd(make_double2(c * hik.x, c * hik.y), cmul(cconj(sr), hik1));
-            const double2 nk1 = csub(make_double2(c * hik1.x, c * hik1.y), cmul(sr, hik));
-            if (row <= k + 1) at(row, k) = nk;
-            at(row, k + 1) = nk1;
-            if (row == k + 2) nb = nk;
-          }
-          __syncwarp();
-          // next rotation's pair: (h_{k+1,k}, bulge (k+2, k)), broadcast from the owning lanes
-          if (k + 1 < hi) {
-            const int ob = (k + 2) & 31;
-            bulge = make_double2(__shfl_sync(0xffffffffu, nb.x, ob), __shfl_sync(0xffffffffu, nb.y, ob));
-            f = at(k + 1, k);
-            g = bulge;
-          }
-        }
+        f = csub(at(lo, lo), mu);
+        g = at(lo + 1, lo);
+        bulge = make_double2(0.0, 0.0);
       }
       if (lane == 0) { lo_s = sweep ? lo : -1; conv_s = failed ? -1 : (hi <= 0 ? 1 : 0); hi_s = hi; }
     }
     __syncthreads();
     const int lo = lo_s, hiv = hi_s;
+    c_defl += clock64() - cA; cA = clock64();
     if (lo >= 0) {
+      for (int k0 = lo; k0 < hiv; k0 += RE_W) {
+        const int k1 = min(k0 + RE_W, hiv);
+        const int cmax = min(k1 + 1, m - 1);
+        const int rmin = max(k0 - 1, 0);
+        nsteps += k1 - k0;
+        const long long cB = clock64();
+        if (warp == 0) {
+          for (int k = k0; k < k1; ++k) {
+            // rotation G = [[a, b], [-conj(b), conj(a)]], a = conj(f)/nrm, b = conj(g)/nrm, so that
+            // G [f; g] = [nrm; 0]: one reciprocal square root on the dependent chain (every lane)
+            double2 a = make_double2(1.0, 0.0), b = make_double2(0.0, 0.0);
+            {
+              double n2 = f.x * f.x + f.y * f.y + g.x * g.x + g.y * g.y;
+              if (n2 > 0.0) {
+                double sc = 1.0;
+                if (n2 < 1e-280 || n2 > 1e280) {   // rescale before squaring (rare)
+                  sc = fmax(fmax(fabs(f.x), fabs(f.y)), fmax(fabs(g.x), fabs(g.y)));
+                  sc = 1.0 / sc;
+                  const double2 fs = make_double2(f.x * sc, f.y * sc), gs = make_double2(g.x * sc, g.y * sc);
+                  n2 = fs.x * fs.x + fs.y * fs.y + gs.x * gs.x + gs.y * gs.y;
+                }
+                const double in = rsqrt(n2) * sc;
+                a = make_double2(f.x * in, -f.y * in);
+                b = make_double2(g.x * in, -g.y * in);
+              }
+            }
+            if (lane == 0) { rot_c[k] = a; rot_s[k] = b; }
+            // rows k, k+1, columns (k-1 or lo) .. cmax: <= RE_W + 3 = 32 entries, one per lane
+            {
+              const int col = (k > lo ? k - 1 : lo) + lane;
+              if (col <= cmax) {
+                const double2 hk = at(k, col);
+                const double2 hk1 = (k + 1 <= col + 1) ? at(k + 1, col) : bulge;
+                at(k, col) = cadd(cmul(a, hk), cmul(b, hk1));
+                if (k + 1 <= col + 1) at(k + 1, col) = csub(cmul(cconj(a), hk1), cmul(cconj(b), hk));
+              }
+            }
+            __syncwarp();
+            // columns k, k+1, rows rmin .. min(k+2, hi): <= 32 entries, one per lane; (k+2, k) is
+            // zero before, the new bulge after
+            const int r1 = min(k + 2, hiv);
+            double2 nb = make_double2(0.0, 0.0);
+            {
+              const int row = rmin + lane;
+              if (row <= r1) {
+                const double2 hik = (row <= k + 1) ? at(row, k) : make_double2(0.0, 0.0);
+                const double2 hik1 = at(row, k + 1);
+                const double2 nk = cadd(cmul(cconj(a), hik), cmul(cconj(b), hik1));
+                if (row <= k + 1) at(row, k) = nk;
+                at(row, k + 1) = csub(cmul(a, hik1), cmul(b, hik));
+                nb = nk;
+              }
+            }
+            __syncwarp();
+            // next rotation's pair: (h_{k+1,k}, bulge (k+2, k)), broadcast from the owning lane
+            if (k + 1 < hiv) {
+              const int ob = (k + 2 - rmin) & 31;
+              bulge = make_double2(__shfl_sync(0xffffffffu, nb.x, ob), __shfl_sync(0xffffffffu, nb.y, ob));
+              f = at(k + 1, k);
+              g = bulge;
+            }
+          }
+        }
+        __syncthreads();
+        c_chase += clock64() - cB;
+        const long long cC = clock64();
+        // the window's rotations on the columns right of it (left chain down rows k0..k1) and
+        // on the rows above it (right chain across columns k0..k1)
+        const int ncol = m - 1 - cmax, nrow = rmin;
+        for (int t = tid; t < ncol + nrow; t += RE_T) {
+          if (t < ncol) {
+            const int col = cmax + 1 + t;
+            double2 x = at(k0, col);
+            for (int k = k0; k < k1; ++k) {
+              const double2 a = rot_c[k], b = rot_s[k], y = at(k + 1, col);
+              at(k, col) = cadd(cmul(a, x), cmul(b, y));
+              x = csub(cmul(cconj(a), y), cmul(cconj(b), x));
+            }
+            at(k1, col) = x;
+          } else {
+            const int row = t - ncol;
+            double2 x = at(row, k0);
+            for (int k = k0; k < k1; ++k) {
+              const double2 a = rot_c[k], b = rot_s[k], y = at(row, k + 1);
+              at(row, k) = cadd(cmul(cconj(a), x), cmul(cconj(b), y));
+              x = csub(cmul(a, y), cmul(b, x));
+            }
+            at(row, k1) = x;
+          }
+        }
+        __syncthreads();
+      }
+      c_defer += clock64() - cA; cA = clock64();
       // Z <- Z G_k^H, k = lo..hiv-1, one thread per row; the row segment is prefetched 8 at a time
       for (int row = tid; row < m; row += RE_T) {
         double2* zr = Z + row;
@@ -270,10 +334,9 @@ __global__ void __launch_bounds__(RE_T) reduced_eig_kernel(double2* __restrict__
           for (int e = 0; e < 8; ++e) {
             const int k = k0 + e;
             if (k < hiv) {
-              const double c = rot_c[k].x;
-              const double2 sr = rot_s[k];
-              const double2 nk = cadd(make_double2(c * zk.x, c * zk.y), cmul(cconj(sr), nx[e]));
-              zk = csub(make_double2(c * nx[e].x, c * nx[e].y), cmul(sr, zk));
+              const double2 a = rot_c[k], b = rot_s[k];
+              const double2 nk = cadd(cmul(cconj(a), zk), cmul(cconj(b), nx[e]));
+              zk = csub(cmul(a, nx[e]), cmul(b, zk));
               zr[(int64_t)k * ldz] = nk;
             }
           }
@@ -282,8 +345,13 @@ __global__ void __launch_bounds__(RE_T) reduced_eig_kernel(double2* __restrict__
       }
     }
     __syncthreads();
+    if (lo >= 0) c_z += clock64() - cA;
     if (conv_s != 0) break;
   }
+  t_qr = clock64();
+  if (dbg && tid == 0)
+    printf("reduced_eig m=%d: hessenberg %lld cyc, qr %lld cyc, sweeps %d, steps %lld; defl+shift %lld, chase %lld, "
+           "windows %lld, Z %lld\n", m, t_hess - t_begin, t_qr - t_hess, total, nsteps, c_defl, c_chase, c_defer, c_z);
   if (conv_s < 0) {
     if (tid == 0) info[0] = 1;
     return;
@@ -305,6 +373,7 @@ __global__ void __launch_bounds__(RE_T) reduced_eig_kernel(double2* __restrict__
     }
   }
   if (tid == 0) info[0] = 0;
+  if (dbg && tid == 0) printf("reduced_eig m=%d: vectors %lld cyc\n", m, clock64() - t_qr);
 }
 
 }  // namespace
@@ -319,7 +388,8 @@ bool reduced_eig_launch(double2* H, int m, int64_t ldh, double2* Z, int64_t ldz,
     cudaFuncSetAttribute(reduced_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     configured = true;
   }
-  reduced_eig_kernel<<<1, RE_T, smem, s>>>(H, m, ldh, Z, ldz, lam, Y, ldy, info);
+  static const int dbg = getenv("FEAST_RE_DEBUG") ? 1 : 0;
+  reduced_eig_kernel<<<1, RE_T, smem, s>>>(H, m, ldh, Z, ldz, lam, Y, ldy, info, dbg);
   count_launch();
   return true;
 }
