@@ -204,7 +204,9 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
           if (kk > bk) { bk = kk; bs = s; }
         }
       }
-      // every thread inverts its own candidate now, overlapping the division with the reduction
+      // warp argmax first (the REDUX issues before the reciprocal's dependent chain), then every
+      // thread inverts its own candidate while the reduction is in flight
+      const unsigned long long wk = warp_max_key(bk);
       double2 myrcp = make_double2(0.0, 0.0);
 #pragma unroll
       for (int s = 0; s < S; ++s)
@@ -220,7 +222,6 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
             }
           }
         }
-      const unsigned long long wk = warp_max_key(bk);
       // the warp's winning lane stages its chunk row and 1/pivot; one barrier for the CTA step
       if (wk != 0ull && bk == wk) {
 #pragma unroll

@@ -12,6 +12,7 @@
 // holding rows l and l + 32 in registers; T sits in shared memory.  Step t of a forward solve:
 // x_t is broadcast from its owner lane by shuffle (scaled by the precomputed 1/T_tt if not unit),
 // and every lane applies x_r -= T_rt x_t to its rows r > t (two LDS.128 + two complex FMAs).
+// T is staged in shared memory by TMA bulk copies (one per column) completing an mbarrier.
 // One column per warp and few warps per CTA spread the independent chains over many SMs (the
 // pieces are issue-latency bound per warp); all warps of a CTA share one copy of T.
 #include "common.cuh"
@@ -21,37 +22,52 @@
 namespace feast {
 namespace {
 
-constexpr int NB = 64, LDT = NB + 1;   // T[r][c] at Ts[r * LDT + c]: lanes (rows) 16 B x 65 apart
+constexpr int NB = 64, LDT = NB + 1;   // T[r][c] at Ts[c * LDT + r] (column-major, 1040 B columns)
 constexpr int WARPS = 4;      // warps per CTA; one right-hand-side column per warp (spread over SMs)
 
 __device__ __forceinline__ double2 shfl2(double2 v, int src) {
   return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
 }
 
-// op(T)[r][c] from the shared copy (CONJT: op = ^H)
+// op(T)[r][c] from the shared copy, stored column-major Ts[c * LDT + r] (CONJT: op = ^H).  Lanes
+// run over r: consecutive 16 B (no conflict) for op = T; 1040 B apart for op = T^H (4 wavefronts,
+// the minimum for a warp's 512 B).
 template <bool CONJT>
 __device__ __forceinline__ double2 opT(const double2* Ts, int r, int c) {
-  if (!CONJT) return Ts[r * LDT + c];
-  const double2 v = Ts[c * LDT + r];
+  if (!CONJT) return Ts[c * LDT + r];
+  const double2 v = Ts[r * LDT + c];
   return make_double2(v.x, -v.y);
 }
 
-// Load the nb x nb block into Ts (identity-padded to nbp), all elements in flight at once with
-// cp.async (a latency chain of dependent loads would dominate these microsecond kernels).  The
-// solves read only the strict triangle of op(T) and its diagonal (through dinv), so the other
+__device__ __forceinline__ unsigned saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+// Stage the nb x nb block into Ts with the TMA unit: one bulk copy (cp.async.bulk, nb * 16 B) per
+// column, completing a transaction mbarrier; the identity padding up to nbp is written meanwhile.
+// The solves read only the strict triangle of op(T) and its diagonal (through dinv), so the other
 // factor stored in the same LU workspace block needs no masking.  1 / diagonal into dinv.
 template <bool LOWER, bool UNIT, bool CONJT>
 __device__ void load_tri(const double2* __restrict__ T, int64_t ld, int nb, int nbp, double2* Ts, double2* dinv) {
-  for (int idx = threadIdx.x; idx < nbp * nbp; idx += blockDim.x) {
-    const int r = idx % nbp, c = idx / nbp;   // source element T[r][c] (coalesced along r)
-    if (r < nb && c < nb) {
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(&Ts[r * LDT + c]);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(T + r + (int64_t)c * ld));
-    } else {
-      Ts[r * LDT + c] = make_double2(r == c ? 1.0 : 0.0, 0.0);
-    }
+  __shared__ __align__(8) unsigned long long tbar;
+  const unsigned bar = saddr(&tbar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)(nb * nb * 16))
+                 : "memory");
   }
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  for (int c = threadIdx.x; c < nb; c += blockDim.x)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(saddr(Ts + c * LDT)), "l"(T + (int64_t)c * ld), "r"(nb * 16), "r"(bar) : "memory");
+  if (nb < nbp)
+    for (int idx = threadIdx.x; idx < nbp * nbp; idx += blockDim.x) {
+      const int r = idx % nbp, c = idx / nbp;
+      if (r >= nb || c >= nb) Ts[c * LDT + r] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+    }
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done) : "r"(bar) : "memory");
   __syncthreads();
   if (!UNIT)
     for (int i = threadIdx.x; i < nbp; i += blockDim.x) dinv[i] = crcp(opT<CONJT>(Ts, i, i));

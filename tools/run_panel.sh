@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+python -m pytest tests -m gpu -x -q > gpurun_out/ptests.log 2>&1
+python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/pbench.log 2>&1
