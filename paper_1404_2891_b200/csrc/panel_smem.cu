@@ -32,7 +32,8 @@ namespace cg = cooperative_groups;
 namespace feast {
 namespace {
 
-constexpr int PT = 128;          // threads per CTA (one panel row each, S rows)
+constexpr int PT = 128;          // threads per CTA up to 256 rows (S = 1, 2 rows per thread); 2 * PT
+                                 // threads for 257..512 rows (four rows per thread spill registers)
 constexpr int CSM = 16;          // max cluster size
 constexpr int WMAX = 64;         // max panel width
 
@@ -59,6 +60,17 @@ __device__ __forceinline__ unsigned long long warp_max_key(unsigned long long k)
   const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
   const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
   return ((unsigned long long)mhi << 32) | mlo;
+}
+
+// 1/x for 1e-300 < x < 1e300: MUFU.RCP64H seed + two Newton steps (~1 ulp; __drcp_rn's correctly
+// rounded sequence costs ~400 cycles on the per-column critical path)
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
 }
 
 __device__ __forceinline__ bool better(double v, int i, double bv, int bi) {
@@ -92,12 +104,15 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 __device__ unsigned long long g_ptrace[512];
 #define PTRACE(i) do { if (blockIdx.x == 0 && threadIdx.x == 0 && k == 0) { unsigned long long t_; \
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_ptrace[(i)] = t_; } } while (0)
+__device__ unsigned long long g_ctrace[2][16];
+#define CT(i) do { if (ctr) { const long long t_ = clock64(); ct_[i] += t_ - ct_prev; ct_prev = t_; } } while (0)
 #else
 #define PTRACE(i) do {} while (0)
+#define CT(i) do {} while (0)
 #endif
 
-template <int S, int WC>
-__global__ void __launch_bounds__(PT, 1)
+template <int S, int WC, int NT>
+__global__ void __launch_bounds__(NT, 1)
 panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__ ipiv_all,
                   double* __restrict__ stats_all, int32_t* __restrict__ info_all) {
   cg::cluster_group cluster = cg::this_cluster();
@@ -124,12 +139,16 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
   __shared__ int pvt[WMAX];                      // pivot (panel row index) per column
   // per-warp candidates, double-buffered by column parity (a single-CTA "cluster" decides the
   // pivot straight from them: one __syncthreads per column, no DSMEM exchange)
-  __shared__ unsigned long long wkey[2][PT / 32];
-  __shared__ double2 wrow[2][PT / 32][WC + 1];
+  __shared__ __align__(16) unsigned long long wkey[2][NT / 32];
+  __shared__ double2 wrow[2][NT / 32][WC + 1];
   __shared__ __align__(8) unsigned long long mbar[4];   // slots[0], slots[1], U12s, load
   __shared__ int pos2row[WMAX], cur[WMAX];
 
   PTRACE(0);
+#ifdef FEAST_PANEL_TRACE
+  const bool ctr = blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == 96) && k == 0;
+  long long ct_[16] = {0}, ct_prev = clock64();
+#endif
   if (tid == 0) {
     mbar_init(saddr(&mbar[0]), 1);
     mbar_init(saddr(&mbar[1]), 1);
@@ -147,7 +166,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
   const bool tma = nrow > 0 && w > WC;
   if (tma) {
     if (tid == 0) mbar_arm(lbar, (uint32_t)((w - WC) * nrow * 16));
-    for (int c = WC + tid; c < w; c += PT) {
+    for (int c = WC + tid; c < w; c += NT) {
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                    ::"r"(saddr(P + (c - WC) * PLD)), "l"(C + rbeg + c * ld), "r"(nrow * 16), "r"(lbar) : "memory");
     }
@@ -158,13 +177,29 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
     const int wc0 = min(WC, w);
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-      const int r = tid + s * PT;
+      const int r = tid + s * NT;
 #pragma unroll
       for (int jj = 0; jj < WC; ++jj)
         a[s][jj] = (r < nrow && jj < wc0) ? C[rbeg + r + (int64_t)jj * ld] : make_double2(0.0, 0.0);
     }
   }
   cluster.sync();   // mbarrier inits visible cluster-wide before any remote st.async
+  // this thread's slot elements of the per-column push (fixed for the whole panel): element e of
+  // CTA dcta's slot [buf][crank] and dcta's mbarrier [buf], t = tid (+ NT) = dcta * (WC + 2) + e
+  static_assert(CSM * (WC + 2) <= 2 * NT, "push covers at most two elements per thread");
+  int push_e[2];
+  uint32_t push_slot[2][2], push_bar[2][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int t = h * NT + tid;
+    const int dcta = min(t / (WC + 2), CS - 1);
+    push_e[h] = t - (t / (WC + 2)) * (WC + 2);
+#pragma unroll
+    for (int bb = 0; bb < 2; ++bb) {
+      push_slot[h][bb] = mapa(saddr(&slots[bb][crank]), dcta) + push_e[h] * 16;
+      push_bar[h][bb] = mapa(saddr(&mbar[bb]), dcta);
+    }
+  }
   if (tma) mbar_wait(lbar, 0);
   PTRACE(1);
 
@@ -180,7 +215,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
     if (j0 > 0) {
 #pragma unroll
       for (int s = 0; s < S; ++s) {
-        const int r = tid + s * PT;
+        const int r = tid + s * NT;
 #pragma unroll
         for (int jj = 0; jj < WC; ++jj)
           a[s][jj] = (r < nrow && jj < wc) ? P[(j0 - WC + jj) * PLD + r] : make_double2(0.0, 0.0);
@@ -193,20 +228,23 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
       const int buf = col & 1;
       const uint32_t bar = saddr(&mbar[buf]);
       PTRACE(8 + 4 * col);
+      CT(0);
       if (tid == 0 && CS > 1) mbar_arm(bar, (uint32_t)(CS * SLOT_BYTES));
       unsigned long long bk = 0ull;
       int bs = -1;
 #pragma unroll
       for (int s = 0; s < S; ++s) {
-        const int r = tid + s * PT;
+        const int r = tid + s * NT;
         if (r < nrow && !used[s]) {
           const unsigned long long kk = make_key(cabs1(a[s][jj]), rbeg + r);
           if (kk > bk) { bk = kk; bs = s; }
         }
       }
+      CT(1);
       // warp argmax first (the REDUX issues before the reciprocal's dependent chain), then every
       // thread inverts its own candidate while the reduction is in flight
       const unsigned long long wk = warp_max_key(bk);
+      CT(2);
       double2 myrcp = make_double2(0.0, 0.0);
 #pragma unroll
       for (int s = 0; s < S; ++s)
@@ -215,13 +253,14 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
           if (pv.x != 0.0 || pv.y != 0.0) {
             const double m2 = fma(pv.x, pv.x, pv.y * pv.y);
             if (m2 > 1e-300 && m2 < 1e300) {       // 1/p = conj(p) / |p|^2, one reciprocal
-              const double d = __drcp_rn(m2);
+              const double d = fast_rcp(m2);
               myrcp = make_double2(pv.x * d, -pv.y * d);
             } else {
               myrcp = crcp(pv);                     // Smith's division at extreme magnitudes
             }
           }
         }
+      CT(3);
       // the warp's winning lane stages its chunk row and 1/pivot; one barrier for the CTA step
       if (wk != 0ull && bk == wk) {
 #pragma unroll
@@ -233,13 +272,20 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
           }
       }
       if (lane == 0) wkey[buf][warp] = wk;
+      CT(4);
       __syncthreads();
-      unsigned long long ck = wkey[buf][0];
+      CT(5);
+      // CTA argmax of the NT/32 warp keys (16-byte loads; keys are distinct or 0)
+      unsigned long long ck = 0ull;
       int cw = 0;
 #pragma unroll
-      for (int q = 1; q < PT / 32; ++q)
-        if (wkey[buf][q] > ck) { ck = wkey[buf][q]; cw = q; }
+      for (int q = 0; q < NT / 32; q += 2) {
+        const ulonglong2 kk = *reinterpret_cast<const ulonglong2*>(&wkey[buf][q]);
+        if (kk.x > ck) { ck = kk.x; cw = q; }
+        if (kk.y > ck) { ck = kk.y; cw = q + 1; }
+      }
       PTRACE(9 + 4 * col);
+      CT(6);
       unsigned long long gk;
       const double2* prow;
       double2 pinv;
@@ -250,17 +296,19 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
         pinv = wrow[buf][cw][WC];
       } else {
         // push {row[WC], key, 1/pivot} into slot [buf][crank] of every CTA (st.async -> its mbarrier)
-        for (int t = tid; t < CS * (WC + 2); t += PT) {
-          const int dcta = t / (WC + 2), e = t - dcta * (WC + 2);
-          const uint32_t rslot = mapa(saddr(&slots[buf][crank]), dcta);
-          const uint32_t rbar = mapa(bar, dcta);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h * NT + tid >= CS * (WC + 2)) break;
+          const int e = push_e[h];
           double2 v;
           if (e < WC) v = ck ? wrow[buf][cw][e] : make_double2(0.0, 0.0);
           else if (e == WC) v = make_double2(__longlong_as_double((long long)ck), 0.0);
           else v = ck ? wrow[buf][cw][WC] : make_double2(0.0, 0.0);
-          st_async16(rslot + e * 16, v, rbar);
+          st_async16(push_slot[h][buf], v, push_bar[h][buf]);
         }
+        CT(7);
         mbar_wait(bar, (uint32_t)((col >> 1) & 1));
+        CT(8);
         PTRACE(10 + 4 * col);
         // global pivot: lanes read the CS keys, 64-bit max by REDUX (every warp, same result)
         const unsigned long long lk = lane < CS ? slots[buf][lane].key : 0ull;
@@ -269,6 +317,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
         prow = slots[buf][gb].row;
         pinv = slots[buf][gb].pinv;
       }
+      CT(9);
       const int gi = key_row(gk);
       if (tid < WC) L11s[jj][tid] = prow[tid];
       if (tid == 0) pvt[col] = gi;
@@ -276,7 +325,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
       const bool pzero = (p.x == 0.0 && p.y == 0.0);
 #pragma unroll
       for (int s = 0; s < S; ++s) {
-        const int r = tid + s * PT;
+        const int r = tid + s * NT;
         if (r < nrow && !used[s]) {
           if (rbeg + r == gi) {
             used[s] = true;   // pivot row: its values are U (cols >= col) and L (cols < col)
@@ -288,6 +337,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
           }
         }
       }
+      CT(10);
       if (crank == 0 && tid == 0) {
         const double ap2 = fma(p.x, p.x, p.y * p.y);   // |p|^2; sqrt taken once at the end
         pmin = fmin(pmin, ap2);
@@ -298,7 +348,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
     // ---- chunk done: its columns are final (L multipliers; U for the pivot rows) -> global
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-      const int r = tid + s * PT;
+      const int r = tid + s * NT;
       if (r < nrow) {
 #pragma unroll
         for (int jj = 0; jj < WC; ++jj)
@@ -316,7 +366,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
       for (int jj = 0; jj < wc; ++jj) {
         const int pr = pvt[j0 + jj] - rbeg;
         if (pr >= 0 && pr < nrow) {
-          for (int idx = tid; idx < rem * CS; idx += PT) {
+          for (int idx = tid; idx < rem * CS; idx += NT) {
             const int dcta = idx / rem, c = idx - dcta * rem;
             if (CS == 1) U12s[jj][c] = P[(c1 - WC + c) * PLD + pr];
             else st_async16(mapa(saddr(&U12s[jj][c]), dcta), P[(c1 - WC + c) * PLD + pr], mapa(ubar, dcta));
@@ -328,7 +378,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
       else mbar_wait(ubar, (uint32_t)(chunk & 1));
       PTRACE(301 + 4 * chunk);
       // U12 = L11^-1 (pivot rows), unit lower L11 (chunk multipliers of the pivot rows)
-      for (int c = tid; c < rem; c += PT) {
+      for (int c = tid; c < rem; c += NT) {
         double2 u[WC];
 #pragma unroll
         for (int jj = 0; jj < WC; ++jj) {
@@ -347,27 +397,29 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
       for (int jj = 0; jj < wc; ++jj) {
         const int pr = pvt[j0 + jj] - rbeg;
         if (pr >= 0 && pr < nrow)
-          for (int c = tid; c < rem; c += PT) P[(c1 - WC + c) * PLD + pr] = U12s[jj][c];
+          for (int c = tid; c < rem; c += NT) P[(c1 - WC + c) * PLD + pr] = U12s[jj][c];
       }
 #pragma unroll
       for (int s = 0; s < S; ++s) {
-        const int r = tid + s * PT;
+        const int r = tid + s * NT;
         if (r < nrow && !used[s]) {
           double2* colp = P + (c1 - WC) * PLD + r;
           int c = 0;
-          // 8 independent accumulation chains per pass (ILP: one warp per SM sub-partition)
-          for (; c + 8 <= rem; c += 8) {
-            double2 v[8];
+          // CH independent accumulation chains per pass (ILP: one warp per SM sub-partition); 4 at
+          // four rows per thread, where the chunk registers already take 128 of the 255
+          constexpr int CH = S >= 4 ? 4 : 8;
+          for (; c + CH <= rem; c += CH) {
+            double2 v[CH];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) v[e] = colp[(c + e) * PLD];
+            for (int e = 0; e < CH; ++e) v[e] = colp[(c + e) * PLD];
 #pragma unroll
             for (int jj = 0; jj < WC; ++jj)
               if (jj < wc) {
 #pragma unroll
-                for (int e = 0; e < 8; ++e) v[e] = cfms(v[e], a[s][jj], U12s[jj][c + e]);
+                for (int e = 0; e < CH; ++e) v[e] = cfms(v[e], a[s][jj], U12s[jj][c + e]);
               }
 #pragma unroll
-            for (int e = 0; e < 8; ++e) colp[(c + e) * PLD] = v[e];
+            for (int e = 0; e < CH; ++e) colp[(c + e) * PLD] = v[e];
           }
           for (; c + 4 <= rem; c += 4) {
             double2 v0 = colp[(c + 0) * PLD], v1 = colp[(c + 1) * PLD], v2 = colp[(c + 2) * PLD], v3 = colp[(c + 3) * PLD];
@@ -396,6 +448,10 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
     }
   }
   PTRACE(2);
+#ifdef FEAST_PANEL_TRACE
+  if (ctr)
+    for (int i = 0; i < 16; ++i) g_ctrace[threadIdx.x == 0 ? 0 : 1][i] = (unsigned long long)ct_[i];
+#endif
   // ---- LAPACK ipiv from the pivot sequence (rows / positions relative to k)
   if (crank == 0 && tid == 0) {
     for (int i = 0; i < w; ++i) { pos2row[i] = i; cur[i] = i; }
@@ -419,7 +475,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
   // st.async that this CTA waited for (the last column's slots), so it may exit.
 }
 
-template <int S, int WC>
+template <int S, int WC, int NT>
 void launch_s(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info, int batch, int cs,
               cudaStream_t s) {
   const int64_t L = n - k;
@@ -427,13 +483,13 @@ void launch_s(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* sta
   const size_t smem = (size_t)Lc * (w > WC ? w - WC : 0) * sizeof(double2);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(panel_smem_kernel<S, WC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(panel_smem_kernel<S, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(panel_smem_kernel<S, WC, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(panel_smem_kernel<S, WC, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(batch * cs), 1, 1);
-  cfg.blockDim = dim3(PT, 1, 1);
+  cfg.blockDim = dim3(NT, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -443,7 +499,7 @@ void launch_s(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* sta
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, panel_smem_kernel<S, WC>, C, n, k, w, ipiv, stats, info);
+  cudaLaunchKernelEx(&cfg, panel_smem_kernel<S, WC, NT>, C, n, k, w, ipiv, stats, info);
   count_launch();
 }
 
@@ -451,6 +507,7 @@ void launch_s(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* sta
 
 #ifdef FEAST_PANEL_TRACE
 void panel_trace_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_ptrace, sizeof(g_ptrace)); }
+void panel_ctrace_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_ctrace, sizeof(g_ctrace)); }
 #endif
 
 // Diagnostics: how many clusters of `cs` CTAs with the panel of L rows x w columns can be
@@ -459,7 +516,7 @@ int panel_smem_max_clusters(int64_t L, int w, int cs) {
   const int Lc = (int)((L + cs - 1) / cs);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(16 * cs), 1, 1);
-  cfg.blockDim = dim3(PT, 1, 1);
+  cfg.blockDim = dim3(Lc <= 2 * PT ? PT : 2 * PT, 1, 1);
   const int wc = 8;
   cfg.dynamicSmemBytes = (size_t)Lc * (w > wc ? w - wc : 0) * sizeof(double2);
   cudaLaunchAttribute attr[1];
@@ -470,7 +527,7 @@ int panel_smem_max_clusters(int64_t L, int w, int cs) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int nc = -1;
-  auto k = Lc <= PT ? panel_smem_kernel<1, 8> : (Lc <= 2 * PT ? panel_smem_kernel<2, 8> : panel_smem_kernel<4, 8>);
+  auto k = Lc <= PT ? panel_smem_kernel<1, 8, PT> : (Lc <= 2 * PT ? panel_smem_kernel<2, 8, PT> : panel_smem_kernel<2, 8, 2 * PT>);
   cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (cudaOccupancyMaxActiveClusters(&nc, k, &cfg) != cudaSuccess) { cudaGetLastError(); return -1; }
@@ -496,9 +553,9 @@ void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, do
   while (cs > 1 && (n - k + cs / 2 - 1) / (cs / 2) <= rowcap) cs /= 2;
   const int64_t Lc = (n - k + cs - 1) / cs;
   // register chunk: 8 columns (a 16-column chunk spills at 2 rows per thread)
-  if (Lc <= PT) launch_s<1, 8>(C, n, k, w, ipiv, stats, info, batch, cs, s);
-  else if (Lc <= 2 * PT) launch_s<2, 8>(C, n, k, w, ipiv, stats, info, batch, cs, s);
-  else launch_s<4, 8>(C, n, k, w, ipiv, stats, info, batch, cs, s);
+  if (Lc <= PT) launch_s<1, 8, PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);
+  else if (Lc <= 2 * PT) launch_s<2, 8, PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);
+  else launch_s<2, 8, 2 * PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);   // 512 rows: 256 threads x 2
 }
 
 }  // namespace feast

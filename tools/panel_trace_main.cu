@@ -5,7 +5,7 @@
 #include <cuda_runtime.h>
 #include "kernels.h"
 #ifndef NO_TRACE_READ
-namespace feast { void panel_trace_read(unsigned long long* out); }
+namespace feast { void panel_trace_read(unsigned long long* out); void panel_ctrace_read(unsigned long long* out); }
 #else
 namespace feast { inline void panel_trace_read(unsigned long long*) {} }
 #endif
@@ -40,4 +40,13 @@ int main(int argc, char** argv) {
     printf("\n");
   }
   printf("end loop %.2f  end %.2f\n", us(2), us(3));
+  unsigned long long ct[2][16];
+  feast::panel_ctrace_read(&ct[0][0]);
+  const char* nm[11] = {"chunk-end/loop", "key search", "warp REDUX", "rcp", "stage wrow", "syncthreads",
+                        "CTA argmax", "push", "mbar wait", "global pick", "rank-1 update"};
+  for (int t = 0; t < 2; ++t) {
+    printf("thread %s cycles per column:", t ? "96" : "0");
+    for (int i = 0; i < 11; ++i) printf(" %s %.0f |", nm[i], ct[t][i] / (double)W);
+    printf("\n");
+  }
 }
