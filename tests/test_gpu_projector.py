@@ -425,10 +425,13 @@ def test_ragged_sizes_across_panel_paths(n, m0):
     assert rel(Q, oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
 
 
-def test_register_panel_height_spectral():
-    """n = 4200 > 16 x 256: the first panels take the register-chunk kernel, later ones the
-    shared-memory cluster kernel; checked with the spectral identity (closed-form filter)."""
-    P = synth.make_pencil_torch("C2", n=4200, m0=16)
+@pytest.mark.parametrize("n", [4200, 8400])
+def test_register_panel_height_spectral(n):
+    """Tall panels: n = 4200 > 16 x 256 rows starts on the 256-thread shared-memory cluster
+    kernel (two rows per thread, 263 rows per CTA); n = 8400 > 16 x 512 on the register-chunk
+    kernel, both handing over to the 128-thread kernels as L = n - k falls; checked with the
+    spectral identity (closed-form filter)."""
+    P = synth.make_pencil_torch("C2", n=n, m0=16)
     s = P.spec
     f = _handle(P)
     Q = f.project(P.A, P.B, P.X0)
