@@ -245,31 +245,32 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
       // thread inverts its own candidate while the reduction is in flight
       const unsigned long long wk = warp_max_key(bk);
       CT(2);
-      double2 myrcp = make_double2(0.0, 0.0);
+      // the candidate value by predicated selects (no divergent branch per row slot), then ONE
+      // reciprocal chain per lane: 1/p = conj(p) / |p|^2
+      double2 pv = make_double2(0.0, 0.0);
 #pragma unroll
       for (int s = 0; s < S; ++s)
-        if (s == bs) {
-          const double2 pv = a[s][jj];
-          if (pv.x != 0.0 || pv.y != 0.0) {
-            const double m2 = fma(pv.x, pv.x, pv.y * pv.y);
-            if (m2 > 1e-300 && m2 < 1e300) {       // 1/p = conj(p) / |p|^2, one reciprocal
-              const double d = fast_rcp(m2);
-              myrcp = make_double2(pv.x * d, -pv.y * d);
-            } else {
-              myrcp = crcp(pv);                     // Smith's division at extreme magnitudes
-            }
-          }
-        }
+        if (s == bs) pv = a[s][jj];
+      const double m2 = fma(pv.x, pv.x, pv.y * pv.y);
+      double2 myrcp;
+      if (m2 > 1e-300 && m2 < 1e300) {
+        const double d = fast_rcp(m2);
+        myrcp = make_double2(pv.x * d, -pv.y * d);
+      } else {
+        myrcp = (pv.x != 0.0 || pv.y != 0.0) ? crcp(pv) : make_double2(0.0, 0.0);   // extreme magnitudes
+      }
       CT(3);
       // the warp's winning lane stages its chunk row and 1/pivot; one barrier for the CTA step
       if (wk != 0ull && bk == wk) {
 #pragma unroll
-        for (int s = 0; s < S; ++s)
-          if (s == bs) {
+        for (int q = 0; q < WC; ++q) {
+          double2 v = a[0][q];
 #pragma unroll
-            for (int q = 0; q < WC; ++q) wrow[buf][warp][q] = a[s][q];
-            wrow[buf][warp][WC] = myrcp;
-          }
+          for (int s = 1; s < S; ++s)
+            if (s == bs) v = a[s][q];
+          wrow[buf][warp][q] = v;
+        }
+        wrow[buf][warp][WC] = myrcp;
       }
       if (lane == 0) wkey[buf][warp] = wk;
       CT(4);
