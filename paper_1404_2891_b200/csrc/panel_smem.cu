@@ -356,6 +356,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
           if (jj < wc) C[rbeg + r + (int64_t)(j0 + jj) * ld] = a[s][jj];
       }
     }
+    CT(11);
     const int c1 = j0 + wc;
     if (c1 < w) {
       const int rem = w - c1;
@@ -377,6 +378,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
       PTRACE(300 + 4 * chunk);
       if (CS == 1) __syncthreads();
       else mbar_wait(ubar, (uint32_t)(chunk & 1));
+      CT(12);
       PTRACE(301 + 4 * chunk);
       // U12 = L11^-1 (pivot rows), unit lower L11 (chunk multipliers of the pivot rows)
       for (int c = tid; c < rem; c += NT) {
@@ -394,56 +396,66 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
       }
       PTRACE(303 + 4 * chunk);
       __syncthreads();
+      CT(13);
       // pivot rows of this chunk take their U12 values; other rows get the rank-wc update
       for (int jj = 0; jj < wc; ++jj) {
         const int pr = pvt[j0 + jj] - rbeg;
         if (pr >= 0 && pr < nrow)
           for (int c = tid; c < rem; c += NT) P[(c1 - WC + c) * PLD + pr] = U12s[jj][c];
       }
+      // rank-wc update of this thread's S rows, all rows in one pass: each U12 value (a
+      // shared-memory broadcast) feeds S rows, and S x 8 independent accumulation chains keep
+      // the FP64 pipe busy with one warp per SM sub-partition.  Pivot rows (used) and rows past
+      // nrow are computed on zeros and not stored.
+      {
+        bool act[S];
+        int rr[S];
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
-        const int r = tid + s * NT;
-        if (r < nrow && !used[s]) {
-          double2* colp = P + (c1 - WC) * PLD + r;
-          int c = 0;
-          // CH independent accumulation chains per pass (ILP: one warp per SM sub-partition); 4 at
-          // four rows per thread, where the chunk registers already take 128 of the 255
-          constexpr int CH = S >= 4 ? 4 : 8;
-          for (; c + CH <= rem; c += CH) {
-            double2 v[CH];
+        for (int s = 0; s < S; ++s) {
+          rr[s] = tid + s * NT;
+          act[s] = rr[s] < nrow && !used[s];
+        }
+        double2* colp = P + (c1 - WC) * PLD;
+        constexpr int CH = 8;
+        int c = 0;
+        for (; c + CH <= rem; c += CH) {
+          double2 v[S][CH];
 #pragma unroll
-            for (int e = 0; e < CH; ++e) v[e] = colp[(c + e) * PLD];
+          for (int s = 0; s < S; ++s)
 #pragma unroll
-            for (int jj = 0; jj < WC; ++jj)
-              if (jj < wc) {
+            for (int e = 0; e < CH; ++e) v[s][e] = act[s] ? colp[(c + e) * PLD + rr[s]] : make_double2(0.0, 0.0);
 #pragma unroll
-                for (int e = 0; e < CH; ++e) v[e] = cfms(v[e], a[s][jj], U12s[jj][c + e]);
+          for (int jj = 0; jj < WC; ++jj)
+            if (jj < wc) {
+#pragma unroll
+              for (int e = 0; e < CH; ++e) {
+                const double2 u = U12s[jj][c + e];
+#pragma unroll
+                for (int s = 0; s < S; ++s) v[s][e] = cfms(v[s][e], a[s][jj], u);
               }
+            }
 #pragma unroll
-            for (int e = 0; e < CH; ++e) colp[(c + e) * PLD] = v[e];
-          }
-          for (; c + 4 <= rem; c += 4) {
-            double2 v0 = colp[(c + 0) * PLD], v1 = colp[(c + 1) * PLD], v2 = colp[(c + 2) * PLD], v3 = colp[(c + 3) * PLD];
+          for (int s = 0; s < S; ++s)
+            if (act[s]) {
 #pragma unroll
-            for (int jj = 0; jj < WC; ++jj)
-              if (jj < wc) {
-                v0 = cfms(v0, a[s][jj], U12s[jj][c + 0]);
-                v1 = cfms(v1, a[s][jj], U12s[jj][c + 1]);
-                v2 = cfms(v2, a[s][jj], U12s[jj][c + 2]);
-                v3 = cfms(v3, a[s][jj], U12s[jj][c + 3]);
-              }
-            colp[(c + 0) * PLD] = v0; colp[(c + 1) * PLD] = v1; colp[(c + 2) * PLD] = v2; colp[(c + 3) * PLD] = v3;
-          }
-          for (; c < rem; ++c) {
-            double2 v = colp[c * PLD];
+              for (int e = 0; e < CH; ++e) colp[(c + e) * PLD + rr[s]] = v[s][e];
+            }
+        }
+        for (; c < rem; ++c) {
 #pragma unroll
-            for (int jj = 0; jj < WC; ++jj)
-              if (jj < wc) v = cfms(v, a[s][jj], U12s[jj][c]);
-            colp[c * PLD] = v;
-          }
+          for (int s = 0; s < S; ++s)
+            if (act[s]) {
+              double2 v = colp[c * PLD + rr[s]];
+#pragma unroll
+              for (int jj = 0; jj < WC; ++jj)
+                if (jj < wc) v = cfms(v, a[s][jj], U12s[jj][c]);
+              colp[c * PLD + rr[s]] = v;
+            }
         }
       }
+      CT(14);
       __syncthreads();
+      CT(15);
       PTRACE(302 + 4 * chunk);
       if (chunk == 0) PTRACE(400);
     }

@@ -42,11 +42,12 @@ int main(int argc, char** argv) {
   printf("end loop %.2f  end %.2f\n", us(2), us(3));
   unsigned long long ct[2][16];
   feast::panel_ctrace_read(&ct[0][0]);
-  const char* nm[11] = {"chunk-end/loop", "key search", "warp REDUX", "rcp", "stage wrow", "syncthreads",
-                        "CTA argmax", "push", "mbar wait", "global pick", "rank-1 update"};
+  const char* nm[16] = {"loop top", "key search", "warp REDUX", "rcp", "stage wrow", "syncthreads",
+                        "CTA argmax", "push", "mbar wait", "global pick", "rank-1 update", "chunk store",
+                        "U12 push+wait", "U12 solve+sync", "rank-8 update", "final sync"};
   for (int t = 0; t < 2; ++t) {
     printf("thread %s cycles per column:", t ? "96" : "0");
-    for (int i = 0; i < 11; ++i) printf(" %s %.0f |", nm[i], ct[t][i] / (double)W);
+    for (int i = 0; i < 16; ++i) printf(" %s %.0f |", nm[i], ct[t][i] / (double)W);
     printf("\n");
   }
 }
