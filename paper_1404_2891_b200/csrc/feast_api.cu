@@ -392,8 +392,17 @@ bool smem_panel_for(const feast_ctx* h, int64_t k) {
   return h->smem_cs_max > 0 && (h->n - k + h->smem_cs_max - 1) / h->smem_cs_max <= 256;
 }
 
+// Timing ablation (FEAST_ABLATE, never for results): bit 1 skips the panels (identity pivots),
+// bit 2 the triangular kernels, bit 4 the row swaps — to measure each class's marginal cost in
+// the overlapped schedule.
+int ablate() {
+  static const int a = [] { const char* e = getenv("FEAST_ABLATE"); return e ? atoi(e) : 0; }();
+  return a;
+}
+
 void panel_at(feast_ctx* h, const Lu& v, int64_t k, int w, cudaStream_t s) {
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr);
+  if (ablate() & 1) { feast::ipiv_identity_launch(v.ipiv, n, k, w, v.nbat, s); return; }
   if (smem_panel_for(h, k))
     feast::panel_smem_launch(bat(v.Cw, ld, st), n, k, w, v.ipiv, v.stats, v.info, v.nbat, h->smem_cs_max, s);
   else
@@ -427,14 +436,14 @@ void factor_block(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, cudaStream_
       const int wpp = (int)std::min<int64_t>(wp, ki + wi - kp);
       panel_at(h, v, kp, wpp, s);
       if (smem) {
-        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, K0 + Wo, nbat, s, h->laswp_perm);
+        if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, K0 + Wo, nbat, s, h->laswp_perm);
       } else {   // the register-chunk panel already swapped its own columns
-        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, kp, nbat, s, h->laswp_perm);
-        feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, kp + wpp, K0 + Wo, nbat, s, h->laswp_perm);
+        if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, kp, nbat, s, h->laswp_perm);
+        if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, kp + wpp, K0 + Wo, nbat, s, h->laswp_perm);
       }
       const int64_t cp = kp + wpp, remb = ki + wi - cp;
       if (remb > 0) {
-        feast::trsm_launch(bat(C + kp + kp * ld, ld, st), bat(C + kp + cp * ld, ld, st), wpp, remb, true, true, false,
+        if (!(ablate() & 2)) feast::trsm_launch(bat(C + kp + kp * ld, ld, st), bat(C + kp + cp * ld, ld, st), wpp, remb, true, true, false,
                            nbat, s);
         ZgemmArgs p{n - cp, remb, wpp, C + cp + kp * ld, ld, st, C + kp + cp * ld, ld, st, C + cp + cp * ld, ld, st,
                     make_double2(-1, 0), make_double2(1, 0), nbat};
@@ -450,10 +459,10 @@ void factor_block(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, cudaStream_
       cudaStreamWaitEvent(v.sx, v.ev_t, 0);
       st_inv = v.sx;
     }
-    feast::trtri_launch(bat(C, ld, st), n, ki / 64, 1, v.Inv, h->inv_stride, 2, nbat, st_inv);
+    if (!(ablate() & 2)) feast::trtri_launch(bat(C, ld, st), n, ki / 64, 1, v.Inv, h->inv_stride, 2, nbat, st_inv);
     if (rem > 0) {
       // in-block U12 = L11^-1 A12 (warp TRSM on the chain), then A22 -= L21 U12 (DMMA)
-      feast::trsm_launch(bat(C + ki + ki * ld, ld, st), bat(C + ki + c1 * ld, ld, st), wi, rem, true, true, false,
+      if (!(ablate() & 2)) feast::trsm_launch(bat(C + ki + ki * ld, ld, st), bat(C + ki + c1 * ld, ld, st), wi, rem, true, true, false,
                          nbat, s);
       ZgemmArgs p{n - c1, rem, wi, C + c1 + ki * ld, ld, st, C + ki + c1 * ld, ld, st, C + c1 + c1 * ld, ld, st,
                   make_double2(-1, 0), make_double2(1, 0), nbat};
@@ -512,7 +521,7 @@ void lu_batched(feast_ctx* h, const Lu& v, int64_t aug, const std::function<void
     factor_block(h, v, 0, Wo, sm);
   }
   if (v.ev_first) cudaEventRecord(v.ev_first, sm);   // releases the next (staggered) group
-  feast::laswp_launch(bat(C, ld, st), n, 0, (int)Wo, v.ipiv, Wo, ntot, nbat, sm, h->laswp_perm);
+  if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, 0, (int)Wo, v.ipiv, Wo, ntot, nbat, sm, h->laswp_perm);
   for (int64_t K0 = 0; K0 < n; K0 += Wo, Wo = std::min<int64_t>(NBO, n - K0)) {
     const int64_t K1 = K0 + Wo;
     if (K1 >= n) {
@@ -533,8 +542,8 @@ void lu_batched(feast_ctx* h, const Lu& v, int64_t aug, const std::function<void
       factor_block(h, v, K1, Wo1, sm);
     }
     // block K1's swaps on every column outside it
-    feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, 0, K1, nbat, sm, h->laswp_perm);
-    feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, K1 + Wo1, ntot, nbat, sm, h->laswp_perm);
+    if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, 0, K1, nbat, sm, h->laswp_perm);
+    if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, K1 + Wo1, ntot, nbat, sm, h->laswp_perm);
   }
 }
 
@@ -828,7 +837,7 @@ int project_impl(feast_ctx* h, const double2* A, int64_t lda, const double2* B, 
     if (inf[u] || ratio < 1e-14) singular = true;
     else if (ratio < 1e-10) ill = true;
   }
-  if (singular) {
+  if (singular && !(ablate() & 1)) {   // (a timing ablation has no pivots to judge)
     char b[64];
     snprintf(b, sizeof b, "%d", h->worst);
     return fail(h, FEAST_E_SINGULAR, "shifted matrix at node %s is singular (pivot ratio < 1e-14)", b);

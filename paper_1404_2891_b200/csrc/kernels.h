@@ -63,6 +63,7 @@ void trsm_launch(Batched T, Batched X, int nb, int64_t ncols, bool lower_op, boo
 // which: 0 = L only, 1 = U only, 2 = both.
 void trtri_launch(Batched C, int64_t n, int64_t kb0, int64_t nblocks, double2* inv, int64_t inv_node_stride, int which,
                   int batch, cudaStream_t s);
+void ipiv_identity_launch(int32_t* ipiv, int64_t n, int64_t k, int w, int batch, cudaStream_t s);
 void stats_init_launch(double* stats, int32_t* info, int batch, cudaStream_t s);
 // perm_b from ipiv_b (sequential swaps of rows 0..n-1); iperm (optional) = inverse permutation
 void perm_launch(const int32_t* ipiv, int32_t* perm, int32_t* iperm, int64_t n, int batch, cudaStream_t s);

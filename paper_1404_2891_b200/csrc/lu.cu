@@ -346,6 +346,17 @@ void panel_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double*
   else if (cfg.W == 4 && cfg.S == 8) panel_launch_t<4, 8>(C, n, k, w, ipiv, stats, info, batch, cfg.cluster, s);
 }
 
+// timing ablation only (FEAST_ABLATE bit 1): identity pivots in place of a skipped panel
+__global__ void ipiv_identity_kernel(int32_t* ipiv, int64_t n, int64_t k, int w, int batch) {
+  const int b = blockIdx.x, i = threadIdx.x;
+  if (b < batch && i < w) ipiv[(int64_t)b * n + k + i] = (int32_t)(k + i);
+}
+
+void ipiv_identity_launch(int32_t* ipiv, int64_t n, int64_t k, int w, int batch, cudaStream_t s) {
+  ipiv_identity_kernel<<<batch, 64, 0, s>>>(ipiv, n, k, w, batch);
+  count_launch();
+}
+
 __global__ void stats_init_kernel(double* stats, int32_t* info, int batch) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < batch) { stats[2 * b] = DBL_MAX; stats[2 * b + 1] = 0.0; info[b] = 0; }
