@@ -20,7 +20,6 @@
 namespace feast {
 namespace {
 
-constexpr int BK = 16;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -46,7 +45,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 //   accumulators: C[g][2t + i], i = 0, 1 (re and im in separate registers).
 // Shared layout: As[k][m] with ld BM + 2 (quarter-warp rows 32 B apart: conflict-free 128-bit
 // loads), Bs[n][k] with ld BK + 4.
-template <int BM, int BN, int WGM, int WGN, int ST>
+template <int BM, int BN, int WGM, int WGN, int ST, int BK>
 struct Tile {
   static constexpr int THREADS = 32 * WGM * WGN;
   static constexpr int TM = BM / WGM, TN = BN / WGN;
@@ -57,9 +56,9 @@ struct Tile {
   static constexpr size_t SMEM_BYTES = (size_t)ST * (A_STAGE + B_STAGE) * sizeof(double2);
 };
 
-template <int BM, int BN, int WGM, int WGN, int ST, int MINB, bool CONJA, int MODE>
+template <int BM, int BN, int WGM, int WGN, int ST, int MINB, bool CONJA, int MODE, bool PREC = true, int BK = 16>
 __global__ void __launch_bounds__(32 * WGM * WGN, MINB) zgemm_dmma_kernel(ZgemmArgs p) {
-  using T = Tile<BM, BN, WGM, WGN, ST>;
+  using T = Tile<BM, BN, WGM, WGN, ST, BK>;
   constexpr int THREADS = T::THREADS, LDA_S = T::LDA_S, LDB3 = T::LDB_S, A_STAGE = T::A_STAGE,
                 B_STAGE = T::B_STAGE;
   constexpr int MI = T::MI, NJ = T::NJ;
@@ -138,7 +137,8 @@ __global__ void __launch_bounds__(32 * WGM * WGN, MINB) zgemm_dmma_kernel(ZgemmA
   // mode C_old is prefetched into registers here, so its latency overlaps the pipeline fill and
   // no DMMA waits on it.
   double cre[MI][NJ][2], cim[MI][NJ][2];
-  double2 cold[MODE == ZG_SUB ? MI : 1][MODE == ZG_SUB ? NJ : 1][2];
+  constexpr bool PRE = MODE == ZG_SUB && PREC;   // C_old prefetched into registers
+  double2 cold[PRE ? MI : 1][PRE ? NJ : 1][2];
 #pragma unroll
   for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(32 * WGM * WGN, MINB) zgemm_dmma_kernel(ZgemmA
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         cre[mi][nj][i] = cim[mi][nj][i] = 0.0;
-        if (MODE == ZG_SUB) {
+        if (PRE) {
           const int64_t r = m0 + wm + mi * 8 + g, c = n0 + wn + nj * 8 + 2 * t + i;
           cold[mi][nj][i] = (r < M && c < N) ? C[r + c * p.ldc] : make_double2(0.0, 0.0);
         }
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(32 * WGM * WGN, MINB) zgemm_dmma_kernel(ZgemmA
           double2* cp = C + r + c * p.ldc;
           double2 v = make_double2(cre[mi][nj][i], cim[mi][nj][i]);
           if (MODE == ZG_SUB) {
-            v = cadd(cold[MODE == ZG_SUB ? mi : 0][MODE == ZG_SUB ? nj : 0][i], v);
+            v = cadd(PRE ? cold[PRE ? mi : 0][PRE ? nj : 0][i] : *cp, v);
           } else {
             v = cmul(p.alpha, v);
             if (use_beta) v = cadd(v, cmul(p.beta, *cp));
@@ -224,10 +224,10 @@ __global__ void __launch_bounds__(32 * WGM * WGN, MINB) zgemm_dmma_kernel(ZgemmA
         }
       }
 }
-template <int BM, int BN, int WGM, int WGN, int ST, int MINB, bool CONJA, int MODE>
+template <int BM, int BN, int WGM, int WGN, int ST, int MINB, bool CONJA, int MODE, bool PREC = true, int BK = 16>
 void launch3(const ZgemmArgs& p, cudaStream_t s) {
-  using T = Tile<BM, BN, WGM, WGN, ST>;
-  auto kern = zgemm_dmma_kernel<BM, BN, WGM, WGN, ST, MINB, CONJA, MODE>;
+  using T = Tile<BM, BN, WGM, WGN, ST, BK>;
+  auto kern = zgemm_dmma_kernel<BM, BN, WGM, WGN, ST, MINB, CONJA, MODE, PREC, BK>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_BYTES);
@@ -254,6 +254,8 @@ void launch_variant(const ZgemmArgs& p, int v, cudaStream_t s) {
     case 3: launch3<32, 32, 2, 2, 3, 4, CONJA, MODE>(p, s); break;
     case 4: launch3<128, 64, 4, 2, 3, 1, CONJA, MODE>(p, s); break;
     case 5: launch3<32, 64, 2, 2, 4, 2, CONJA, MODE>(p, s); break;
+    case 6: launch3<32, 32, 2, 2, 3, 2, CONJA, MODE, true, 32>(p, s); break;   // BK = 32
+    case 7: launch3<32, 32, 2, 2, 4, 3, CONJA, MODE, false>(p, s); break;      // C_old read in the epilogue
     default: launch_t<CONJA, MODE>(p, s); break;
   }
 }
