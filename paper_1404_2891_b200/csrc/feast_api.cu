@@ -499,34 +499,54 @@ void outer_update(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, int64_t c0,
   }
 }
 
-// rest(s): enqueues the formation of the columns beyond the first outer block on stream s
-void lu_batched(feast_ctx* h, const Lu& v, int64_t aug, const std::function<void(cudaStream_t)>& rest = nullptr) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), ntot = n + aug;
-  double2* C = v.Cw;
-  const int nbat = v.nbat;
-  cudaStream_t sm = v.sm, sp = v.sp;
-  const int64_t NBO = h->nbo;
-  int64_t Wo = std::min<int64_t>(NBO, n);
-  if (rest && h->lookahead && !h->prof_serial && Wo < n) {
-    // the first block is factored on the high-priority side stream while the main stream forms
-    // the rest of [C_j | R] (HBM-bound, needed only once the block is done)
-    cudaEventRecord(v.ev_a, sm);
-    cudaStreamWaitEvent(sp, v.ev_a, 0);
-    factor_block(h, v, 0, Wo, sp);
-    cudaEventRecord(v.ev_p, sp);
-    rest(sm);
-    cudaStreamWaitEvent(sm, v.ev_p, 0);
-  } else {
-    if (rest) rest(sm);
-    factor_block(h, v, 0, Wo, sm);
-  }
-  if (v.ev_first) cudaEventRecord(v.ev_first, sm);   // releases the next (staggered) group
-  if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, 0, (int)Wo, v.ipiv, Wo, ntot, nbat, sm, h->laswp_perm);
-  for (int64_t K0 = 0; K0 < n; K0 += Wo, Wo = std::min<int64_t>(NBO, n - K0)) {
+// The batched LU as a resumable sequence: step() enqueues the first outer block (and, with
+// rest(s), the formation of the remaining columns of [C_j | R] on stream s underneath it), then
+// one outer block per call; it returns true once the factorisation is fully enqueued.  The node
+// groups' sequences are enqueued round-robin, block by block (project_enqueue), so the groups
+// progress together instead of group 0 running ahead and the last group's latency-bound tail
+// finishing alone.
+struct LuRun {
+  feast_ctx* h;
+  Lu v;
+  int64_t aug;
+  std::function<void(cudaStream_t)> rest;
+  int phase = 0;          // 0: not started, 1: outer blocks, 2: done
+  int64_t K0 = 0, Wo = 0;
+
+  bool step() {
+    const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), ntot = n + aug;
+    double2* C = v.Cw;
+    const int nbat = v.nbat;
+    cudaStream_t sm = v.sm, sp = v.sp;
+    const int64_t NBO = h->nbo;
+    if (phase == 2) return true;
+    if (phase == 0) {
+      Wo = std::min<int64_t>(NBO, n);
+      if (rest && h->lookahead && !h->prof_serial && Wo < n) {
+        // the first block is factored on the high-priority side stream while the main stream
+        // forms the rest of [C_j | R] (HBM-bound, needed only once the block is done)
+        cudaEventRecord(v.ev_a, sm);
+        cudaStreamWaitEvent(sp, v.ev_a, 0);
+        factor_block(h, v, 0, Wo, sp);
+        cudaEventRecord(v.ev_p, sp);
+        rest(sm);
+        cudaStreamWaitEvent(sm, v.ev_p, 0);
+      } else {
+        if (rest) rest(sm);
+        factor_block(h, v, 0, Wo, sm);
+      }
+      if (v.ev_first) cudaEventRecord(v.ev_first, sm);   // releases the next (staggered) group
+      if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, 0, (int)Wo, v.ipiv, Wo, ntot, nbat, sm, h->laswp_perm);
+      phase = 1;
+      K0 = 0;
+      return false;
+    }
+    if (K0 >= n) { phase = 2; return true; }
     const int64_t K1 = K0 + Wo;
     if (K1 >= n) {
       outer_update(h, v, K0, Wo, n, aug, sm);      // last block: augmented columns only
-      break;
+      phase = 2;
+      return true;
     }
     const int64_t Wo1 = std::min<int64_t>(NBO, n - K1);
     outer_update(h, v, K0, Wo, K1, Wo1, sm);       // next block's columns first
@@ -544,6 +564,15 @@ void lu_batched(feast_ctx* h, const Lu& v, int64_t aug, const std::function<void
     // block K1's swaps on every column outside it
     if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, 0, K1, nbat, sm, h->laswp_perm);
     if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, K1 + Wo1, ntot, nbat, sm, h->laswp_perm);
+    K0 = K1;
+    Wo = Wo1;
+    return false;
+  }
+};
+
+void lu_batched(feast_ctx* h, const Lu& v, int64_t aug, const std::function<void(cudaStream_t)>& rest = nullptr) {
+  LuRun r{h, v, aug, rest};
+  while (!r.step()) {
   }
 }
 
@@ -680,6 +709,9 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
     // split the batch into G concurrent groups (group 0 on the handle's stream)
     const int G = (h->group_streams && !h->prof_serial) ? std::max(1, std::min(h->groups, nbat)) : 1;
     if (G > 1) cudaEventRecord(h->ev_fork, h->stream);
+    // pass 1: per group, the fork, the shift of the first outer block and the LU sequence object
+    std::vector<Lu> vs;
+    std::vector<LuRun> runs;
     for (int g = 0; g < G; ++g) {
       const int b0 = g * nbat / G, b1 = (g + 1) * nbat / G;
       Lu v{h->Cw + b0 * st, h->Inv + b0 * h->inv_stride, h->ipiv + (int64_t)b0 * n, h->stats + 2 * (j + b0),
@@ -687,15 +719,16 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
            g ? h->gev_p[g] : h->ev_p, (h->stagger && g + 1 < G) ? h->gev_first[g] : nullptr,
            h->prof_serial ? nullptr : h->gx[g], h->gev_t[g], h->gev_x[g]};
       if (g) cudaStreamWaitEvent(v.sm, (h->stagger && g > 0) ? h->gev_first[g - 1] : h->ev_fork, 0);
+      vs.push_back(v);
       if (!reuse) {
         feast::stats_init_launch(v.stats, v.info, v.nbat, v.sm);
         // a2: C_j = z_j B - A ; R appended as extra columns (augmented system [C_j | R]).  Only the
-        // first outer block's columns are formed before its factorisation starts; lu_batched
-        // forms the rest underneath it (needed only once the block is factored).
+        // first outer block's columns are formed before its factorisation starts; the LU forms
+        // the rest underneath it (needed only once the block is factored).
         const int64_t w0 = std::min<int64_t>(h->nbo, n);
         const double2* zj = h->zd + j + b0;
         feast::shift_launch(bat(v.Cw, ld, st), A, lda, B, ldb, zj, n, v.nbat, v.sm, 0, w0);
-        auto rest = [&, zj](cudaStream_t sr) {
+        auto rest = [&, zj, v](cudaStream_t sr) {
           feast::shift_launch(bat(v.Cw, ld, st), A, lda, B, ldb, zj, n, v.nbat, sr, w0, n);
           if (rhs_wait) cudaStreamWaitEvent(sr, rhs_wait, 0);
           if (doR)
@@ -706,7 +739,19 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
                                          feast::BC_CONJ, sr);
         };
         // a3 (+ forward substitution of a4): P_j [C_j | R] -> [U_j | L_j^-1 P_j R]
-        lu_batched(h, v, solve ? ncr : 0, rest);
+        runs.push_back(LuRun{h, v, solve ? ncr : 0, rest});
+      }
+    }
+    // pass 2: the groups' LU sequences enqueued round-robin, one outer block each per turn
+    for (bool all = runs.empty(); !all;) {
+      all = true;
+      for (auto& r : runs) all = r.step() && all;
+    }
+    // pass 3: per group, the substitutions and the join
+    for (int g = 0; g < G; ++g) {
+      const int b0 = g * nbat / G;
+      const Lu& v = vs[g];
+      if (!reuse) {
         if (doL || h->cache_on)
           feast::perm_launch(v.ipiv, h->perm + (int64_t)b0 * n, h->iperm + (int64_t)b0 * n, n, v.nbat, v.sm);
         // a4: Y_j = U_j^-1 (L_j^-1 P_j R)
