@@ -393,7 +393,8 @@ bool smem_panel_for(const feast_ctx* h, int64_t k) {
 }
 
 // Timing ablation (FEAST_ABLATE, never for results): bit 1 skips the panels (identity pivots),
-// bit 2 the triangular kernels, bit 4 the row swaps — to measure each class's marginal cost in
+// bit 2 the triangular kernels, bit 4 the row swaps, bit 8 the back substitution — to measure
+// each class's marginal cost in
 // the overlapped schedule.
 int ablate() {
   static const int a = [] { const char* e = getenv("FEAST_ABLATE"); return e ? atoi(e) : 0; }();
@@ -755,7 +756,7 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
         if (doL || h->cache_on)
           feast::perm_launch(v.ipiv, h->perm + (int64_t)b0 * n, h->iperm + (int64_t)b0 * n, n, v.nbat, v.sm);
         // a4: Y_j = U_j^-1 (L_j^-1 P_j R)
-        if (solve) solve_right_back(h, v, v.Cw + n * ld, st, ncr);
+        if (solve && !(ablate() & 8)) solve_right_back(h, v, v.Cw + n * ld, st, ncr);
       } else if (doR) {
         // cached factors (NEXT-1, "factored just once"): Y_j = U^-1 L^-1 P_j R
         double2* Yg = h->Y + b0 * ld * mr;   // (factor cache and real-pencil mode are exclusive: mr = m)
