@@ -109,20 +109,25 @@ __global__ void __launch_bounds__(32 * WGM * WGN, MINB) zgemm_dmma_kernel(ZgemmA
     const double2* as = a_src + kt * a_kt;
     const double2* bs = b_src + k0;
     const uint32_t ad = as_dst + stage * (A_STAGE * 16), bd = bs_dst + stage * (B_STAGE * 16);
+    // source pointers advanced incrementally (no per-i 64-bit offsets held in registers)
+    const double2* ap = as;
 #pragma unroll
     for (int i = 0; i < LA; ++i) {
       const bool kin = CONJA ? (k0 + a_k < K) : (k0 + a_k + i * A_DI < K);
       const bool pred = ((a_ok >> i) & 1u) && kin;
       const int sz = pred ? 16 : 0;
-      const double2* src = pred ? as + i * a_step : A;
+      const double2* src = pred ? ap : A;
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(ad + i * A_DST_STEP), "l"(src), "r"(sz));
+      ap += a_step;
     }
+    const double2* bp = bs;
 #pragma unroll
     for (int i = 0; i < LB; ++i) {
       const bool pred = ((b_ok >> i) & 1u) && (k0 + b_k < K);
       const int sz = pred ? 16 : 0;
-      const double2* src = pred ? bs + i * b_step : B;
+      const double2* src = pred ? bp : B;
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(bd + i * B_DST_STEP), "l"(src), "r"(sz));
+      bp += b_step;
     }
   };
 
@@ -256,6 +261,7 @@ void launch_variant(const ZgemmArgs& p, int v, cudaStream_t s) {
     case 5: launch3<32, 64, 2, 2, 4, 2, CONJA, MODE>(p, s); break;
     case 6: launch3<32, 32, 2, 2, 3, 2, CONJA, MODE, true, 32>(p, s); break;   // BK = 32
     case 7: launch3<32, 32, 2, 2, 4, 3, CONJA, MODE, false>(p, s); break;      // C_old read in the epilogue
+    case 8: launch3<64, 64, 2, 2, 3, 2, CONJA, MODE, false>(p, s); break;      // 32x32 warp tiles
     default: launch_t<CONJA, MODE>(p, s); break;
   }
 }
