@@ -246,7 +246,10 @@ void launch3(const ZgemmArgs& p, cudaStream_t s) {
 
 template <bool CONJA, int MODE>
 void launch_t(const ZgemmArgs& p, cudaStream_t s) {
-  if (p.inplace) launch3<64, 32, 2, 2, 4, 2, CONJA, MODE>(p, s);   // BM >= M: one CTA row
+  // in place (C aliases B, BM >= M: one CTA row of tiles): 64x16 CTAs when the 64x32 grid would
+  // leave most SMs idle (the substitutions' Y_k <- T_kk^-1 Y_k with N = m0)
+  if (p.inplace && (p.N + 31) / 32 * p.batch < 148) launch3<64, 16, 4, 1, 4, 2, CONJA, MODE>(p, s);
+  else if (p.inplace) launch3<64, 32, 2, 2, 4, 2, CONJA, MODE>(p, s);
   else launch3<32, 32, 2, 2, 4, 3, CONJA, MODE>(p, s);
 }
 
