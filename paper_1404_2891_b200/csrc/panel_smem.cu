@@ -178,9 +178,12 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int r = tid + s * NT;
+      const double2* src = C + rbeg + r;   // advanced by ld per column (no 64-bit products)
 #pragma unroll
-      for (int jj = 0; jj < WC; ++jj)
-        a[s][jj] = (r < nrow && jj < wc0) ? C[rbeg + r + (int64_t)jj * ld] : make_double2(0.0, 0.0);
+      for (int jj = 0; jj < WC; ++jj) {
+        a[s][jj] = (r < nrow && jj < wc0) ? *src : make_double2(0.0, 0.0);
+        src += ld;
+      }
     }
   }
   cluster.sync();   // mbarrier inits visible cluster-wide before any remote st.async
@@ -351,9 +354,12 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
     for (int s = 0; s < S; ++s) {
       const int r = tid + s * NT;
       if (r < nrow) {
+        double2* dst = C + rbeg + r + (int64_t)j0 * ld;
 #pragma unroll
-        for (int jj = 0; jj < WC; ++jj)
-          if (jj < wc) C[rbeg + r + (int64_t)(j0 + jj) * ld] = a[s][jj];
+        for (int jj = 0; jj < WC; ++jj) {
+          if (jj < wc) *dst = a[s][jj];
+          dst += ld;
+        }
       }
     }
     CT(11);
