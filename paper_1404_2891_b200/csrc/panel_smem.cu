@@ -73,6 +73,10 @@ __device__ __forceinline__ double fast_rcp(double x) {
   return fma(r, e, r);
 }
 
+// Smith's complex reciprocal for extreme magnitudes, kept out of line (it is never on the fast
+// path, and inlined into every unrolled column step it only costs instruction-cache space)
+__device__ __noinline__ double2 crcp_slow(double2 b) { return crcp(b); }
+
 __device__ __forceinline__ bool better(double v, int i, double bv, int bi) {
   return v > bv || (v == bv && i < bi);
 }
@@ -111,7 +115,7 @@ __device__ unsigned long long g_ctrace[2][16];
 #define CT(i) do {} while (0)
 #endif
 
-template <int S, int WC, int NT>
+template <int S, int WC, int NT, bool CLU>   // CLU: cluster of > 1 CTAs (else the single-CTA path)
 __global__ void __launch_bounds__(NT, 1)
 panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__ ipiv_all,
                   double* __restrict__ stats_all, int32_t* __restrict__ info_all) {
@@ -232,7 +236,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
       const uint32_t bar = saddr(&mbar[buf]);
       PTRACE(8 + 4 * col);
       CT(0);
-      if (tid == 0 && CS > 1) mbar_arm(bar, (uint32_t)(CS * SLOT_BYTES));
+      if (tid == 0 && CLU) mbar_arm(bar, (uint32_t)(CS * SLOT_BYTES));
       unsigned long long bk = 0ull;
       int bs = -1;
 #pragma unroll
@@ -260,7 +264,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
         const double d = fast_rcp(m2);
         myrcp = make_double2(pv.x * d, -pv.y * d);
       } else {
-        myrcp = (pv.x != 0.0 || pv.y != 0.0) ? crcp(pv) : make_double2(0.0, 0.0);   // extreme magnitudes
+        myrcp = (pv.x != 0.0 || pv.y != 0.0) ? crcp_slow(pv) : make_double2(0.0, 0.0);   // extreme magnitudes
       }
       CT(3);
       // the warp's winning lane stages its chunk row and 1/pivot; one barrier for the CTA step
@@ -293,7 +297,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
       unsigned long long gk;
       const double2* prow;
       double2 pinv;
-      if (CS == 1) {
+      if (!CLU) {
         // single CTA: the CTA winner is the pivot
         gk = ck;
         prow = wrow[buf][cw];
@@ -367,7 +371,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
     if (c1 < w) {
       const int rem = w - c1;
       const uint32_t ubar = saddr(&mbar[2]);
-      if (tid == 0 && CS > 1) mbar_arm(ubar, (uint32_t)(wc * rem * 16));
+      if (tid == 0 && CLU) mbar_arm(ubar, (uint32_t)(wc * rem * 16));
       __syncthreads();
       // owners push the chunk pivot rows' rest-of-panel values to every CTA (single CTA: plain
       // shared-memory copies and a barrier)
@@ -376,13 +380,13 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
         if (pr >= 0 && pr < nrow) {
           for (int idx = tid; idx < rem * CS; idx += NT) {
             const int dcta = idx / rem, c = idx - dcta * rem;
-            if (CS == 1) U12s[jj][c] = P[(c1 - WC + c) * PLD + pr];
+            if (!CLU) U12s[jj][c] = P[(c1 - WC + c) * PLD + pr];
             else st_async16(mapa(saddr(&U12s[jj][c]), dcta), P[(c1 - WC + c) * PLD + pr], mapa(ubar, dcta));
           }
         }
       }
       PTRACE(300 + 4 * chunk);
-      if (CS == 1) __syncthreads();
+      if (!CLU) __syncthreads();
       else mbar_wait(ubar, (uint32_t)(chunk & 1));
       CT(12);
       PTRACE(301 + 4 * chunk);
@@ -502,8 +506,9 @@ void launch_s(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* sta
   const size_t smem = (size_t)Lc * (w > WC ? w - WC : 0) * sizeof(double2);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(panel_smem_kernel<S, WC, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(panel_smem_kernel<S, WC, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(panel_smem_kernel<S, WC, NT, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(panel_smem_kernel<S, WC, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(panel_smem_kernel<S, WC, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -518,7 +523,8 @@ void launch_s(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* sta
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, panel_smem_kernel<S, WC, NT>, C, n, k, w, ipiv, stats, info);
+  if (cs > 1) cudaLaunchKernelEx(&cfg, panel_smem_kernel<S, WC, NT, true>, C, n, k, w, ipiv, stats, info);
+  else cudaLaunchKernelEx(&cfg, panel_smem_kernel<S, WC, NT, false>, C, n, k, w, ipiv, stats, info);
   count_launch();
 }
 
@@ -546,7 +552,8 @@ int panel_smem_max_clusters(int64_t L, int w, int cs) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int nc = -1;
-  auto k = Lc <= PT ? panel_smem_kernel<1, 8, PT> : (Lc <= 2 * PT ? panel_smem_kernel<2, 8, PT> : panel_smem_kernel<2, 8, 2 * PT>);
+  auto k = Lc <= PT ? panel_smem_kernel<1, 8, PT, true>
+                    : (Lc <= 2 * PT ? panel_smem_kernel<2, 8, PT, true> : panel_smem_kernel<2, 8, 2 * PT, true>);
   cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (cudaOccupancyMaxActiveClusters(&nc, k, &cfg) != cudaSuccess) { cudaGetLastError(); return -1; }
