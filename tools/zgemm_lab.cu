@@ -28,7 +28,11 @@ int main(int argc, char** argv) {
                            {1984, 1984, 64, 16, 0, false},  {4096, 4096, 256, 4, 0, false},
                            {8192, 8192, 256, 1, 0, false},  {4096, 4096, 4096, 1, 1, false},
                            {1920, 128, 128, 16, 0, false},  {2048, 128, 2048, 1, 1, true},
-                           {64, 1920, 64, 16, 1, false},    {448, 128, 64, 16, 0, true}};
+                           {64, 1920, 64, 16, 1, false},    {448, 128, 64, 16, 0, true},
+                           // the LU's short-K updates of one 4-node group (C2): in-block (K = 32,
+                           // 64) and the outer block's per-64-block sub-updates (M < 256)
+                           {1984, 32, 32, 4, 0, false},    {1920, 192, 64, 4, 0, false},
+                           {192, 1792, 64, 4, 0, false},   {1536, 1664, 256, 4, 0, false}};
   std::vector<int> variants = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9};
   int only_cfg = -2, only_var = -2;
   if (argc > 2) { only_cfg = atoi(argv[1]); only_var = atoi(argv[2]); }
