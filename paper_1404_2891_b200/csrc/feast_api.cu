@@ -56,6 +56,7 @@ struct feast_ctx {
   feast::PanelCfg pcfg{};
   int smem_cs = 0;   // cluster size of the shared-memory panel kernel for the full height (0: too tall)
   int smem_cs_max = 16;  // largest cluster the shared-memory panel may use (FEAST_CS_MAX)
+  bool panel_one_row = false;  // 256 threads x 1 row panels: set when <= 4 units are owned (latency-bound)
   bool lookahead = true;
   bool cache_on = false, cache_valid = false;   // factor-once reuse across calls
   const void *cache_A = nullptr, *cache_B = nullptr;
@@ -405,7 +406,8 @@ void panel_at(feast_ctx* h, const Lu& v, int64_t k, int w, cudaStream_t s) {
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr);
   if (ablate() & 1) { feast::ipiv_identity_launch(v.ipiv, n, k, w, v.nbat, s); return; }
   if (smem_panel_for(h, k))
-    feast::panel_smem_launch(bat(v.Cw, ld, st), n, k, w, v.ipiv, v.stats, v.info, v.nbat, h->smem_cs_max, s);
+    feast::panel_smem_launch(bat(v.Cw, ld, st), n, k, w, v.ipiv, v.stats, v.info, v.nbat, h->smem_cs_max, s,
+                             h->panel_one_row);
   else
     feast::panel_launch(bat(v.Cw, ld, st), n, k, w, v.ipiv, v.stats, v.info, v.nbat, h->pcfg, s);
 }
@@ -983,6 +985,10 @@ int setup_units(feast_ctx* h) {
   const int owned = h->j1 - h->j0;
   h->batch = std::max(1, h->max_batch == 0 ? owned : std::min<int>(h->max_batch, owned));
   h->mr = (h->real || (h->csym && h->mode == FEAST_BI)) ? 2 * h->m0 : h->m0;
+  // few concurrent LUs: the panel chain bounds the step, so panels take the faster 8-warp form
+  // (measured C2 rank shares: 4 nodes 7.5 -> 7.2 ms, 2 nodes 6.4 -> 6.2 ms; 16 nodes lose 4 %)
+  h->panel_one_row = h->batch <= 4;
+  if (const char* e = getenv("FEAST_PANEL_1ROW")) h->panel_one_row = e[0] == '1';
   return 0;
 }
 

@@ -50,7 +50,8 @@ void laswp_launch(Batched C, int64_t n, int64_t k, int cnt, const int32_t* ipiv,
 bool panel_smem_fits(int64_t n, int w, int cs);
 int panel_smem_max_clusters(int64_t L, int w, int cs);
 void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info, int batch,
-                       int cs, cudaStream_t s);
+                       int cs, cudaStream_t s,
+                       bool one_row = false);
 
 // Triangular solve op(T) X = X in place, T = nb x nb diagonal block (nb <= 64),
 // X = nb x ncols.  lower_op: op(T) lower (forward); unit: unit diagonal; conjT: op = ^H.

@@ -567,7 +567,8 @@ bool panel_smem_fits(int64_t n, int w, int cs) {
 }
 
 void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info, int batch,
-                       int cs, cudaStream_t s) {
+                       int cs, cudaStream_t s,
+                       bool one_row) {
   const double L_ = (double)(n - k);
   ProfScope ps_(K_PANEL, (double)batch * (4.0 * L_ * w * w - 4.0 * w * (double)w * w / 3.0), 0.0, s);
   // Shrink the cluster as the panel gets shorter (L = n - k): the smallest cluster that keeps
@@ -579,7 +580,12 @@ void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, do
   while (cs > 1 && (n - k + cs / 2 - 1) / (cs / 2) <= rowcap) cs /= 2;
   const int64_t Lc = (n - k + cs - 1) / cs;
   // register chunk: 8 columns (a 16-column chunk spills at 2 rows per thread)
+  // one_row: 129..256 rows per CTA on 256 threads x 1 row (8 warps, faster
+  // per column and in the chunk-end update, but the CTA takes most of the register file, so no
+  // trailing-update GEMM CTA shares its SM): chosen by the caller when few nodes are factored
+  // and the panel chain, not GEMM throughput, bounds the step
   if (Lc <= PT) launch_s<1, 8, PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);
+  else if (Lc <= 2 * PT && one_row) launch_s<1, 8, 2 * PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);
   else if (Lc <= 2 * PT) launch_s<2, 8, PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);
   else launch_s<2, 8, 2 * PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);   // 512 rows: 256 threads x 2
 }
