@@ -382,6 +382,19 @@ def test_permutation_laswp_variant(monkeypatch):
     assert rel(Q, oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
 
 
+@pytest.mark.parametrize("one_row", ["0", "1"])
+def test_panel_thread_layouts(monkeypatch, one_row):
+    """Both panel thread layouts for 129..256 rows per CTA (128 threads x 2 rows, the default for
+    many concurrent nodes; 256 threads x 1 row, the default for <= 4) give the oracle's projector
+    on heights that walk through cluster sizes 8 -> 1 (n = 1100, ragged)."""
+    monkeypatch.setenv("FEAST_PANEL_1ROW", one_row)
+    P = synth.make_pencil("C2", n=1100, m0=12)
+    z, w = _oracle_nodes(P)
+    f = _handle(P)
+    Q = host(f.project(dev(P.A), dev(P.B), dev(P.X0)))
+    assert rel(Q, oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
+
+
 @pytest.mark.parametrize("key,n,m0", [("C2", 220, 24), ("C4", 200, 30)])
 def test_projector_parity_at_later_iterations(key, n, m0):
     """Parity protocol P1 at k > 1: the GPU projector applied to the ORACLE's
