@@ -83,8 +83,10 @@ enum {
  *  mode                         FEAST_RIGHT or FEAST_BI
  *  b_is_identity                non-zero when B = I (B pointers may then be NULL)
  *  rank, world                  node sharding (world >= 1, 0 <= rank < world, q % world == 0)
- *  max_batch                    nodes factored concurrently (0 = all owned nodes); bounds
- *                               the workspace at max_batch * 16 n^2 bytes plus blocks
+ *  max_batch                    nodes factored concurrently (0 = all owned nodes that fit:
+ *                               feast_workspace_bytes shrinks the batch until the workspace
+ *                               takes at most 90 % of the free device memory); bounds the
+ *                               workspace at max_batch * 16 n^2 bytes plus blocks
  *  cuda_stream                  cudaStream_t the work is enqueued on (NULL = legacy stream)
  * Errors: FEAST_E_ARG, FEAST_E_CUDA. */
 int feast_init(feast_handle* h, int64_t n, int64_t m0, double c_re, double c_im, double r,

@@ -1123,6 +1123,22 @@ static size_t layout(feast_ctx* h, char* base) {
 int feast_workspace_bytes(feast_handle h, size_t* bytes) {
   if (!h || !bytes) return FEAST_E_ARG;
   *bytes = layout(h, nullptr);
+  if (h->max_batch == 0) {
+    // "all owned nodes" means all that fit: shrink the concurrent batch until the workspace
+    // takes at most 90 % of the device memory free now (C5 on one B200: 16 nodes x 17.7 GB of
+    // augmented blocks do not fit next to A and B; 4 do)
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && free_b > 0) {
+      const size_t cap = free_b / 10 * 9;
+      while (*bytes > cap && h->batch > 1) {
+        h->batch = std::max(1, h->batch * 3 / 4);
+        *bytes = layout(h, nullptr);
+      }
+      if (!getenv("FEAST_PANEL_1ROW")) h->panel_one_row = h->batch <= 4;
+    } else {
+      cudaGetLastError();
+    }
+  }
   return FEAST_OK;
 }
 
