@@ -25,21 +25,21 @@ Prof& prof() {
 }
 
 // ============================================================================ shift
-// C_b = z_b B - A  (HBM-bound: reads A (+B), writes C_b).
+// C_b = z_b B - A  (HBM-bound).  One thread per element of A for the whole batch: A
+// and B are read once per element and the batch's C_b written from registers, so a group of
+// nodes costs 32 + 16 * batch bytes per element instead of 48 * batch (A + B = 134 MB at
+// n = 2048 do not stay in the 126 MB L2 between per-node passes).
 __global__ void shift_kernel(Batched C, const double2* __restrict__ A, int64_t lda,
                              const double2* __restrict__ B, int64_t ldb, const double2* __restrict__ z,
-                             int64_t n, int64_t c0) {
-  const int b = blockIdx.z;
+                             int64_t n, int64_t c0, int batch) {
   const int64_t col = c0 + blockIdx.y;
-  const double2 zb = z[b];
-  double2* Cc = C.p + b * C.stride + col * C.ld;
   const double2* Ac = A + col * lda;
+  const double2* Bc = B ? B + col * ldb : nullptr;
+  double2* Cc = C.p + col * C.ld;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double2 a = Ac[i];
-    double2 v;
-    if (B) v = csub(cmul(zb, B[i + col * ldb]), a);
-    else v = (i == col) ? make_double2(zb.x - a.x, zb.y - a.y) : make_double2(-a.x, -a.y);
-    Cc[i] = v;
+    const double2 a = Ac[i];
+    const double2 bv = Bc ? Bc[i] : make_double2(i == col ? 1.0 : 0.0, 0.0);
+    for (int b = 0; b < batch; ++b) Cc[b * C.stride + i] = csub(cmul(z[b], bv), a);
   }
 }
 
@@ -47,12 +47,12 @@ void shift_launch(Batched C, const double2* A, int64_t lda, const double2* B, in
                   const double2* z, int64_t n, int batch, cudaStream_t s, int64_t c0, int64_t c1) {
   if (c1 < 0) c1 = n;
   if (c1 <= c0) return;
-  ProfScope ps_(K_SHIFT, 0.0, (double)batch * n * (c1 - c0) * 16.0 * (B ? 3 : 2), s);
+  ProfScope ps_(K_SHIFT, 0.0, (double)(c1 - c0) * n * 16.0 * ((B ? 2 : 1) + batch), s);
   const int threads = 256;
   unsigned gx = (unsigned)((n + threads - 1) / threads);
   if (gx > 8) gx = 8;
-  dim3 grid(gx, (unsigned)(c1 - c0), (unsigned)batch);
-  shift_kernel<<<grid, threads, 0, s>>>(C, A, lda, B, ldb, z, n, c0);
+  dim3 grid(gx, (unsigned)(c1 - c0), 1);
+  shift_kernel<<<grid, threads, 0, s>>>(C, A, lda, B, ldb, z, n, c0, batch);
   count_launch();
 }
 
