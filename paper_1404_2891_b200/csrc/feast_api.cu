@@ -358,8 +358,16 @@ void gemm_gen(feast_ctx* h, int64_t M, int64_t N, int64_t K, bool conjA, const d
   const int64_t tiles = ((M + 31) / 32) * ((N + 31) / 32);
   int splits = 1;
   if (tiles < 444 && K >= 512 && h->SK) {
-    splits = (int)std::min<int64_t>((444 + tiles - 1) / tiles, K / 256);
-    while (splits > 1 && (int64_t)splits * M * N > h->sk_elems) --splits;
+    // the split count whose tile grid best fills whole waves of 444 CTAs (2 splits of a 256-tile
+    // grid would run 1.15 waves at 58 % occupancy of the second; 5 splits fill 96 %)
+    double best = (double)tiles / 444.0;
+    const int smax = (int)std::min<int64_t>(16, K / 128);
+    for (int sp = 2; sp <= smax; ++sp) {
+      if ((int64_t)sp * M * N > h->sk_elems) break;
+      const int64_t t = tiles * sp, waves = (t + 443) / 444;
+      const double eff = (double)t / (double)(waves * 444) - 0.01 * sp;   // mild cost per split
+      if (eff > best) { best = eff; splits = sp; }
+    }
   }
   if (splits <= 1) {
     ZgemmArgs p{M, N, K, A, lda, 0, B, ldb, 0, C, ldc, 0, alpha, beta, 1};
@@ -1113,7 +1121,7 @@ static size_t layout(feast_ctx* h, char* base) {
   h->RL = (!h->b_id && h->mode == FEAST_BI) ? (double2*)take((size_t)ld * m * 16) : nullptr;
   h->AQ = (double2*)take((size_t)ld * m * 16);
   h->BQ = !h->b_id ? (double2*)take((size_t)ld * m * 16) : nullptr;
-  h->sk_elems = std::max<int64_t>(8 * m * m, (int64_t)4 * ld * m);
+  h->sk_elems = std::max<int64_t>(16 * m * m, (int64_t)6 * ld * m);
   h->SK = (double2*)take((size_t)h->sk_elems * 16);
   h->nblk = (n + 63) / 64;
   h->inv_stride = h->nblk * 2 * 4096;
