@@ -1121,7 +1121,9 @@ static size_t layout(feast_ctx* h, char* base) {
   h->RL = (!h->b_id && h->mode == FEAST_BI) ? (double2*)take((size_t)ld * m * 16) : nullptr;
   h->AQ = (double2*)take((size_t)ld * m * 16);
   h->BQ = !h->b_id ? (double2*)take((size_t)ld * m * 16) : nullptr;
-  h->sk_elems = std::max<int64_t>(16 * m * m, (int64_t)6 * ld * m);
+  // split-K partials: up to 6 n x m0 slices (grids that small need splits; large ones do not),
+  // capped at 512 MB
+  h->sk_elems = std::max<int64_t>(16 * m * m, std::min<int64_t>((int64_t)6 * ld * m, (int64_t)1 << 25));
   h->SK = (double2*)take((size_t)h->sk_elems * 16);
   h->nblk = (n + 63) / 64;
   h->inv_stride = h->nblk * 2 * 4096;
