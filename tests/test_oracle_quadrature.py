@@ -184,3 +184,54 @@ def test_composite_spec_examples():
     assert abs(r_in - 1) < 1e-6 and abs(r_out) < 1e-6
     errs = [abs(oracle.rho(*oracle.contour_nodes(TRIANGLE, K, 0), [1j / 3])[0] - 1) for K in (4, 8, 16, 32)]
     assert all(b < a for a, b in zip(errs, errs[1:]))
+
+
+# ---------------------------------------------------------------- ellipse weights, aspect != 1
+# eq. ellipses and eq. quadrature_for_pi: sigma = w_k phi'(t)/(2 pi i) with
+# phi'(t) = (pi/2) R (-sin th + i a cos th).  These pins bind the aspect a inside the derivative
+# (dropping it leaves the pole positions, and every a = 1 pin, unchanged).
+ELLIPSES = [(0.3 - 0.1j, 0.4, 0.15), (0.0, 0.4, 0.15), (0.5 + 0.2j, 1.3, 0.5), (-0.2j, 0.25, 2.0)]
+
+
+@pytest.mark.parametrize("c,R,a", ELLIPSES)
+@pytest.mark.parametrize("rule,n_e", [(0, 8), (0, 16), (0, 32), (1, 16)])
+def test_ellipse_moments_vanish_exactly(c, R, a, rule, n_e):
+    """The midpoint and endpoint trapezoid rules are the q-point periodic trapezoid rule in
+    theta, exact on trigonometric polynomials of degree <= q - 1.  (z - c)^k phi'(theta) has
+    degree k + 1, so sum_j w_j (z_j - c)^k = (1/2 pi i) oint (z - c)^k dz = 0 for k <= q - 2
+    (Cauchy's theorem), for every aspect a."""
+    z, w = oracle.nodes(c, R, a, n_e, rule)
+    q = len(z)
+    assert q == n_e
+    for k in range(q - 1):
+        scale = np.sum(np.abs(w) * np.abs(z - c) ** k)
+        assert abs(np.sum(w * (z - c) ** k)) <= 1e-14 * scale, (k, a)
+
+
+@pytest.mark.parametrize("c,R,a", ELLIPSES + [(0.1, 0.7, 1.0)])
+@pytest.mark.parametrize("rule,n_e", [(0, 8), (0, 16), (1, 16), (2, 8), (2, 16)])
+def test_ellipse_area_identity(c, R, a, rule, n_e):
+    """Green's theorem: oint conj(z - c) dz = 2i * Area, so (1/2 pi i) oint conj(z - c) dz =
+    Area / pi = R * (R a) = R^2 a for the ellipse with semi-axes R and R a (reading R2).  The
+    trapezoid rules integrate this degree-2 trigonometric polynomial exactly; Gauss-Legendre on
+    the two halves integrates the entire function of t to rounding at K >= 8."""
+    z, w = oracle.nodes(c, R, a, n_e, rule)
+    assert abs(np.sum(w * np.conj(z - c)) - R * R * a) <= 1e-14 * R * R
+
+
+@pytest.mark.parametrize("rule", [0, 2])
+@pytest.mark.parametrize("a", [0.15, 0.5])
+def test_ellipse_cauchy_limit(rule, a):
+    """Cauchy's integral formula (eq. cauchy_contour) on thin ellipses: rho -> 1 at
+    points inside, -> 0 outside, monotonically as K grows, to 1e-8 at K = 256 per half."""
+    c, R = 0.3 - 0.1j, 0.4
+    inside = c + R * np.array([0.0, 0.3, 0.5j * a, -0.2 + 0.1j * a])
+    outside = c + R * np.array([1.6, 3j * a, -2.0, 1.2 + 0.5j])
+    prev = None
+    for K in (8, 16, 32, 64, 128, 256):
+        z, w = oracle.nodes(c, R, a, 2 * K if rule == 0 else K, rule)
+        err = max(np.max(np.abs(oracle.rho(z, w, inside) - 1)), np.max(np.abs(oracle.rho(z, w, outside))))
+        if prev is not None and prev > 1e-13:
+            assert err < prev, (K, err, prev)
+        prev = err
+    assert prev < 1e-8
