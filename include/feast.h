@@ -189,19 +189,6 @@ int feast_reduce(feast_handle h, const void* A, int64_t lda, const void* B, int6
 int feast_estimate_count(feast_handle h, const void* A, int64_t lda, const void* B, int64_t ldb,
                          const void* U, int64_t ldu, void* Q, int64_t ldq, double* estimate);
 
-/* Small dense eigensolver for the reduced problem (R-FEAST step 5; Bi-FEAST step 7,
- * P:530-532), used by feast_iterate when FEAST_EIG=own and m0 <= 160: one CTA, Householder Hessenberg
- * reduction + complex single-shift QR (Wilkinson / exceptional shifts) with the Hessenberg
- * matrix packed in shared memory, eigenvectors by back-substitution on the Schur form and a
- * DMMA product W = Z Y.  M: m x m device (not modified); lam: m complex (device); W: m x m
- * device right eigenvectors (not normalised), ld >= m; work: device, >= 3 m^2 * 16 + 16 bytes.
- * FEAST_E_ARG for m > 160 or bad arguments, FEAST_E_REDUCED if the QR iteration does not
- * converge (30 m sweeps; feast_iterate then falls back to cuSOLVER Xgeev).  Synchronises.
- * Device-resident (no host round trips), but measured slower than cuSOLVER Xgeev on B200
- * (m = 64 / 128 / 160: 5.6 / 28 / 49 ms vs 5.8 / 26 / - ms): the default stays cuSOLVER. */
-int feast_small_eig(int64_t m, const void* M, int64_t ldm, void* lam, void* W, int64_t ldw, void* work,
-                    size_t work_bytes, void* cuda_stream);
-
 /* All-reduce callback for world > 1: sum `count` float64 values at device pointer `buf`
  * across ranks, in place, ordered on `cuda_stream` (the library's stream: the callback must
  * enqueue its collective there, or complete it before returning); return 0 on success. */

@@ -68,8 +68,6 @@ struct feast_ctx {
   // concurrent node groups (group 0 uses stream / side / ev_a / ev_p)
   static constexpr int GMAX = 4;
   bool laswp_perm = false;            // FEAST_LASWP=perm: permutation-gather row swaps
-  bool own_eig = false;               // FEAST_EIG=own: reduced eig on one CTA for m0 <= RE_MAXM
-                                      // (device-resident; 28 ms vs cuSOLVER Xgeev 26 ms at m0 = 128)
   bool prof_serial = false;           // feast_profile(h, 2): one stream, no lookahead / groups
   int groups = 4;                     // concurrent node groups per batch (FEAST_GROUPS)
   bool group_streams = false;
@@ -1059,7 +1057,6 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   if (const char* e = getenv("FEAST_LOOKAHEAD")) h->lookahead = e[0] != '0';
   if (const char* e = getenv("FEAST_GRAPH")) h->graphs = e[0] != '0';
   if (const char* e = getenv("FEAST_LASWP")) h->laswp_perm = e[0] == 'p';
-  if (const char* e = getenv("FEAST_EIG")) h->own_eig = e[0] == 'o';
   if (const char* e = getenv("FEAST_STAGGER")) h->stagger = e[0] != '0';
   if (const char* e = getenv("FEAST_WIDE_ROWS")) h->wide_panel_rows = atol(e);
   if (const char* e = getenv("FEAST_GROUPS")) {
@@ -1307,29 +1304,6 @@ int feast_estimate_count(feast_handle h, const void* A, int64_t lda, const void*
   return pst;
 }
 
-int feast_small_eig(int64_t m, const void* M, int64_t ldm, void* lam, void* W, int64_t ldw, void* work,
-                    size_t work_bytes, void* cuda_stream) {
-  if (m < 1 || m > feast::RE_MAXM || !M || !lam || !W || !work || ldm < m || ldw < m ||
-      work_bytes < (size_t)3 * m * m * 16 + 16)
-    return FEAST_E_ARG;
-  cudaStream_t s = (cudaStream_t)cuda_stream;
-  double2* H = (double2*)work;
-  double2* Z = H + m * m;
-  double2* Y = Z + m * m;
-  int32_t* info = (int32_t*)(Y + m * m);
-  if (cudaMemcpy2DAsync(H, m * 16, M, ldm * 16, m * 16, m, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-    return FEAST_E_CUDA;
-  feast::reduced_eig_launch(H, (int)m, m, Z, m, (double2*)lam, Y, m, info, s);
-  int32_t hinfo = 0;
-  if (cudaMemcpyAsync(&hinfo, info, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
-    return FEAST_E_CUDA;
-  if (hinfo) return FEAST_E_REDUCED;
-  feast::ZgemmArgs p{m, m, m, Z, m, 0, Y, m, 0, (double2*)W, ldw, 0, make_double2(1, 0), make_double2(0, 0), 1};
-  feast::zgemm_launch(p, false, feast::ZG_GEN, s);
-  if (cudaStreamSynchronize(s) != cudaSuccess) return FEAST_E_CUDA;
-  return FEAST_OK;
-}
-
 int feast_set_allreduce(feast_handle h, feast_allreduce_fn fn, void* user) {
   if (!h) return FEAST_E_ARG;
   h->ar = fn;
@@ -1396,26 +1370,11 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
   SOL_TRY(h, cusolverDnZgetrs(h->sol, CUBLAS_OP_N, (int)m, (int)m, (cuDoubleComplex*)it.T, (int)m, it.piv,
                               (cuDoubleComplex*)it.M, (int)m, it.info));
   int hinfo = 0;
-  bool solved = false;
-  if (m <= feast::RE_MAXM && h->own_eig) {
-    // one-CTA Hessenberg + shifted QR (reduced_eig.cu) on a copy of M (kept for the fallback):
-    // W = Z Y with Z the Schur vectors and Y the eigenvectors of the Schur form
-    CUDA_TRY(h, cudaMemcpyAsync(it.W, it.M, m * m * 16, cudaMemcpyDeviceToDevice, h->stream));
-    feast::reduced_eig_launch(it.W, (int)m, m, it.Z, m, it.lam, it.T, m, it.info, h->stream);
-    CUDA_TRY(h, cudaMemcpyAsync(&hinfo, it.info, 4, cudaMemcpyDeviceToHost, h->stream));
-    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-    if (hinfo == 0) {
-      gemm_gen(h, m, m, m, false, it.Z, m, it.T, m, it.W, m, one, zero);
-      solved = true;
-    }
-  }
-  if (!solved) {
-    SOL_TRY(h, cusolverDnXgeev(h->sol, h->solp, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, m, CUDA_C_64F,
-                               it.M, m, CUDA_C_64F, it.lam, CUDA_C_64F, nullptr, m, CUDA_C_64F, it.W, m, CUDA_C_64F,
-                               it.sw, it.sw_bytes, it.hw.data(), it.hw.size(), it.info));
-    CUDA_TRY(h, cudaMemcpyAsync(&hinfo, it.info, 4, cudaMemcpyDeviceToHost, h->stream));
-    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-  }
+  SOL_TRY(h, cusolverDnXgeev(h->sol, h->solp, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, m, CUDA_C_64F,
+                             it.M, m, CUDA_C_64F, it.lam, CUDA_C_64F, nullptr, m, CUDA_C_64F, it.W, m, CUDA_C_64F,
+                             it.sw, it.sw_bytes, it.hw.data(), it.hw.size(), it.info));
+  CUDA_TRY(h, cudaMemcpyAsync(&hinfo, it.info, 4, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   if (hinfo != 0) {
     char b[32];
     snprintf(b, sizeof b, "%d", hinfo);

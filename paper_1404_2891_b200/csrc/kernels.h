@@ -98,12 +98,6 @@ void frob2_launch(const double2* A, int64_t lda, int64_t n, double* partial, int
 // partial[b] = sum_{c = b mod nparts} sum_i conj(U[i][c]) Q[i][c]  (nparts blocks, host sums in order)
 void cdot_launch(const double2* U, int64_t ldu, const double2* Q, int64_t ldq, int64_t n, int64_t m, double2* partial,
                  int nparts, cudaStream_t s);
-// Reduced eigenproblem on one CTA (reduced_eig.cu), m <= RE_MAXM: H (m x m, overwritten) ->
-// eigenvalues lam, Schur vectors Z, eigenvectors Y of the Schur form (W = Z Y); info[0] = 0, or 1
-// if the QR iteration did not converge.  Returns false (nothing launched) if m is out of range.
-constexpr int RE_MAXM = 160;
-bool reduced_eig_launch(double2* H, int m, int64_t ldh, double2* Z, int64_t ldz, double2* lam, double2* Y, int64_t ldy,
-                        int32_t* info, cudaStream_t s);
 // Scale columns of X by 1/xn[c] and rows of W by same: X[:,c] /= xn[c], W[:,c] /= xn[c]
 void colscale_launch(double2* X, int64_t ldx, int64_t n, double2* W, int64_t ldw, int64_t m,
                      const double* xn, cudaStream_t s);

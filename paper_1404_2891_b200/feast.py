@@ -34,27 +34,10 @@ EXPORTS = ["feast_init", "feast_workspace_bytes", "feast_bind_workspace", "feast
            "feast_project_left", "feast_project_bi", "feast_reduce", "feast_set_allreduce", "feast_iterate",
            "feast_node_stats", "feast_factor_cache", "feast_set_real_pencil",
            "feast_set_complex_symmetric", "feast_estimate_count", "feast_set_contour", "feast_filter",
-           "feast_small_eig", "feast_last_launch_count", "feast_profile", "feast_profile_summary",
+           "feast_last_launch_count", "feast_profile", "feast_profile_summary",
            "feast_profile_records", "feast_last_error",
            "feast_version", "feast_destroy"]
 K_CLASSES = ["shift", "panel", "laswp", "trsm", "zgemm", "perm", "accum", "other"]
-
-
-def small_eig(M: torch.Tensor):
-    """Eigenvalues and right eigenvectors of a small (m <= 160) complex matrix on the GPU with the
-    library's one-CTA Hessenberg-QR solver (the reduced eigenproblem of feast_iterate)."""
-    lib = load_library()
-    m = M.shape[0]
-    Mc = M.to(torch.complex128).t().contiguous().t()
-    lam = torch.empty(m, dtype=torch.complex128, device=M.device)
-    W = empty_colmajor(m, m, M.device)
-    work = torch.empty(3 * m * m * 16 + 256, dtype=torch.uint8, device=M.device)
-    rc = lib.feast_small_eig(m, ctypes.c_void_p(Mc.data_ptr()), m, ctypes.c_void_p(lam.data_ptr()),
-                             ctypes.c_void_p(W.data_ptr()), m, ctypes.c_void_p(work.data_ptr()), work.numel(),
-                             ctypes.c_void_p(torch.cuda.current_stream(M.device).cuda_stream))
-    if rc != OK:
-        raise FeastError(rc, "feast_small_eig failed")
-    return lam, W
 
 
 class FeastError(RuntimeError):
@@ -94,7 +77,6 @@ def load_library(path: str = LIB_PATH):
     lib.feast_estimate_count.argtypes = [P, P, I64, P, I64, P, I64, P, I64, P]
     lib.feast_set_contour.argtypes = [P, I32, P, P, I32, I32]
     lib.feast_filter.argtypes = [P, I64, P, P]
-    lib.feast_small_eig.argtypes = [I64, P, I64, P, P, I64, P, SZ, P]
     lib.feast_profile.argtypes = [P, I32]
     lib.feast_profile_summary.argtypes = [P, I32, P, P, P, P]
     lib.feast_profile_records.argtypes = [P, I64, P, P, P, P, P, P]

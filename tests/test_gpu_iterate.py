@@ -83,26 +83,3 @@ def test_c1_iterate_with_factor_cache_matches():
     c0, c1 = _converged(outs[0]), _converged(outs[1])
     assert c0.sum() == c1.sum() >= 1
     assert _match(np.asarray(outs[0]["lam"])[c0], np.asarray(outs[1]["lam"])[c1], 1e-10 * s.r)
-
-
-def test_iterate_with_own_reduced_eigensolver(monkeypatch):
-    """FEAST_EIG=own: feast_iterate solves the reduced problem with the one-CTA solver; the C1
-    Ritz values inside the contour match those of the default (cuSOLVER) path."""
-    import numpy as np
-    import synth
-    from paper_1404_2891_b200 import Feast, feast as fb
-    from gpu_util import dev
-    P = synth.make_pencil("C1")
-    s = P.spec
-    outs = []
-    for mode in ("cusolver", "own"):
-        monkeypatch.setenv("FEAST_EIG", mode)
-        f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, True)
-        X = dev(P.X0)
-        for _ in range(s.iters):
-            out = f.iterate(dev(P.A), None, X)
-        lam = np.array(out["lam"])
-        ok = (np.array(out["flags"]) & 1).astype(bool) & (np.array(out["resid"]) < 1e-10)
-        outs.append(np.sort_complex(lam[ok]))
-    assert len(outs[0]) == len(outs[1]) > 0
-    assert np.max(np.abs(outs[0] - outs[1])) < 1e-10
