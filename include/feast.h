@@ -34,10 +34,13 @@
  *
  * MULTI-GPU (§5.5: parallelism over the linear systems)
  *   Rank r of `world` owns the contiguous node block [r q/world, (r+1) q/world) (reading R17);
- *   q % world must be 0.  feast_project / feast_project_left return this rank's PARTIAL sum
- *   over its own nodes.  The node sum across ranks is one all-reduce of n x m0 complex128,
- *   which feast_iterate performs through the callback registered with feast_set_allreduce
- *   (the Python binding registers torch.distributed.all_reduce over NCCL).
+ *   q % world must be 0.  Every projector call (feast_project, _left, _bi, feast_estimate_count,
+ *   feast_iterate) returns the FULL node sum on every rank: after its own nodes it performs the
+ *   node sum across ranks (§8(a) a6) as one SUM all-reduce of the n x m0 block(s) (Q and QL
+ *   packed into one buffer) through the callback registered with feast_set_allreduce (the
+ *   Python binding registers torch.distributed.all_reduce: NCCL on GPUs).  With world > 1 and
+ *   no callback these calls return FEAST_E_COMM, unless feast_set_partial(h, 1) asked for this
+ *   rank's partial sum (the caller then sums over ranks itself).
  */
 #ifndef FEAST_B200_H
 #define FEAST_B200_H
@@ -149,15 +152,16 @@ int feast_bind_workspace(feast_handle h, void* dev_ptr, size_t bytes);
  * be NULL. */
 int feast_nodes(feast_handle h, int32_t* q, double* z, double* w, int32_t* j0, int32_t* j1);
 
-/* Right projector, this rank's partial sum (eq. Rasp):
- *   Q = sum_{j owned} w_j (z_j B - A)^{-1} (B X)       (B = NULL when b_is_identity)
+/* Right projector (eq. Rasp), node-summed over the ranks (see MULTI-GPU):
+ *   Q = sum_j w_j (z_j B - A)^{-1} (B X)       (B = NULL when b_is_identity)
  * A, B: n x n; X, Q: n x m0.  Q is overwritten (X and Q must not alias).
- * Returns FEAST_OK, FEAST_W_ILLCOND, FEAST_E_SINGULAR, FEAST_E_ARG, FEAST_E_STATE, FEAST_E_CUDA. */
+ * Returns FEAST_OK, FEAST_W_ILLCOND, FEAST_E_SINGULAR, FEAST_E_ARG, FEAST_E_STATE, FEAST_E_CUDA,
+ * FEAST_E_COMM (world > 1: no callback registered and partial mode off, or the callback failed). */
 int feast_project(feast_handle h, const void* A, int64_t lda, const void* B, int64_t ldb,
                   const void* X, int64_t ldx, void* Q, int64_t ldq);
 
-/* Left projector, this rank's partial sum (eq. Lasp, P:424-439 read as R4):
- *   QL = sum_{j owned} conj(w_j) (z_j B - A)^{-H} (B^H V)
+/* Left projector (eq. Lasp, P:424-439 read as R4), node-summed over the ranks:
+ *   QL = sum_j conj(w_j) (z_j B - A)^{-H} (B^H V)
  * solved with the conjugate-transposed factors of the same LU. */
 int feast_project_left(feast_handle h, const void* A, int64_t lda, const void* B, int64_t ldb,
                        const void* V, int64_t ldv, void* QL, int64_t ldql);
@@ -195,8 +199,16 @@ int feast_estimate_count(feast_handle h, const void* A, int64_t lda, const void*
 typedef int (*feast_allreduce_fn)(void* buf, int64_t count, void* cuda_stream, void* user);
 int feast_set_allreduce(feast_handle h, feast_allreduce_fn fn, void* user);
 
+/* Partial mode (world > 1): enable = 1 makes feast_project / _left / _bi / feast_estimate_count
+ * return this rank's PARTIAL sum over its own nodes [j0, j1) with no collective (for callers
+ * that reduce over ranks themselves, or several "virtual ranks" driven from one process).
+ * feast_iterate then returns FEAST_E_STATE.  Default 0 (full node sum through the callback). */
+int feast_set_partial(feast_handle h, int32_t enable);
+
 /* One FEAST iteration (R-FEAST P:503-517 / Bi-FEAST P:520-537):
- *   project (+ all-reduce), orthonormalise U^ (and V^) (reading R13), reduce, solve the
+ *   project (+ node sum over the ranks), orthonormalise U^ (and V^) (reading R13), reduce (with
+ *   world > 1 the rows of A Q, B Q and of the residual block A x - l B x are sharded over the
+ *   ranks: the m0 x m0 partials and the m0 squared residual norms are all-reduced), solve the
  *   m0 x m0 eigenproblem (outside the hot path; cuSOLVER), X <- U^ W with unit columns,
  *   Bi: V <- V^ Z with Z = (B^ W)^-H (reading R5).
  * X (n x m0, device) in/out; V (bi only, else NULL) in/out.

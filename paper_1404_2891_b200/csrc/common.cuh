@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #define FEAST_DEV __device__ __forceinline__
 
 FEAST_DEV double2 cmul(double2 a, double2 b) {
@@ -40,5 +42,14 @@ FEAST_DEV double2 cdiv(double2 a, double2 b) {
 // Launch-count accounting (bench "gpu_launches"): every launcher bumps this counter.
 namespace feast {
 extern thread_local int64_t g_launches;
+// Kernel attributes (dynamic smem size, non-portable clusters) belong to the CURRENT device: a
+// launcher configures its kernel once per device.  Returns true the first time it is called for
+// the current device with this mask (thread-safe; a race only repeats the idempotent setting).
+inline bool first_use_on_device(std::atomic<uint64_t>& mask) {
+  int d = 0;
+  cudaGetDevice(&d);
+  const uint64_t bit = 1ull << (d & 63);
+  return !(mask.fetch_or(bit) & bit);
+}
 inline void count_launch(int k = 1) { g_launches += k; }
 }  // namespace feast

@@ -16,6 +16,8 @@
 #include <cstring>
 #include <ctime>
 #include <string>
+#include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "../../include/feast.h"
@@ -125,6 +127,8 @@ struct feast_ctx {
   int64_t glaunches = 0;
   feast_allreduce_fn ar = nullptr;
   void* ar_user = nullptr;
+  bool partial = false;               // feast_set_partial: return this rank's partial node sum
+  double2* NS = nullptr;              // node-sum staging block [Q | QL] (n x m0 each, ld n), world > 1
   std::string err;
   int64_t launches = 0;
 };
@@ -737,7 +741,8 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
            h->info + (j + b0), b1 - b0, g ? h->gs[g] : h->stream, g ? h->gside[g] : h->side, g ? h->gev_a[g] : h->ev_a,
            g ? h->gev_p[g] : h->ev_p, (h->stagger && g + 1 < G) ? h->gev_first[g] : nullptr,
            h->prof_serial ? nullptr : h->gx[g], h->gev_t[g], h->gev_x[g]};
-      if (g) cudaStreamWaitEvent(v.sm, (h->stagger && g > 0) ? h->gev_first[g - 1] : h->ev_fork, 0);
+      // (gev_first is recorded only by an LuRun: the factor-cache path waits on the fork)
+      if (g) cudaStreamWaitEvent(v.sm, (h->stagger && !reuse) ? h->gev_first[g - 1] : h->ev_fork, 0);
       vs.push_back(v);
       if (!reuse) {
         feast::stats_init_launch(v.stats, v.info, v.nbat, v.sm);
@@ -821,8 +826,39 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
 // Driver: enqueue the sequence (replaying a CUDA graph of it when the call repeats with the same
 // pointers: the second identical call is captured, later ones replay it), then read back the
 // pivot diagnostics.
+// a6: the node sum over ranks (parallelism over the linear systems): one SUM all-reduce
+// through the registered callback of the n x m0 block(s) this rank accumulated.  Q and QL are
+// packed into the contiguous staging block [Q | QL] (ld = n) so that the callback sees one flat
+// float64 buffer (any caller ld) and Bi-FEAST's two blocks travel in one collective.
+int node_sum(feast_ctx* h, double2* Q, int64_t ldq, double2* QL, int64_t ldql) {
+  if (h->world <= 1 || h->partial) return FEAST_OK;
+  if (!h->ar) return fail(h, FEAST_E_COMM, "world > 1 needs feast_set_allreduce (or feast_set_partial)%s");
+  const int64_t n = h->n, m = h->m0;
+  double2* blk[2] = {Q, QL};
+  const int64_t lds[2] = {ldq, ldql};
+  int nb = 0;
+  for (int k = 0; k < 2; ++k)
+    if (blk[k]) {
+      CUDA_TRY(h, cudaMemcpy2DAsync(h->NS + nb * n * m, n * 16, blk[k], lds[k] * 16, n * 16, m, cudaMemcpyDeviceToDevice,
+                                    h->stream));
+      ++nb;
+    }
+  if (nb == 0) return FEAST_OK;
+  if (h->ar(h->NS, 2 * n * m * nb, h->stream, h->ar_user)) return fail(h, FEAST_E_COMM, "all-reduce failed%s");
+  nb = 0;
+  for (int k = 0; k < 2; ++k)
+    if (blk[k]) {
+      CUDA_TRY(h, cudaMemcpy2DAsync(blk[k], lds[k] * 16, h->NS + nb * n * m, n * 16, n * 16, m, cudaMemcpyDeviceToDevice,
+                                    h->stream));
+      ++nb;
+    }
+  return FEAST_OK;
+}
+
 int project_impl(feast_ctx* h, const double2* A, int64_t lda, const double2* B, int64_t ldb, const double2* X,
                  int64_t ldx, const double2* V, int64_t ldv, double2* Q, int64_t ldq, double2* QL, int64_t ldql) {
+  if (h->world > 1 && !h->partial && !h->ar)
+    return fail(h, FEAST_E_COMM, "world > 1 needs feast_set_allreduce (or feast_set_partial)%s");
   const int64_t t0 = feast::g_launches;
   const int owned = h->j1 - h->j0;
   const bool reuse = h->cache_on && h->cache_valid && h->batch >= owned && h->cache_A == A && h->cache_B == B;
@@ -878,6 +914,7 @@ int project_impl(feast_ctx* h, const double2* A, int64_t lda, const double2* B, 
   }
   if (!reuse && h->cache_on && h->batch >= owned) { h->cache_valid = true; h->cache_A = A; h->cache_B = B; }
   CUDA_TRY(h, cudaGetLastError());
+  if (int e = node_sum(h, Q, ldq, QL, ldql)) return e;
   h->launches = feast::g_launches - t0;
   // pivot diagnostics of the owned units, reported per node (both poles of an orbit share it)
   std::vector<double> st(2 * (size_t)h->nu);
@@ -1106,40 +1143,50 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   return FEAST_OK;
 }
 
+// Workspace layout.  base == nullptr: size only (the handle's pointers are left untouched, so the
+// call is safe after a workspace is bound).
 static size_t layout(feast_ctx* h, char* base) {
   const int64_t n = h->n, m = h->m0, ld = h->ldc;
   size_t off = 0;
-  auto take = [&](size_t b) { size_t o = off; off += align256(b); return base ? (void*)(base + o) : nullptr; };
+  auto take = [&](size_t b) { size_t o = off; off += align256(b); return o; };
+  auto set = [&](auto*& ptr, size_t b, bool want = true) {
+    if (!want) { if (base) ptr = nullptr; return; }
+    const size_t o = take(b);
+    if (base) ptr = reinterpret_cast<std::remove_reference_t<decltype(ptr)>>(base + o);
+  };
   const int64_t mr = h->mr;
-  h->Cw = (double2*)take((size_t)h->batch * ld * (n + mr) * 16);  // [C_j | R (| conj R)] (augmented)
-  h->Y = (double2*)take((size_t)h->batch * ld * mr * 16);            // right solves with cached factors
-  h->YL = h->mode == FEAST_BI ? (double2*)take((size_t)h->batch * ld * mr * 16) : nullptr;
-  h->R = !h->b_id ? (double2*)take((size_t)ld * m * 16) : nullptr;
-  h->RL = (!h->b_id && h->mode == FEAST_BI) ? (double2*)take((size_t)ld * m * 16) : nullptr;
-  h->AQ = (double2*)take((size_t)ld * m * 16);
-  h->BQ = !h->b_id ? (double2*)take((size_t)ld * m * 16) : nullptr;
+  const bool bi = h->mode == FEAST_BI;
+  set(h->Cw, (size_t)h->batch * ld * (n + mr) * 16);  // [C_j | R (| conj R)] (augmented)
+  set(h->Y, (size_t)h->batch * ld * mr * 16);           // right solves with cached factors
+  set(h->YL, (size_t)h->batch * ld * mr * 16, bi);
+  set(h->R, (size_t)ld * m * 16, !h->b_id);
+  set(h->RL, (size_t)ld * m * 16, !h->b_id && bi);
+  set(h->AQ, (size_t)ld * m * 16);
+  set(h->BQ, (size_t)ld * m * 16, !h->b_id);
   // split-K partials: up to 6 n x m0 slices (grids that small need splits; large ones do not),
   // capped at 512 MB
   h->sk_elems = std::max<int64_t>(16 * m * m, std::min<int64_t>((int64_t)6 * ld * m, (int64_t)1 << 25));
-  h->SK = (double2*)take((size_t)h->sk_elems * 16);
+  set(h->SK, (size_t)h->sk_elems * 16);
   h->nblk = (n + 63) / 64;
   h->inv_stride = h->nblk * 2 * 4096;
-  h->Inv = (double2*)take((size_t)h->batch * h->inv_stride * 16);
-  h->ipiv = (int32_t*)take((size_t)h->batch * n * 4);
-  h->perm = (int32_t*)take((size_t)h->batch * n * 4);
-  h->iperm = (int32_t*)take((size_t)h->batch * n * 4);
-  h->zd = (double2*)take((size_t)h->nu * 16);
-  h->wd = (double2*)take((size_t)h->nu * 16);
-  h->wpd = h->real ? (double2*)take((size_t)h->nu * 16) : nullptr;
-  h->stats = (double*)take((size_t)h->nu * 16);
-  h->info = (int32_t*)take((size_t)h->nu * 4);
-  h->realviol = (int32_t*)take(16);
+  set(h->Inv, (size_t)h->batch * h->inv_stride * 16);
+  set(h->ipiv, (size_t)h->batch * n * 4);
+  set(h->perm, (size_t)h->batch * n * 4);
+  set(h->iperm, (size_t)h->batch * n * 4);
+  set(h->zd, (size_t)h->nu * 16);
+  set(h->wd, (size_t)h->nu * 16);
+  set(h->wpd, (size_t)h->nu * 16, h->real);
+  set(h->stats, (size_t)h->nu * 16);
+  set(h->info, (size_t)h->nu * 4);
+  set(h->realviol, 16);
+  set(h->NS, (size_t)n * m * (bi ? 2 : 1) * 16, h->world > 1);   // node-sum staging [Q | QL]
   return off;
 }
 
 int feast_workspace_bytes(feast_handle h, size_t* bytes) {
   if (!h || !bytes) return FEAST_E_ARG;
   *bytes = layout(h, nullptr);
+  if (h->ws) return FEAST_OK;   // bound: the batch (and the layout) stay frozen
   if (h->max_batch == 0) {
     // "all owned nodes" means all that fit: shrink the concurrent batch until the workspace
     // takes at most 90 % of the device memory free now (C5 on one B200: 16 nodes x 17.7 GB of
@@ -1282,16 +1329,12 @@ int feast_estimate_count(feast_handle h, const void* A, int64_t lda, const void*
   int e = check_args_common(h, A, lda, B, ldb);
   if (e) return e;
   if (!U || !Q || !estimate || ldu < h->n || ldq < h->n) return fail(h, FEAST_E_ARG, "U/Q/estimate null or ld < n%s");
-  if (h->world > 1 && !h->ar) return fail(h, FEAST_E_COMM, "world > 1 needs feast_set_allreduce%s");
   Join j_(h);
   const int64_t n = h->n, m = h->m0;
-  // Q = rho(B^-1 A) U (this rank's nodes, then the node sum over ranks)
+  // Q = rho(B^-1 A) U (this rank's nodes, then the node sum over ranks inside project_impl)
   const int pst = project_impl(h, (const double2*)A, lda, (const double2*)B, ldb, (const double2*)U, ldu, nullptr, 0,
                                (double2*)Q, ldq, nullptr, 0);
   if (pst < 0) return pst;
-  if (h->world > 1)
-    for (int64_t c = 0; c < m; ++c)
-      if (h->ar((double2*)Q + c * ldq, 2 * n, h->stream, h->ar_user)) return fail(h, FEAST_E_COMM, "all-reduce failed%s");
   // Hutchinson trace estimate: m ~ tr rho(B^-1 A) ~ Re tr(U^H Q) / m0 (deterministic block sums)
   constexpr int NP = 64;
   feast::cdot_launch((const double2*)U, ldu, (const double2*)Q, ldq, n, m, h->SK, NP, h->stream);
@@ -1311,6 +1354,12 @@ int feast_set_allreduce(feast_handle h, feast_allreduce_fn fn, void* user) {
   return FEAST_OK;
 }
 
+int feast_set_partial(feast_handle h, int32_t enable) {
+  if (!h) return FEAST_E_ARG;
+  h->partial = enable != 0;
+  return FEAST_OK;
+}
+
 int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int64_t ldb, void* X, int64_t ldx,
                   void* V, int64_t ldv, double* ritz, double* resid, int32_t* flags) {
   int e = check_args_common(h, A, lda, B, ldb);
@@ -1318,6 +1367,7 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
   const bool bi = h->mode == FEAST_BI;
   if (!X || ldx < h->n || (bi && (!V || ldv < h->n))) return fail(h, FEAST_E_ARG, "X/V null or ld < n%s");
   if (h->world > 1 && !h->ar) return fail(h, FEAST_E_COMM, "world > 1 needs feast_set_allreduce%s");
+  if (h->world > 1 && h->partial) return fail(h, FEAST_E_STATE, "feast_iterate needs the full node sum (partial mode on)%s");
   Join j_(h);
   e = ensure_iter_mem(h);
   if (e) return e;
@@ -1329,11 +1379,7 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
                               (const double2*)V, ldv, it.Qr, n, it.Ql, n)
                : project_impl(h, (const double2*)A, lda, (const double2*)B, ldb, (const double2*)X, ldx, nullptr, 0,
                               it.Qr, n, nullptr, 0);
-  if (pst < 0) return pst;
-  if (h->world > 1) {
-    if (h->ar(it.Qr, 2 * n * m, h->stream, h->ar_user)) return fail(h, FEAST_E_COMM, "all-reduce failed%s");
-    if (bi && h->ar(it.Ql, 2 * n * m, h->stream, h->ar_user)) return fail(h, FEAST_E_COMM, "all-reduce failed%s");
-  }
+  if (pst < 0) return pst;   // (node-summed over the ranks inside project_impl)
   // orthonormalise U^ (and V^) (reading R13), cuSOLVER Householder QR
   // FEAST_TIMING=1: host wall time of the iteration phases (stream-synchronised), to stderr
   static const bool timing = getenv("FEAST_TIMING") != nullptr;
@@ -1358,8 +1404,8 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
   tmark("project");
   if ((e = orth(it.Qr))) return e;
   if (bi && (e = orth(it.Ql))) return e;
-  // step 4 / 6: reduced matrices
-  e = reduce_impl(h, A, lda, B, ldb, it.Qr, n, bi ? it.Ql : nullptr, n, it.Ah, m, it.Bh, m, false);
+  // step 4 / 6: reduced matrices, rows of A Q (B Q) sharded over the ranks
+  e = reduce_impl(h, A, lda, B, ldb, it.Qr, n, bi ? it.Ql : nullptr, n, it.Ah, m, it.Bh, m, true);
   if (e) return e;
   tmark("qr+reduce");
   // step 5 / 7 (outside the hot path): M = Bh^-1 Ah, eig(M) -> lam, W
@@ -1398,16 +1444,20 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
     gemm_gen(h, n, m, m, false, it.Ql, n, it.Z, m, (double2*)V, ldv, one, zero);
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   }
-  // residuals (reading R11): A x - l B x with x = U^ W (unit columns)
-  gemm_gen(h, n, m, m, false, h->AQ, ld, it.W, m, it.AX, n, one, zero);
+  // residuals (reading R11): A x - l B x with x = U^ W (unit columns), over this rank's rows of
+  // A Q (B Q) when a7 was sharded: squared column norms, summed over the ranks (one m-vector)
+  const bool shard = h->world > 1 && h->ar != nullptr;
+  const int64_t r0 = shard ? h->rank * n / h->world : 0, r1 = shard ? (h->rank + 1) * n / h->world : n, nr = r1 - r0;
+  gemm_gen(h, nr, m, m, false, h->AQ + r0, ld, it.W, m, it.AX + r0, n, one, zero);
   const double2* BXp = (const double2*)X;
   int64_t ldbx = ldx;
-  if (!h->b_id) { gemm_gen(h, n, m, m, false, h->BQ, ld, it.W, m, it.BX, n, one, zero); BXp = it.BX; ldbx = n; }
+  if (!h->b_id) { gemm_gen(h, nr, m, m, false, h->BQ + r0, ld, it.W, m, it.BX + r0, n, one, zero); BXp = it.BX; ldbx = n; }
   if (ldbx != n) {  // resid kernel uses one ld: copy X into BX when B = I and ldx != n
     CUDA_TRY(h, cudaMemcpy2DAsync(it.BX, n * 16, X, ldx * 16, n * 16, m, cudaMemcpyDeviceToDevice, h->stream));
     BXp = it.BX;
   }
-  feast::resid_launch(it.AX, BXp, BXp, n, it.lam, n, m, it.rn, it.xn, h->stream);
+  feast::resid_launch(it.AX + r0, BXp + r0, BXp + r0, n, it.lam, nr, m, it.rn, nullptr, h->stream, true);
+  if (shard && h->ar(it.rn, m, h->stream, h->ar_user)) return fail(h, FEAST_E_COMM, "all-reduce failed%s");
   feast::frob2_launch((const double2*)A, lda, n, it.fr, 256, h->stream);
   std::vector<double2> lam(m);
   std::vector<double> rn(m), fr(256);
@@ -1421,7 +1471,7 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
   tmark("ritz+resid");
   for (int64_t c = 0; c < m; ++c) {
     if (ritz) { ritz[2 * c] = lam[c].x; ritz[2 * c + 1] = lam[c].y; }
-    const double rp = rn[c];  // ||x|| = 1
+    const double rp = std::sqrt(rn[c]);  // ||x|| = 1
     if (resid) resid[c] = an > 0 ? rp / an : rp;
     const bool inside = inside_contour(h, lam[c].x, lam[c].y);
     if (flags) flags[c] = (inside ? 1 : 0) | ((inside && rp <= 1e-4) ? 2 : 0);

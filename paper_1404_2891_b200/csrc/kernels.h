@@ -90,9 +90,10 @@ void accum_launch(double2* Q, int64_t ldq, Batched Y, const double2* w, const do
 void splitk_reduce_launch(double2* C, int64_t ldc, const double2* P, int64_t M, int64_t N, int splits,
                           double2 alpha, double2 beta, cudaStream_t s);
 
-// Column residual norms: out[c] = || AX[:,c] - lam_c BX[:,c] ||_2 and xn[c] = || X[:,c] ||_2.
+// Column residual norms over n rows: out[c] = || AX[:,c] - lam_c BX[:,c] ||_2 and xn[c] = || X[:,c] ||_2
+// (xn may be null); squared = true writes the squared norms (partial sums of a row-sharded block).
 void resid_launch(const double2* AX, const double2* BX, const double2* X, int64_t ld, const double2* lam,
-                  int64_t n, int64_t m, double* out, double* xn, cudaStream_t s);
+                  int64_t n, int64_t m, double* out, double* xn, cudaStream_t s, bool squared = false);
 // || A ||_F^2 partial sums into out (one double, must be zeroed) — deterministic two-pass.
 void frob2_launch(const double2* A, int64_t lda, int64_t n, double* partial, int nparts, cudaStream_t s);
 // partial[b] = sum_{c = b mod nparts} sum_i conj(U[i][c]) Q[i][c]  (nparts blocks, host sums in order)

@@ -305,10 +305,9 @@ panel_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__ ipiv
 template <int W, int S>
 void panel_launch_t(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info,
                     int batch, int cs, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};
+  if (first_use_on_device(configured)) {
     cudaFuncSetAttribute(panel_kernel<W, S>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    configured = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(batch * cs), 1, 1);
@@ -461,10 +460,9 @@ void laswp_launch(Batched C, int64_t n, int64_t k, int cnt, const int32_t* ipiv,
   // 1730 ms) the permutation kernel loses in the overlapped schedule: its many CTAs and row tables
   // compete with the trailing-update GEMMs more than the short chain kernel does.
   if (use_perm && 2 * cnt <= 32 * 16 && smem <= 96 * 1024) {
-    static bool configured = false;
-    if (!configured) {
+    static std::atomic<uint64_t> configured{0};
+    if (first_use_on_device(configured)) {
       cudaFuncSetAttribute(laswp_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-      configured = true;
     }
     const int64_t per_cta = (int64_t)LP_WARPS * LP_COLS;
     dim3 grid((unsigned)((c1 - c0 + per_cta - 1) / per_cta), (unsigned)batch);
@@ -505,10 +503,9 @@ __global__ void perm_kernel(const int32_t* __restrict__ ipiv_all, int32_t* __res
 
 void perm_launch(const int32_t* ipiv, int32_t* perm, int32_t* iperm, int64_t n, int batch, cudaStream_t s) {
   ProfScope ps_(K_PERM, 0.0, (double)batch * n * 12.0, s);
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};
+  if (first_use_on_device(configured)) {
     cudaFuncSetAttribute(perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
   }
   perm_kernel<<<batch, 256, (size_t)n * sizeof(int32_t), s>>>(ipiv, perm, iperm, n);
   count_launch();
@@ -680,7 +677,7 @@ __device__ double block_sum(double v) {
 }
 
 __global__ void resid_kernel(const double2* AX, const double2* BX, const double2* X, int64_t ld,
-                             const double2* lam, int64_t n, double* out, double* xn) {
+                             const double2* lam, int64_t n, double* out, double* xn, bool squared) {
   const int64_t c = blockIdx.x;
   const double2 l = lam[c];
   double r2 = 0.0, x2 = 0.0;
@@ -692,13 +689,16 @@ __global__ void resid_kernel(const double2* AX, const double2* BX, const double2
   }
   r2 = block_sum(r2);
   x2 = block_sum(x2);
-  if (threadIdx.x == 0) { out[c] = sqrt(r2); xn[c] = sqrt(x2); }
+  if (threadIdx.x == 0) {
+    out[c] = squared ? r2 : sqrt(r2);
+    if (xn) xn[c] = squared ? x2 : sqrt(x2);
+  }
 }
 
 void resid_launch(const double2* AX, const double2* BX, const double2* X, int64_t ld, const double2* lam,
-                  int64_t n, int64_t m, double* out, double* xn, cudaStream_t s) {
+                  int64_t n, int64_t m, double* out, double* xn, cudaStream_t s, bool squared) {
   ProfScope ps_(K_OTHER, 0.0, 0.0, s);
-  resid_kernel<<<(unsigned)m, 256, 0, s>>>(AX, BX, X, ld, lam, n, out, xn);
+  resid_kernel<<<(unsigned)m, 256, 0, s>>>(AX, BX, X, ld, lam, n, out, xn, squared);
   count_launch();
 }
 

@@ -504,12 +504,11 @@ void launch_s(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* sta
   const int64_t L = n - k;
   const int Lc = (int)((L + cs - 1) / cs);
   const size_t smem = (size_t)Lc * (w > WC ? w - WC : 0) * sizeof(double2);
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};
+  if (first_use_on_device(configured)) {
     cudaFuncSetAttribute(panel_smem_kernel<S, WC, NT, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(panel_smem_kernel<S, WC, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(panel_smem_kernel<S, WC, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(batch * cs), 1, 1);

@@ -144,11 +144,10 @@ template <bool LOWER, bool UNIT, bool CONJT>
 void trsm_t(Batched T, Batched X, int nb, int64_t ncols, int batch, cudaStream_t s) {
   constexpr int CPW = 1;
   const size_t smem = (size_t)(NB * LDT + NB) * sizeof(double2);
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};
+  if (first_use_on_device(configured)) {
     cudaFuncSetAttribute(trsm_warp_kernel<LOWER, UNIT, CONJT, CPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    configured = true;
   }
   dim3 grid((unsigned)((ncols + WARPS * CPW - 1) / (WARPS * CPW)), (unsigned)batch);
   trsm_warp_kernel<LOWER, UNIT, CONJT, CPW><<<grid, 32 * WARPS, smem, s>>>(T, X, nb, ncols);
@@ -214,10 +213,9 @@ void trtri_t(Batched C, int64_t n, int64_t kb0, int64_t nblocks, double2* inv, i
              int batch, cudaStream_t s) {
   constexpr int TR_CB = NB / (TW * TCPW);
   const size_t smem = (size_t)(NB * LDT + NB) * sizeof(double2);
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};
+  if (first_use_on_device(configured)) {
     cudaFuncSetAttribute(trtri_kernel<TW, TCPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
   }
   dim3 grid((unsigned)batch, which == 2 ? 2u : 1u, (unsigned)(nblocks * TR_CB));
   trtri_kernel<TW, TCPW><<<grid, 32 * TW, smem, s>>>(C, n, kb0, inv, inv_node_stride, which);

@@ -233,10 +233,9 @@ template <int BM, int BN, int WGM, int WGN, int ST, int MINB, bool CONJA, int MO
 void launch3(const ZgemmArgs& p, cudaStream_t s) {
   using T = Tile<BM, BN, WGM, WGN, ST, BK>;
   auto kern = zgemm_dmma_kernel<BM, BN, WGM, WGN, ST, MINB, CONJA, MODE, PREC, BK>;
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};
+  if (first_use_on_device(configured)) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_BYTES);
-    configured = true;
   }
   dim3 grid((unsigned)((p.N + BN - 1) / BN), (unsigned)((p.M + BM - 1) / BM), (unsigned)p.batch);
   kern<<<grid, T::THREADS, T::SMEM_BYTES, s>>>(p);

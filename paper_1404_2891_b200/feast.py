@@ -1,8 +1,10 @@
 """Thin Python binding of the C ABI in include/feast.h (argument marshalling only).
 
 Every step of the FEAST hot path runs in libfeast_b200.so's sm_100a kernels; PyTorch only
-provides device memory, the CUDA stream and torch.distributed (the cross-rank node sum,
-P:910-913).  There is no CPU fallback: if the library is missing this module raises.
+provides device memory, the CUDA stream and torch.distributed: the library calls back into
+torch.distributed.all_reduce for the cross-rank node sum and the row-sharded
+assemblies, on its own stream.  There is no CPU fallback: if the library is missing this
+module raises.
 
 Matrices are complex128 COLUMN-MAJOR CUDA tensors (stride(0) == 1, stride(1) = ld >= rows),
 e.g. ``colmajor(torch.from_numpy(np.asfortranarray(a)))`` or ``empty_colmajor(n, m)``.
@@ -31,7 +33,8 @@ ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, c
 
 # every symbol include/feast.h declares (checked by tests/test_abi.py)
 EXPORTS = ["feast_init", "feast_workspace_bytes", "feast_bind_workspace", "feast_nodes", "feast_project",
-           "feast_project_left", "feast_project_bi", "feast_reduce", "feast_set_allreduce", "feast_iterate",
+           "feast_project_left", "feast_project_bi", "feast_reduce", "feast_set_allreduce", "feast_set_partial",
+           "feast_iterate",
            "feast_node_stats", "feast_factor_cache", "feast_set_real_pencil",
            "feast_set_complex_symmetric", "feast_estimate_count", "feast_set_contour", "feast_filter",
            "feast_last_launch_count", "feast_profile", "feast_profile_summary",
@@ -67,6 +70,7 @@ def load_library(path: str = LIB_PATH):
     lib.feast_project_bi.argtypes = [P, P, I64, P, I64, P, I64, P, I64, P, I64, P, I64]
     lib.feast_reduce.argtypes = [P, P, I64, P, I64, P, I64, P, I64, P, I64, P, I64]
     lib.feast_set_allreduce.argtypes = [P, ALLREDUCE_FN, P]
+    lib.feast_set_partial.argtypes = [P, I32]
     lib.feast_iterate.argtypes = [P, P, I64, P, I64, P, I64, P, I64, P, P, P]
     lib.feast_node_stats.argtypes = [P, P, P]
     lib.feast_last_launch_count.argtypes = [P]
@@ -98,24 +102,19 @@ def empty_colmajor(rows: int, cols: int, device="cuda", dtype=torch.complex128) 
     return torch.empty((cols, rows), dtype=dtype, device=device).t()
 
 
-def _ptr_ld(t, rows, name):
+def _ptr_ld(t, rows, name, device=None):
     if t is None:
         return None, 0
     if t.dtype != torch.complex128 or not t.is_cuda or t.dim() != 2:
         raise FeastError(E_ARG, f"{name} must be a 2-D complex128 CUDA tensor")
-    if t.shape[0] != rows or (t.shape[1] > 1 and t.stride(0) != 1):
+    if device is not None and t.device != device:
+        raise FeastError(E_ARG, f"{name} is on {t.device}, the handle on {device}")
+    if t.shape[0] != rows or (rows > 1 and t.stride(0) != 1):
         raise FeastError(E_ARG, f"{name} must be column-major with {rows} rows")
     ld = t.stride(1) if t.shape[1] > 1 else max(rows, 1)
+    if ld < rows:
+        raise FeastError(E_ARG, f"{name}: leading dimension {ld} < {rows} rows")
     return ctypes.c_void_p(t.data_ptr()), ld
-
-
-def allreduce_node_sum(t: torch.Tensor, group=None) -> torch.Tensor:
-    """The cross-rank node sum of the projector: in-place SUM all-reduce of a rank's
-    partial Q (complex128 is reduced as its float64 view).  No-op without a process group."""
-    import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(torch.view_as_real(t) if t.is_complex() else t, group=group)
-    return t
 
 
 def _dist_world(group=None) -> int:
@@ -123,6 +122,33 @@ def _dist_world(group=None) -> int:
     if dist.is_available() and dist.is_initialized():
         return dist.get_world_size(group)
     return 1
+
+
+def make_allreduce_callback(device, group=None):
+    """The feast_allreduce_fn the library calls for every cross-rank sum (the node sum of Q / QL,
+    the row-sharded a1 / a7 assemblies, the residual norms): SUM all-reduce of `count` float64
+    values at the raw pointer `buf`, in place, ordered on the library's stream.  The library
+    always passes one contiguous flat block (it packs Q and QL itself), so no tensor layout is
+    involved here.  `device` is the torch device of the buffers (cuda:k; "cpu" wraps a host
+    pointer — the CPU tests of this marshalling with gloo)."""
+    import torch.distributed as dist
+    device = torch.device(device)
+
+    def cb(buf, count, stream, user):
+        try:
+            if device.type == "cuda":
+                t = torch.as_tensor(_CudaPtr(buf, count), device=device)
+                with torch.cuda.stream(torch.cuda.ExternalStream(stream, device=device)):
+                    dist.all_reduce(t, group=group)   # enqueued on the library's stream
+            else:
+                import numpy as np
+                arr = np.ctypeslib.as_array(ctypes.cast(buf, ctypes.POINTER(ctypes.c_double)), shape=(int(count),))
+                dist.all_reduce(torch.from_numpy(arr), group=group)
+            return 0
+        except Exception:  # noqa: BLE001 — reported as FEAST_E_COMM by the library
+            return 1
+
+    return cb
 
 
 class _CudaPtr:
@@ -138,7 +164,11 @@ class Feast:
 
     def __init__(self, n, m0, center=0j, r=1.0, aspect=1.0, n_e=8, rule=RULE_TRAPEZOID, mode=RIGHT,
                  b_is_identity=True, rank=0, world=1, max_batch=0, device=None, group=None, real_pencil=False,
-                 complex_symmetric=False, segments=None, k_per_segment=8, segment_rule=RULE_TRAPEZOID):
+                 complex_symmetric=False, segments=None, k_per_segment=8, segment_rule=RULE_TRAPEZOID,
+                 partial=False):
+        """world > 1 needs an initialised torch.distributed process group of `world` ranks (the
+        library then returns node sums over all ranks), or partial=True: every projector call
+        returns this rank's partial sum over its own nodes (virtual ranks, caller-side sums)."""
         self.lib = load_library()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.stream = torch.cuda.current_stream(self.device)
@@ -175,34 +205,24 @@ class Feast:
         aligned = (base + 255) // 256 * 256
         self._check(self.lib.feast_bind_workspace(self.h, ctypes.c_void_p(aligned), int(nbytes.value)))
         self._ar = None
-        if self.world > 1 and _dist_world(group) == self.world:
-            # node sums (and the row-sharded a1 / a7 assemblies) through torch.distributed (NCCL);
-            # without an initialised process group of this size (e.g. virtual ranks in one
-            # process) no callback is registered and calls return this rank's partials
-            self._ar = ALLREDUCE_FN(self._allreduce_cb)
-            self._check(self.lib.feast_set_allreduce(self.h, self._ar, None))
+        self.partial = bool(partial)
+        if self.world > 1:
+            if self.partial:
+                self._check(self.lib.feast_set_partial(self.h, 1))
+            elif _dist_world(group) == self.world:
+                # node sums (and the row-sharded a1 / a7 assemblies) through torch.distributed
+                self._ar = ALLREDUCE_FN(make_allreduce_callback(self.device, group))
+                self._check(self.lib.feast_set_allreduce(self.h, self._ar, None))
+            else:
+                self.close()
+                raise FeastError(E_COMM, f"world={self.world} needs a torch.distributed process group of that "
+                                         f"size (found {_dist_world(group)}) or partial=True")
 
     # ------------------------------------------------------------------ helpers
     def _check(self, rc, allow_warn=True):
         if rc < 0 or (rc > 0 and not allow_warn):
             raise FeastError(rc, self.lib.feast_last_error(self.h).decode())
         return rc
-
-    def _allreduce_cb(self, buf, count, stream, user):
-        try:
-            import torch.distributed as dist
-            t = torch.as_tensor(_CudaPtr(buf, count), device=self.device)
-            with torch.cuda.stream(torch.cuda.ExternalStream(stream, device=self.device)):
-                dist.all_reduce(t, group=self.group)   # ordered on the library's stream
-            return 0
-        except Exception:  # noqa: BLE001 — reported as FEAST_E_COMM by the library
-            return 1
-
-    def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
-        """Node sum across ranks: in-place all-reduce of a partial Q."""
-        if self.world > 1:
-            allreduce_node_sum(t, self.group)
-        return t
 
     def close(self):
         if getattr(self, "h", None):
@@ -227,54 +247,48 @@ class Feast:
         ww = [complex(w[2 * i], w[2 * i + 1]) for i in range(q.value)]
         return zz, ww, j0.value, j1.value
 
-    def project(self, A, B, X, Q=None, allreduce=True):
-        """Q = sum_j w_j (z_j B - A)^-1 (B X); this rank's nodes, then the cross-rank sum."""
+    def project(self, A, B, X, Q=None):
+        """Q = sum_j w_j (z_j B - A)^-1 (B X), node-summed over the ranks by the library
+        (partial=True: this rank's nodes only)."""
         Q = empty_colmajor(self.n, self.m0, self.device) if Q is None else Q
-        pa, lda = _ptr_ld(A, self.n, "A")
-        pb, ldb = _ptr_ld(B, self.n, "B")
-        px, ldx = _ptr_ld(X, self.n, "X")
-        pq, ldq = _ptr_ld(Q, self.n, "Q")
+        pa, lda = _ptr_ld(A, self.n, "A", self.device)
+        pb, ldb = _ptr_ld(B, self.n, "B", self.device)
+        px, ldx = _ptr_ld(X, self.n, "X", self.device)
+        pq, ldq = _ptr_ld(Q, self.n, "Q", self.device)
         self.status = self._check(self.lib.feast_project(self.h, pa, lda, pb, ldb, px, ldx, pq, ldq))
-        if allreduce:
-            self.allreduce_(Q)
         return Q
 
-    def project_left(self, A, B, V, QL=None, allreduce=True):
+    def project_left(self, A, B, V, QL=None):
         QL = empty_colmajor(self.n, self.m0, self.device) if QL is None else QL
-        pa, lda = _ptr_ld(A, self.n, "A")
-        pb, ldb = _ptr_ld(B, self.n, "B")
-        pv, ldv = _ptr_ld(V, self.n, "V")
-        pq, ldq = _ptr_ld(QL, self.n, "QL")
+        pa, lda = _ptr_ld(A, self.n, "A", self.device)
+        pb, ldb = _ptr_ld(B, self.n, "B", self.device)
+        pv, ldv = _ptr_ld(V, self.n, "V", self.device)
+        pq, ldq = _ptr_ld(QL, self.n, "QL", self.device)
         self.status = self._check(self.lib.feast_project_left(self.h, pa, lda, pb, ldb, pv, ldv, pq, ldq))
-        if allreduce:
-            self.allreduce_(QL)
         return QL
 
-    def project_bi(self, A, B, X, V, Q=None, QL=None, allreduce=True):
+    def project_bi(self, A, B, X, V, Q=None, QL=None):
         Q = empty_colmajor(self.n, self.m0, self.device) if Q is None else Q
         QL = empty_colmajor(self.n, self.m0, self.device) if QL is None else QL
-        pa, lda = _ptr_ld(A, self.n, "A")
-        pb, ldb = _ptr_ld(B, self.n, "B")
-        px, ldx = _ptr_ld(X, self.n, "X")
-        pv, ldv = _ptr_ld(V, self.n, "V")
-        pq, ldq = _ptr_ld(Q, self.n, "Q")
-        pl, ldl = _ptr_ld(QL, self.n, "QL")
+        pa, lda = _ptr_ld(A, self.n, "A", self.device)
+        pb, ldb = _ptr_ld(B, self.n, "B", self.device)
+        px, ldx = _ptr_ld(X, self.n, "X", self.device)
+        pv, ldv = _ptr_ld(V, self.n, "V", self.device)
+        pq, ldq = _ptr_ld(Q, self.n, "Q", self.device)
+        pl, ldl = _ptr_ld(QL, self.n, "QL", self.device)
         self.status = self._check(self.lib.feast_project_bi(self.h, pa, lda, pb, ldb, px, ldx, pv, ldv, pq, ldq,
                                                             pl, ldl))
-        if allreduce:
-            self.allreduce_(Q)
-            self.allreduce_(QL)
         return Q, QL
 
     def reduce(self, A, B, Q, QL=None, Ahat=None, Bhat=None):
         Ahat = empty_colmajor(self.m0, self.m0, self.device) if Ahat is None else Ahat
         Bhat = empty_colmajor(self.m0, self.m0, self.device) if Bhat is None else Bhat
-        pa, lda = _ptr_ld(A, self.n, "A")
-        pb, ldb = _ptr_ld(B, self.n, "B")
-        pq, ldq = _ptr_ld(Q, self.n, "Q")
-        pl, ldl = _ptr_ld(QL, self.n, "QL")
-        p1, ld1 = _ptr_ld(Ahat, self.m0, "Ahat")
-        p2, ld2 = _ptr_ld(Bhat, self.m0, "Bhat")
+        pa, lda = _ptr_ld(A, self.n, "A", self.device)
+        pb, ldb = _ptr_ld(B, self.n, "B", self.device)
+        pq, ldq = _ptr_ld(Q, self.n, "Q", self.device)
+        pl, ldl = _ptr_ld(QL, self.n, "QL", self.device)
+        p1, ld1 = _ptr_ld(Ahat, self.m0, "Ahat", self.device)
+        p2, ld2 = _ptr_ld(Bhat, self.m0, "Bhat", self.device)
         self._check(self.lib.feast_reduce(self.h, pa, lda, pb, ldb, pq, ldq, pl, ldl, p1, ld1, p2, ld2))
         return Ahat, Bhat
 
@@ -284,10 +298,10 @@ class Feast:
         ritz = (ctypes.c_double * (2 * m))()
         res = (ctypes.c_double * m)()
         flags = (ctypes.c_int32 * m)()
-        pa, lda = _ptr_ld(A, self.n, "A")
-        pb, ldb = _ptr_ld(B, self.n, "B")
-        px, ldx = _ptr_ld(X, self.n, "X")
-        pv, ldv = _ptr_ld(V, self.n, "V")
+        pa, lda = _ptr_ld(A, self.n, "A", self.device)
+        pb, ldb = _ptr_ld(B, self.n, "B", self.device)
+        px, ldx = _ptr_ld(X, self.n, "X", self.device)
+        pv, ldv = _ptr_ld(V, self.n, "V", self.device)
         self.status = self._check(self.lib.feast_iterate(self.h, pa, lda, pb, ldb, px, ldx, pv, ldv, ritz, res,
                                                          flags))
         lam = [complex(ritz[2 * i], ritz[2 * i + 1]) for i in range(m)]
@@ -306,10 +320,10 @@ class Feast:
         """Eigenvalue-count estimate Re tr(U^H rho(B^-1 A) U) / m0 for a random block U (NEXT-3);
         returns (estimate, Q = rho(B^-1 A) U, node-summed over ranks)."""
         Q = empty_colmajor(self.n, self.m0, self.device) if Q is None else Q
-        pa, lda = _ptr_ld(A, self.n, "A")
-        pb, ldb = _ptr_ld(B, self.n, "B")
-        pu, ldu = _ptr_ld(U, self.n, "U")
-        pq, ldq = _ptr_ld(Q, self.n, "Q")
+        pa, lda = _ptr_ld(A, self.n, "A", self.device)
+        pb, ldb = _ptr_ld(B, self.n, "B", self.device)
+        pu, ldu = _ptr_ld(U, self.n, "U", self.device)
+        pq, ldq = _ptr_ld(Q, self.n, "Q", self.device)
         est = ctypes.c_double()
         self.status = self._check(self.lib.feast_estimate_count(self.h, pa, lda, pb, ldb, pu, ldu, pq, ldq,
                                                                 ctypes.byref(est)))

@@ -99,8 +99,8 @@ def test_virtual_ranks_partition(world):
     Qo = oracle.project(P.A, P.B, P.X0, z, w)
     tot = 0
     for r in range(world):
-        f = _handle(P, rank=r, world=world)
-        part = host(f.project(dev(P.A), dev(P.B), dev(P.X0), allreduce=False))
+        f = _handle(P, rank=r, world=world, partial=True)
+        part = host(f.project(dev(P.A), dev(P.B), dev(P.X0)))
         j0, j1 = synth.node_owner_range(P.q, r, world)
         assert rel(part, oracle.project(P.A, P.B, P.X0, z, w, j0, j1)) <= TOL
         tot = tot + part
@@ -325,7 +325,7 @@ def test_row_sharded_reduce_partials():
     Ah, Bh = host(Ah), host(Bh)
     got = {"A": 0, "B": 0}
     for r in range(world):
-        f = _handle(P, rank=r, world=world)
+        f = _handle(P, rank=r, world=world, partial=True)
         seen = []
 
         def cb(buf, count, stream, user, seen=seen):
@@ -351,7 +351,7 @@ def test_row_sharded_rhs_partials():
     A, B, X = dev(P.A), dev(P.B), dev(P.X0)
     total = 0
     for r in range(world):
-        f = _handle(P, rank=r, world=world)
+        f = _handle(P, rank=r, world=world, partial=True)
         seen = []
 
         def cb(buf, count, stream, user, seen=seen):
@@ -362,7 +362,7 @@ def test_row_sharded_rhs_partials():
 
         f._ar = fb.ALLREDUCE_FN(cb)
         assert f.lib.feast_set_allreduce(f.h, f._ar, None) == 0
-        f.project(A, B, X, allreduce=False)
+        f.project(A, B, X)
         ld = seen[0].size // P.m0
         part = seen[0].reshape(P.m0, ld).T[:P.n]
         r0, r1 = r * P.n // world, (r + 1) * P.n // world
@@ -420,8 +420,8 @@ def test_worst_pivot_node_solution():
     f.project(dev(P.A), dev(P.B), dev(P.X0))
     stats, worst = f.node_stats()
     assert worst == int(np.argmin(stats))
-    g = _handle(P, rank=worst, world=P.q)                       # owns exactly node `worst`
-    part = host(g.project(dev(P.A), dev(P.B), dev(P.X0), allreduce=False))
+    g = _handle(P, rank=worst, world=P.q, partial=True)                      # owns exactly node `worst`
+    part = host(g.project(dev(P.A), dev(P.B), dev(P.X0)))
     Yj = part / w[worst]
     Yo = oracle.project(P.A, P.B, P.X0, z, np.ones_like(w), worst, worst + 1)
     assert rel(Yj, Yo) <= TOL

@@ -18,15 +18,15 @@ d = lambda a: None if a is None else torch.from_numpy(np.asfortranarray(a)).to("
 A, B, X = d(P.A), d(P.B), d(P.X0)
 base = None
 for world in (1, 2, 4, 8):
-    f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, P.B is None, rank=0, world=world)
-    Q = f.project(A, B, X, allreduce=False)
+    f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, P.B is None, rank=0, world=world, partial=True)
+    Q = f.project(A, B, X)
     for _ in range(2):
-        f.project(A, B, X, Q, allreduce=False)
+        f.project(A, B, X, Q)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(5):
-        f.project(A, B, X, Q, allreduce=False)
+        f.project(A, B, X, Q)
         f.reduce(A, B, Q)
     e1.record()
     torch.cuda.synchronize()

@@ -22,20 +22,20 @@ args = ap.parse_args()
 P = synth.make_pencil(args.key, n=args.n)
 s = P.spec
 f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, P.B is None, max_batch=args.batch,
-          world=args.world)
+          world=args.world, partial=args.world > 1)
 d = lambda a: None if a is None else torch.from_numpy(np.asfortranarray(a)).to("cuda")
 A, B, X = d(P.A), d(P.B), d(P.X0)
-Q = f.project(A, B, X, allreduce=False)
-f.project(A, B, X, Q, allreduce=False)
+Q = f.project(A, B, X)
+f.project(A, B, X, Q)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(f.stream)
-f.project(A, B, X, Q, allreduce=False)
+f.project(A, B, X, Q)
 e1.record(f.stream)
 torch.cuda.synchronize()
 print(f"{args.key}: project without events {e0.elapsed_time(e1):.3f} ms")
 f.profile(True)
-f.project(A, B, X, Q, allreduce=False)
+f.project(A, B, X, Q)
 recs = f.profile_records()
 f.profile(False)
 wall = max(r[3] for r in recs)

@@ -21,7 +21,7 @@ A, B, X = d(P.A), d(P.B), d(P.X0)
 Q = torch.empty_like(X)
 for it in range(3):
     f.profile(True, serial=True)
-    f.project(A, B, X, Q, allreduce=False)
+    f.project(A, B, X, Q)
     torch.cuda.synchronize()
 recs = f.profile_records()
 f.profile(False)

@@ -34,7 +34,7 @@ def run_step(mode):
     Bh = torch.empty_like(Ah)
 
     def step():
-        f.project(A, B, X, Q, allreduce=False)
+        f.project(A, B, X, Q)
         f.reduce(A, B, Q, None, Ah, Bh)
 
     f.profile(True, serial=True)
