@@ -48,6 +48,7 @@ def lib():
         _lib.orc_gemm.restype = None
         _lib.orc_project.argtypes = [I64, I64, P, I64, P, I64, P, I64, I32, P, P, I32, I32, I32, P, I64, P]
         _lib.orc_eig.argtypes = [I32, P, P, P, P]
+        _lib.orc_threads.argtypes = [I32]
         _lib.orc_feast_iterate.argtypes = [I64, I64, P, I64, P, I64, I32, P, P, D, D, D, D,
                                            P, I64, P, I64, P, P, P, P, I32]
     return _lib
@@ -180,3 +181,8 @@ def feast_iterate(A, B, X, V, z, w, c, R, a, ortho=True):
     if e:
         raise RuntimeError(f"orc_feast_iterate failed ({e})")
     return dict(X=X, V=V, lam=lam, resid=res, resid_paper=resp, flags=flags)
+
+
+def threads(n: int = 0) -> int:
+    """Set (n > 0) and return the oracle's OpenMP team size (host timing legs only)."""
+    return int(lib().orc_threads(int(n)))

@@ -23,6 +23,7 @@
  * brute force vs scipy at n <= 64, Rayleigh-Ritz exactness on the full space.
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -672,4 +673,12 @@ int orc_feast_iterate(int64_t n, int64_t m0, const double* A, int64_t lda, const
   }
   free(Q); free(QL); free(AQ); free(BQ); free(Ah); free(Bh); free(W);
   return 0;
+}
+
+/* Host-thread control for the timing legs (bench.py cpu_baseline / --impl reference): the OpenMP
+ * team size used across nodes (a launcher may have set OMP_NUM_THREADS=1 before this library
+ * was loaded).  n > 0 sets it; returns the current maximum.  No arithmetic. */
+int orc_threads(int n) {
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
 }

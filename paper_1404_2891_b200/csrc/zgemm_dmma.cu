@@ -279,9 +279,18 @@ static double zgemm_bytes(const ZgemmArgs& p, int mode) {
                  b * p.M * p.N * (readC ? 2.0 : 1.0));
 }
 
+// Algorithmic flops of one launch: 8 M N K per complex GEMM; an in-place launch applies a 64x64
+// TRIANGULAR inverse (L_kk^-1 or U_kk^-1) to a block, K(K+1)/2 complex multiply-adds per column,
+// i.e. 4 K (K + 1) N flops (the kernel executes the dense 8 K^2 N: the zero half is not work).
+static double zgemm_flops(const ZgemmArgs& p) {
+  const double b = p.batch;
+  if (p.inplace) return 4.0 * (double)p.K * (double)(p.K + 1) * (double)p.N * b;
+  return 8.0 * (double)p.M * (double)p.N * (double)p.K * b;
+}
+
 void zgemm_launch_variant(const ZgemmArgs& p, bool conjA, int mode, int variant, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0 || p.batch <= 0) return;
-  ProfScope ps_(K_ZGEMM, 8.0 * (double)p.M * (double)p.N * (double)p.K * p.batch, zgemm_bytes(p, mode), s);
+  ProfScope ps_(K_ZGEMM, zgemm_flops(p), zgemm_bytes(p, mode), s);
   if (conjA) {
     if (mode == ZG_SUB) launch_variant<true, ZG_SUB>(p, variant, s); else launch_variant<true, ZG_GEN>(p, variant, s);
   } else {
@@ -300,7 +309,7 @@ void zgemm_launch(const ZgemmArgs& p, bool conjA, int mode, cudaStream_t s) {
     zgemm_launch_variant(p, conjA, mode, env_variant, s);
     return;
   }
-  ProfScope ps_(K_ZGEMM, 8.0 * (double)p.M * (double)p.N * (double)p.K * p.batch, zgemm_bytes(p, mode), s);
+  ProfScope ps_(K_ZGEMM, zgemm_flops(p), zgemm_bytes(p, mode), s);
   if (conjA) {
     if (mode == ZG_SUB) launch_t<true, ZG_SUB>(p, s); else launch_t<true, ZG_GEN>(p, s);
   } else {
