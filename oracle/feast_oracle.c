@@ -14,7 +14,8 @@
  * Arithmetic: IEEE binary64, complex numbers written out in (re, im) pairs, compiled
  * with -O2 -fno-fast-math -ffp-contract=off (no FMA contraction).  Matrices are
  * column-major, complex interleaved (re, im), leading dimension given explicitly.
- * OpenMP is used only across independent quadrature nodes; the node sum is formed in
+ * OpenMP is used across independent quadrature nodes (a lone node: across the independent
+ * columns of its rank-1 updates and its right-hand sides); the node sum is formed in
  * increasing node order afterwards, so results do not depend on the thread count.
  *
  * Pinning (tests/test_oracle_*.py, -m "not gpu"): quadrature closed forms, the
@@ -240,6 +241,9 @@ int orc_lu(int64_t n, double* Md, int64_t ld, int32_t* ipiv, double* stats) {
     if (a > umax) umax = a;
     if (piv.re == 0.0 && piv.im == 0.0) { if (!info) info = (int)k + 1; continue; }
     for (int64_t i = k + 1; i < n; ++i) AT(M, ld, i, k) = cdiv(AT(M, ld, i, k), piv);
+    /* the columns j of the rank-1 update are independent: threads split them (each element's
+     * update sequence, and so every result bit, is the same for any thread count) */
+#pragma omp parallel for schedule(static) if (n - k > 512)
     for (int64_t j = k + 1; j < n; ++j) {
       cx ukj = AT(M, ld, k, j);
       if (ukj.re == 0.0 && ukj.im == 0.0) continue;
@@ -258,6 +262,8 @@ void orc_lu_solve(int64_t n, const double* LUd, int64_t ld, const int32_t* ipiv,
                   double* Bd, int64_t ldb, int trans) {
   const cx* LU = (const cx*)LUd;
   cx* Bm = (cx*)Bd;
+  /* right-hand sides are independent (threads split them; results independent of the count) */
+#pragma omp parallel for schedule(dynamic, 1) if (nrhs > 1 && n > 256)
   for (int64_t r = 0; r < nrhs; ++r) {
     cx* b = Bm + (size_t)r * (size_t)ldb;
     if (trans == 0) {
@@ -294,6 +300,7 @@ void orc_lu_solve(int64_t n, const double* LUd, int64_t ld, const int32_t* ipiv,
 void orc_gemm(int64_t m, int64_t p, int64_t k, int opa, const double* Ad, int64_t lda,
               const double* Bd, int64_t ldb, double* Cd, int64_t ldc) {
   const cx* A = (const cx*)Ad; const cx* Bm = (const cx*)Bd; cx* C = (cx*)Cd;
+#pragma omp parallel for schedule(dynamic, 1) if (m * k > 65536)
   for (int64_t j = 0; j < p; ++j)
     for (int64_t i = 0; i < m; ++i) {
       cx s = cmk(0, 0);
@@ -320,6 +327,7 @@ int orc_project(int64_t n, int64_t m0, const double* A, int64_t lda, const doubl
   size_t nn = (size_t)n * (size_t)n, nm = (size_t)n * (size_t)m0;
   cx* R = (cx*)malloc(nm * sizeof(cx));        /* R = B X  or  B^H X */
   const cx* Ac = (const cx*)A; const cx* Bc = (const cx*)B; const cx* Xc = (const cx*)X;
+#pragma omp parallel for schedule(dynamic, 1) if (n > 256)
   for (int64_t c = 0; c < m0; ++c)
     for (int64_t i = 0; i < n; ++i) {
       if (!B) { R[i + c * n] = AT(Xc, ldx, i, c); continue; }
@@ -333,7 +341,9 @@ int orc_project(int64_t n, int64_t m0, const double* A, int64_t lda, const doubl
   int nodes = j1 - j0;
   cx* Y = (cx*)malloc((size_t)nodes * nm * sizeof(cx));
   int err = 0;
-#pragma omp parallel for schedule(dynamic, 1)
+  /* nodes in parallel; a single node gets every thread inside its LU and solves instead (the
+   * inner regions are inactive while this one is) */
+#pragma omp parallel for schedule(dynamic, 1) if (nodes > 1)
   for (int jj = 0; jj < nodes; ++jj) {
     int j = j0 + jj;
     cx zj = cmk(z[2 * j], z[2 * j + 1]);

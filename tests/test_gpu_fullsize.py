@@ -94,3 +94,38 @@ def test_c4_full_bifeast_converged_pairs_match_truth():
         i = int(np.argmin(d))
         assert d[i] <= 1e-10 * s.r, (l, rem[i])
         rem.pop(i)
+
+
+@pytest.mark.slow
+def test_c3_full_node_solutions_vs_oracle():
+    """Parity protocol P2 at full C3 size (n = 8192, m0 = 256, GL 16 per half on the a = 0.15
+    ellipse, B = I + 0.01 S): the per-node solves Y_j = (z_j B - A)^-1 B X of node 0 and of the
+    node with the smallest pivot ratio (feast_node_stats), each isolated as a one-node virtual rank
+    (its partial is w_j Y_j) in the launch configuration of the full projector, match the oracle's
+    naive-LU solve of that node element-wise (relative Frobenius 1e-10).  This binds the C3
+    quadrature (poles) and the LU + substitution at full size; the weights are pinned by the
+    oracle's ellipse pins and the full-C3 complex-symmetric test above.  (The oracle's lone-node
+    LU and solves run on all host threads: ~2-5 min.)"""
+    import numpy as np
+
+    import oracle
+    P = synth.make_pencil_torch("C3")
+    s = P.spec
+    f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, False)
+    f.project(P.A, P.B, P.X0)
+    stats, worst = f.node_stats()
+    assert worst == int(np.argmin(stats)) and min(stats) > 0
+    del f
+    z, w = oracle.nodes(s.c, s.r, s.aspect, s.n_e, s.rule)
+    assert len(z) == P.q == 32
+    Ah, Bh, Xh = (np.asfortranarray(t.cpu().numpy()) for t in (P.A, P.B, P.X0))
+    oracle.threads(len(__import__("os").sched_getaffinity(0)))
+    for j in sorted({0, worst}):
+        g = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, False, rank=j, world=P.q, partial=True)
+        zz, ww, j0, j1 = g.nodes()
+        assert (j0, j1) == (j, j + 1) and abs(zz[j] - z[j]) < 1e-15 and abs(ww[j] - w[j]) < 1e-15
+        Yj = g.project(P.A, P.B, P.X0).cpu().numpy() / w[j]
+        del g
+        Yo = oracle.project(Ah, Bh, Xh, z, np.ones_like(w), j, j + 1)
+        err = float(np.linalg.norm(Yj - Yo) / np.linalg.norm(Yo))
+        assert err <= TOL, (j, err)

@@ -114,3 +114,22 @@ def test_eig_permutation_similarity():
     l1, _ = oracle.eig(Ah, Bh)
     l2, _ = oracle.eig(P @ Ah @ P.T, P @ Bh @ P.T)
     assert _match(l1, l2) < 1e-10
+
+
+def test_thread_count_does_not_change_results():
+    """The oracle's OpenMP splits only independent work (nodes; a lone node's update columns and
+    right-hand sides), so every result bit is the same for 1 thread and for all of them."""
+    import os
+    rng = np.random.default_rng(11)
+    n = 640
+    M = np.asfortranarray(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    R = np.asfortranarray(rng.standard_normal((n, 6)) + 1j * rng.standard_normal((n, 6)))
+    z, w = oracle.nodes(0.1, 0.5, 1.0, 4, 0)
+    out = []
+    for t in (1, max(2, len(os.sched_getaffinity(0)))):
+        oracle.threads(t)
+        LU, piv, _, _ = oracle.lu(M)
+        out.append((LU, oracle.lu_solve(LU, piv, R), oracle.gemm(M, R), oracle.project(M, M.T.copy(order="F"), R, z, w),
+                    oracle.project(M, None, R, z, w, 1, 2, left=True)))
+    for a, b in zip(*out):
+        assert np.array_equal(a, b)
