@@ -186,3 +186,75 @@ def feast_iterate(A, B, X, V, z, w, c, R, a, ortho=True):
 def threads(n: int = 0) -> int:
     """Set (n > 0) and return the oracle's OpenMP team size (host timing legs only)."""
     return int(lib().orc_threads(int(n)))
+
+
+# ---------------------------------------------------------------- NEXT-3 (SURVEY §8(f)): count
+# estimate, candidate monitors and the filter-gap report — compositions of the primitives above
+# (projectors, gemm, eig, rho), written out step by step.
+
+def bhat_eigs(A, B, U, V, z, w):
+    """Eigenvalues of V^H B U with U^ = rho(B^-1 A) U and V^ = the left projector of V (Bi-FEAST
+    steps 4-5; the count estimate of P:1046-1050), sorted by decreasing modulus.
+    Since V^ = B^-H rho(B^-1 A)^H B^H V (reading R4), V^^H B U^ = V^H B rho(B^-1 A)^2 U: with
+    V^H B U = I its eigenvalues approximate gamma_i^2 = rho(lambda_i)^2 (exactly when U spans
+    eigenvectors, or when U is square)."""
+    Uh = project(A, B, U, z, w)
+    Vh = project(A, B, V, z, w, left=True)
+    BU = Uh if B is None else gemm(B, Uh)
+    M = gemm(Vh, BU, opa=2)
+    m = M.shape[0]
+    mu, _ = eig(M, np.eye(m, dtype=np.complex128))
+    return mu[np.argsort(-np.abs(mu), kind="stable")]
+
+
+def count_estimate_bi(A, B, U, V, z, w, threshold=0.25):
+    """Eigenvalue-count estimate: the number of eigenvalues mu of V^^H B U^ with
+    |mu| >= threshold; 1/4 = (1/2)^2 counts the gamma_i with |rho(lambda_i)| >= 1/2, the filter's
+    half height (reading R21).  Returns (count, mu sorted by decreasing modulus)."""
+    mu = bhat_eigs(A, B, U, V, z, w)
+    count = 0
+    for x in mu:
+        if abs(x) >= threshold:
+            count += 1
+    return count, mu
+
+
+def monitors(out):
+    """Res_(k) = max ||A u_j - l_j B u_j|| / ||u_j|| and trace_(k) = sum l_j over the candidates
+    (inside the contour and that residual <= 1e-4) of one feast_iterate output.
+    Res_(k) is -1 when there is no candidate."""
+    res, tr, nc = -1.0, 0j, 0
+    for j in range(len(out["lam"])):
+        if out["flags"][j] & 2:
+            nc += 1
+            tr += out["lam"][j]
+            if out["resid_paper"][j] > res:
+                res = out["resid_paper"][j]
+    return res, tr, nc
+
+
+def filter_gap(z, w, lam, p, inside):
+    """FilterGapReport (§4): gamma_j = rho(lambda_j) numbered so that |gamma_1| >= ... >=
+    |gamma_n| (stable in the input order on ties); m = #{lambda_j inside C}; m' = the smallest
+    l >= (last sorted position of an inside eigenvalue) with a strict gap |gamma_{l+1}| < |gamma_l|
+    (or l = n), a relative difference <= 1e-12 counting as a tie (reading R22); eps = |gamma_{p+1} / gamma_{m'}| and log10 |rho(lambda_{p+1}) / rho(lambda_m)|
+    (P:613-618; SPEC S:329-332).  Returns dict(abs_sorted, order, m, m_prime, eps, log10_gap);
+    eps / log10_gap are nan when p >= n or m (m') = 0."""
+    lam = np.asarray(lam, dtype=np.complex128)
+    n = len(lam)
+    g = rho(z, w, lam)
+    a = [abs(x) for x in g]
+    order = sorted(range(n), key=lambda j: (-a[j], j))
+    asorted = [a[j] for j in order]
+    m = int(sum(1 for j in range(n) if inside[j]))
+    last = 0
+    for pos, j in enumerate(order, start=1):
+        if inside[j]:
+            last = pos
+    mp = last
+    while mp < n and mp > 0 and not (asorted[mp] < (1.0 - 1e-12) * asorted[mp - 1]):   # a tie is no gap (R22)
+        mp += 1
+    eps = asorted[p] / asorted[mp - 1] if (p < n and mp >= 1) else float("nan")
+    lg = float(np.log10(asorted[p] / asorted[m - 1])) if (p < n and m >= 1) else float("nan")
+    return dict(abs_sorted=np.array(asorted), order=np.array(order, dtype=np.int64), m=m, m_prime=mp, eps=eps,
+                log10_gap=lg)
