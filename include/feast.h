@@ -220,6 +220,49 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
                   void* X, int64_t ldx, void* V, int64_t ldv,
                   double* ritz, double* resid, int32_t* flags);
 
+/* ---- NEXT-3: count estimate, candidate monitors, filter-gap report ---------- */
+
+/* Eigenvalue-count estimate of Bi-FEAST ("the eigenvalues of V^^H B U^ (U^, V^ from
+ * Steps 4 and 5 of Bi-FEAST)"): U^ = rho(B^-1 A) U into Q and V^ = the left projector of V into
+ * QL (as feast_project_bi, node-summed over the ranks), then the eigenvalues mu of the m0 x m0
+ * matrix V^^H B U^ (cuSOLVER Xgeev; outside the hot path), sorted by decreasing modulus into mu
+ * (host, 2*m0 doubles, complex interleaved; may be NULL), and *count = #{|mu| >= 1/4}.
+ * Reading R21: with V^H B U = I (e.g. V = U (U^H B U)^-H, reading R6, or any Bi-FEAST iterate),
+ * V^^H B U^ = V^H B rho(B^-1 A)^2 U, whose eigenvalues are rho(lambda_i)^2 when U spans
+ * eigenvectors (or is square) and approach the dominant rho(lambda_i)^2 as the iteration
+ * converges; 1/4 = (1/2)^2 counts |rho(lambda)| >= 1/2, the filter's half height (on a circle
+ * exactly the eigenvalues inside).  From random U, V at the first iteration the estimate is rough.
+ * FEAST_BI handles only (FEAST_E_STATE otherwise).  Returns as feast_project_bi, plus
+ * FEAST_E_REDUCED if the eigensolver fails. */
+int feast_estimate_count_bi(feast_handle h, const void* A, int64_t lda, const void* B, int64_t ldb,
+                            const void* U, int64_t ldu, const void* V, int64_t ldv,
+                            void* Q, int64_t ldq, void* QL, int64_t ldql, double* mu, int32_t* count);
+
+/* enable = 1: every Bi-FEAST feast_iterate also forms V^^H B U^ of its steps 4-5 (from the R factors
+ * of the orthonormalisation: R_l^H (V_o^H B U_o) R_q, m0^3 work) and its eigenvalues (Xgeev, no
+ * vectors): the count estimate above, tracked along the iteration (feast_monitors). */
+int feast_set_count_estimate(feast_handle h, int32_t enable);
+
+/* Monitors of the last feast_iterate (host outputs, any may be NULL), P:695-712:
+ *   *res_k   = Res_(k) = max ||A u_j - l_j B u_j|| / ||u_j|| over the candidates (-1: none)
+ *   trace_k  = trace_(k) = sum of the candidate Ritz values l_j (2 doubles: re, im)
+ *   *ncand   = number of candidates (inside the contour and that residual <= 1e-4)
+ *   mu, *count: eig(V^^H B U^) sorted by decreasing modulus and the count estimate of that
+ *              iteration (feast_set_count_estimate on, Bi-FEAST; else *count = -1, mu zeros). */
+int feast_monitors(feast_handle h, double* res_k, double* trace_k, int32_t* ncand, double* mu, int32_t* count);
+
+/* Filter-gap report (§4; SPEC FilterGapReport): for nl eigenvalues lam (host, 2*nl
+ * doubles, e.g. a full spectrum of a small or synthetic problem), gamma_j = rho(lambda_j) of this
+ * handle's quadrature, numbered |gamma_1| >= ... >= |gamma_nl| (stable on ties):
+ *   abs_sorted (nl) = |gamma_j| in that order, order (nl) = the input index of each,
+ *   *m_inside = #{lambda inside the contour}, *m_prime = the smallest l >= (last position of an
+ *   inside eigenvalue) with a strict gap |gamma_{l+1}| < |gamma_l| (a relative difference <= 1e-12
+ *   is a tie, reading R22), *eps = |gamma_{p+1} / gamma_{m'}|, *log10_gap =
+ *   log10 |rho(lambda_{p+1}) / rho(lambda_m)|; NaN when p >= nl or m (m') = 0.
+ * Host computation; any output may be NULL. */
+int feast_filter_gap(feast_handle h, int64_t nl, const double* lam, int64_t p, double* abs_sorted, int32_t* order,
+                     int32_t* m_inside, int32_t* m_prime, double* eps, double* log10_gap);
+
 /* Pivot diagnostics of the last projection (host outputs): min_rel_pivot[q] =
  * min|u_ii| / max|u_ii| per node (owned nodes only; others are set to -1), *worst_node =
  * index of the smallest ratio.  Either pointer may be NULL. */

@@ -104,6 +104,7 @@ struct feast_ctx {
   cusolverDnParams_t solp = nullptr;
   struct It {
     double2 *Qr, *Ql, *AX, *BX, *Ah, *Bh, *M, *W, *Z, *T, *lam, *tau;
+    double2 *Rq, *Rl, *mu;               // R factors of U^, V^ and eig(V^^H B U^) (count estimate)
     double *rn, *xn, *fr;
     int *piv, *info;
     void* sw;
@@ -128,6 +129,12 @@ struct feast_ctx {
   feast_allreduce_fn ar = nullptr;
   void* ar_user = nullptr;
   bool partial = false;               // feast_set_partial: return this rank's partial node sum
+  // NEXT-3: monitors of the last feast_iterate
+  bool count_on = false;              // feast_set_count_estimate: eig(V^^H B U^) in Bi-FEAST iterations
+  double mon_res = -1.0;
+  double2 mon_trace{0.0, 0.0};
+  int mon_ncand = 0, mon_count = -1;
+  std::vector<double2> mon_mu;
   double2* NS = nullptr;              // node-sum staging block [Q | QL] (n x m0 each, ld n), world > 1
   std::string err;
   int64_t launches = 0;
@@ -968,11 +975,18 @@ int ensure_iter_mem(feast_ctx* h) {
   SOL_TRY(h, cusolverDnXgeev_bufferSize(h->sol, h->solp, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, m,
                                         CUDA_C_64F, nullptr, m, CUDA_C_64F, nullptr, CUDA_C_64F, nullptr, m,
                                         CUDA_C_64F, nullptr, m, CUDA_C_64F, &ws_geev_d, &ws_geev_h));
+  size_t ws_nn_d = 0, ws_nn_h = 0;
+  SOL_TRY(h, cusolverDnXgeev_bufferSize(h->sol, h->solp, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_NOVECTOR, m,
+                                        CUDA_C_64F, nullptr, m, CUDA_C_64F, nullptr, CUDA_C_64F, nullptr, m,
+                                        CUDA_C_64F, nullptr, m, CUDA_C_64F, &ws_nn_d, &ws_nn_h));
+  ws_geev_d = std::max(ws_geev_d, ws_nn_d);
+  ws_geev_h = std::max(ws_geev_h, ws_nn_h);
   const size_t nm = (size_t)n * m * 16, mm = (size_t)m * m * 16;
   size_t off = 0;
   auto take = [&](size_t b) { size_t o = off; off += align256(b); return o; };
   size_t o_q = take(nm), o_ql = take(nm), o_ax = take(nm), o_bx = take(nm);
   size_t o_ah = take(mm), o_bh = take(mm), o_m = take(mm), o_w = take(mm), o_z = take(mm), o_t = take(mm);
+  size_t o_rq = take(mm), o_rl = take(mm), o_mu = take(m * 16);
   size_t o_lam = take(m * 16), o_rn = take(m * 8), o_xn = take(m * 8), o_fr = take(256 * 8);
   size_t o_tau = take(m * 16), o_piv = take(m * 4), o_info = take(16);
   size_t o_sw = take(std::max({ws_geqrf, ws_getrf, ws_geev_d, (size_t)256}));
@@ -989,6 +1003,9 @@ int ensure_iter_mem(feast_ctx* h) {
   h->it.W = (double2*)(base + o_w);
   h->it.Z = (double2*)(base + o_z);
   h->it.T = (double2*)(base + o_t);
+  h->it.Rq = (double2*)(base + o_rq);
+  h->it.Rl = (double2*)(base + o_rl);
+  h->it.mu = (double2*)(base + o_mu);
   h->it.lam = (double2*)(base + o_lam);
   h->it.rn = (double*)(base + o_rn);
   h->it.xn = (double*)(base + o_xn);
@@ -999,6 +1016,35 @@ int ensure_iter_mem(feast_ctx* h) {
   h->it.sw = (void*)(base + o_sw);
   h->it.sw_bytes = std::max({ws_geqrf, ws_getrf, ws_geev_d, (size_t)256});
   h->it.hw.resize(std::max<size_t>(ws_geev_h, 16));
+  return FEAST_OK;
+}
+
+// NEXT-3 count estimate: eigenvalues of the m0 x m0 matrix V^^H B U^ (device, ld m,
+// destroyed) by cuSOLVER Xgeev without vectors, sorted by decreasing modulus (stable in index);
+// count = #{|mu| >= 1/4}: |rho(lambda)| >= 1/2, the filter's half height (reading R21), since
+// V^^H B U^ = V^H B rho(B^-1 A)^2 U with V^H B U = I.
+int bhat_count(feast_ctx* h, double2* M) {
+  const int64_t m = h->m0;
+  auto& it = h->it;
+  SOL_TRY(h, cusolverDnXgeev(h->sol, h->solp, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_NOVECTOR, m, CUDA_C_64F, M,
+                             m, CUDA_C_64F, it.mu, CUDA_C_64F, nullptr, m, CUDA_C_64F, nullptr, m, CUDA_C_64F, it.sw,
+                             it.sw_bytes, it.hw.data(), it.hw.size(), it.info));
+  std::vector<double2> mu(m);
+  int hinfo = 0;
+  CUDA_TRY(h, cudaMemcpyAsync(mu.data(), it.mu, m * 16, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(&hinfo, it.info, 4, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  if (hinfo != 0) return fail(h, FEAST_E_REDUCED, "eig(V^H B U) failed%s");
+  std::vector<int> ord(m);
+  for (int64_t i = 0; i < m; ++i) ord[i] = (int)i;
+  std::stable_sort(ord.begin(), ord.end(),
+                   [&](int a, int b) { return std::hypot(mu[a].x, mu[a].y) > std::hypot(mu[b].x, mu[b].y); });
+  h->mon_mu.resize(m);
+  h->mon_count = 0;
+  for (int64_t i = 0; i < m; ++i) {
+    h->mon_mu[i] = mu[ord[i]];
+    if (std::hypot(mu[ord[i]].x, mu[ord[i]].y) >= 0.25) ++h->mon_count;
+  }
   return FEAST_OK;
 }
 
@@ -1394,19 +1440,31 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
     last = now;
   };
   tmark(nullptr);
-  auto orth = [&](double2* Qb) -> int {
+  const bool count = bi && h->count_on;
+  auto orth = [&](double2* Qb, double2* Rk) -> int {
     SOL_TRY(h, cusolverDnZgeqrf(h->sol, (int)n, (int)m, (cuDoubleComplex*)Qb, (int)n, (cuDoubleComplex*)it.tau,
                                 (cuDoubleComplex*)it.sw, (int)(it.sw_bytes / 16), it.info));
+    if (Rk) {   // keep R (U^ = Q_o R) for the count estimate: V^^H B U^ = R_l^H (V_o^H B U_o) R_q
+      CUDA_TRY(h, cudaMemcpy2DAsync(Rk, m * 16, Qb, n * 16, m * 16, m, cudaMemcpyDeviceToDevice, h->stream));
+      feast::tril_zero_launch(Rk, m, m, h->stream);
+    }
     SOL_TRY(h, cusolverDnZungqr(h->sol, (int)n, (int)m, (int)m, (cuDoubleComplex*)Qb, (int)n, (cuDoubleComplex*)it.tau,
                                 (cuDoubleComplex*)it.sw, (int)(it.sw_bytes / 16), it.info));
     return 0;
   };
   tmark("project");
-  if ((e = orth(it.Qr))) return e;
-  if (bi && (e = orth(it.Ql))) return e;
+  if ((e = orth(it.Qr, count ? it.Rq : nullptr))) return e;
+  if (bi && (e = orth(it.Ql, count ? it.Rl : nullptr))) return e;
   // step 4 / 6: reduced matrices, rows of A Q (B Q) sharded over the ranks
   e = reduce_impl(h, A, lda, B, ldb, it.Qr, n, bi ? it.Ql : nullptr, n, it.Ah, m, it.Bh, m, true);
   if (e) return e;
+  h->mon_count = -1;
+  h->mon_mu.clear();
+  if (count) {   // NEXT-3: eig(V^^H B U^) of this iteration's steps 4-5
+    gemm_gen(h, m, m, m, false, it.Bh, m, it.Rq, m, it.W, m, one, zero);
+    gemm_gen(h, m, m, m, true, it.Rl, m, it.W, m, it.Z, m, one, zero);
+    if ((e = bhat_count(h, it.Z))) return e;
+  }
   tmark("qr+reduce");
   // step 5 / 7 (outside the hot path): M = Bh^-1 Ah, eig(M) -> lam, W
   CUDA_TRY(h, cudaMemcpyAsync(it.T, it.Bh, m * m * 16, cudaMemcpyDeviceToDevice, h->stream));
@@ -1469,14 +1527,108 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
   for (double v : fr) an += v;
   an = std::sqrt(an);
   tmark("ritz+resid");
+  h->mon_res = -1.0;
+  h->mon_trace = make_double2(0.0, 0.0);
+  h->mon_ncand = 0;
   for (int64_t c = 0; c < m; ++c) {
     if (ritz) { ritz[2 * c] = lam[c].x; ritz[2 * c + 1] = lam[c].y; }
     const double rp = std::sqrt(rn[c]);  // ||x|| = 1
     if (resid) resid[c] = an > 0 ? rp / an : rp;
     const bool inside = inside_contour(h, lam[c].x, lam[c].y);
     if (flags) flags[c] = (inside ? 1 : 0) | ((inside && rp <= 1e-4) ? 2 : 0);
+    if (inside && rp <= 1e-4) {   // candidate: Res_(k) and trace_(k)
+      ++h->mon_ncand;
+      h->mon_res = std::max(h->mon_res, rp);
+      h->mon_trace.x += lam[c].x;
+      h->mon_trace.y += lam[c].y;
+    }
   }
   return pst;
+}
+
+int feast_set_count_estimate(feast_handle h, int32_t enable) {
+  if (!h) return FEAST_E_ARG;
+  h->count_on = enable != 0;
+  return FEAST_OK;
+}
+
+int feast_monitors(feast_handle h, double* res_k, double* trace_k, int32_t* ncand, double* mu, int32_t* count) {
+  if (!h) return FEAST_E_ARG;
+  if (res_k) *res_k = h->mon_res;
+  if (trace_k) { trace_k[0] = h->mon_trace.x; trace_k[1] = h->mon_trace.y; }
+  if (ncand) *ncand = h->mon_ncand;
+  if (count) *count = h->mon_count;
+  if (mu)
+    for (int64_t i = 0; i < h->m0; ++i) {
+      const bool have = i < (int64_t)h->mon_mu.size();
+      mu[2 * i] = have ? h->mon_mu[i].x : 0.0;
+      mu[2 * i + 1] = have ? h->mon_mu[i].y : 0.0;
+    }
+  return FEAST_OK;
+}
+
+int feast_estimate_count_bi(feast_handle h, const void* A, int64_t lda, const void* B, int64_t ldb, const void* U,
+                            int64_t ldu, const void* V, int64_t ldv, void* Q, int64_t ldq, void* QL, int64_t ldql,
+                            double* mu, int32_t* count) {
+  int e = check_args_common(h, A, lda, B, ldb);
+  if (e) return e;
+  if (h->mode != FEAST_BI) return fail(h, FEAST_E_STATE, "the bi count estimate needs a FEAST_BI handle%s");
+  if (!U || !V || !Q || !QL || ldu < h->n || ldv < h->n || ldq < h->n || ldql < h->n)
+    return fail(h, FEAST_E_ARG, "U/V/Q/QL null or ld < n%s");
+  if (h->world > 1 && h->partial) return fail(h, FEAST_E_STATE, "the count estimate needs the full node sum%s");
+  Join j_(h);
+  if ((e = ensure_iter_mem(h))) return e;
+  const int64_t n = h->n, m = h->m0, ld = h->ldc;
+  const double2 one = make_double2(1, 0), zero = make_double2(0, 0);
+  // Bi-FEAST steps 4-5: U^ = rho U, V^ = left projector of V (node sums over the ranks inside)
+  const int pst = project_impl(h, (const double2*)A, lda, (const double2*)B, ldb, (const double2*)U, ldu,
+                               (const double2*)V, ldv, (double2*)Q, ldq, (double2*)QL, ldql);
+  if (pst < 0) return pst;
+  // V^^H B U^ (m0 x m0; B U^ on the rows this rank owns when sharded: partials all-reduced)
+  const bool shard = h->world > 1 && h->ar != nullptr;
+  const int64_t r0 = shard ? h->rank * n / h->world : 0, r1 = shard ? (h->rank + 1) * n / h->world : n, nr = r1 - r0;
+  const double2* BU = (const double2*)Q + r0;
+  int64_t ldbu = ldq;
+  if (!h->b_id) {
+    gemm_gen(h, nr, m, n, false, (const double2*)B + r0, ldb, (const double2*)Q, ldq, h->BQ + r0, ld, one, zero);
+    BU = h->BQ + r0;
+    ldbu = ld;
+  }
+  gemm_gen(h, m, m, nr, true, (const double2*)QL + r0, ldql, BU, ldbu, h->it.Z, m, one, zero);
+  if (shard && h->ar(h->it.Z, 2 * m * m, h->stream, h->ar_user)) return fail(h, FEAST_E_COMM, "all-reduce failed%s");
+  if ((e = bhat_count(h, h->it.Z))) return e;
+  if (count) *count = h->mon_count;
+  if (mu)
+    for (int64_t i = 0; i < m; ++i) { mu[2 * i] = h->mon_mu[i].x; mu[2 * i + 1] = h->mon_mu[i].y; }
+  return pst;
+}
+
+int feast_filter_gap(feast_handle h, int64_t nl, const double* lam, int64_t p, double* abs_sorted, int32_t* order,
+                     int32_t* m_inside, int32_t* m_prime, double* eps, double* log10_gap) {
+  if (!h || nl < 1 || !lam || p < 0) return FEAST_E_ARG;
+  // gamma_j = rho(lambda_j) (eq. quadrature_for_pi), numbered |gamma_1| >= ... >= |gamma_n| (
+  // stable in the input order on ties); m, m' and eps = |gamma_{p+1} / gamma_{m'}|
+  std::vector<double> rr(2 * nl);
+  feast_filter(h, nl, lam, rr.data());
+  std::vector<double> a(nl);
+  for (int64_t j = 0; j < nl; ++j) a[j] = std::hypot(rr[2 * j], rr[2 * j + 1]);
+  std::vector<int32_t> ord(nl);
+  for (int64_t j = 0; j < nl; ++j) ord[j] = (int32_t)j;
+  std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) { return a[x] > a[y]; });
+  int64_t m = 0, last = 0;
+  for (int64_t pos = 0; pos < nl; ++pos)
+    if (inside_contour(h, lam[2 * ord[pos]], lam[2 * ord[pos] + 1])) { ++m; last = pos + 1; }
+  int64_t mp = last;   // smallest l >= last with a strict gap |gamma_{l+1}| < |gamma_l| (a tie: reading R22)
+  while (mp < nl && mp > 0 && !(a[ord[mp]] < (1.0 - 1e-12) * a[ord[mp - 1]])) ++mp;
+  const double nan = std::nan("");
+  if (abs_sorted)
+    for (int64_t j = 0; j < nl; ++j) abs_sorted[j] = a[ord[j]];
+  if (order) std::memcpy(order, ord.data(), nl * 4);
+  if (m_inside) *m_inside = (int32_t)m;
+  if (m_prime) *m_prime = (int32_t)mp;
+  if (eps) *eps = (p < nl && mp >= 1) ? a[ord[p]] / a[ord[mp - 1]] : nan;
+  if (log10_gap) *log10_gap = (p < nl && m >= 1) ? std::log10(a[ord[p]] / a[ord[m - 1]]) : nan;
+  return FEAST_OK;
 }
 
 int feast_node_stats(feast_handle h, double* min_rel_pivot, int32_t* worst_node) {

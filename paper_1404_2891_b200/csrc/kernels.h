@@ -99,6 +99,8 @@ void frob2_launch(const double2* A, int64_t lda, int64_t n, double* partial, int
 // partial[b] = sum_{c = b mod nparts} sum_i conj(U[i][c]) Q[i][c]  (nparts blocks, host sums in order)
 void cdot_launch(const double2* U, int64_t ldu, const double2* Q, int64_t ldq, int64_t n, int64_t m, double2* partial,
                  int nparts, cudaStream_t s);
+// Zero the strictly lower triangle of an m x m matrix.
+void tril_zero_launch(double2* M, int64_t ld, int64_t m, cudaStream_t s);
 // Scale columns of X by 1/xn[c] and rows of W by same: X[:,c] /= xn[c], W[:,c] /= xn[c]
 void colscale_launch(double2* X, int64_t ldx, int64_t n, double2* W, int64_t ldw, int64_t m,
                      const double* xn, cudaStream_t s);

@@ -743,6 +743,18 @@ void cdot_launch(const double2* U, int64_t ldu, const double2* Q, int64_t ldq, i
   count_launch();
 }
 
+// Zero the strictly lower triangle of an m x m matrix (the R factor left by geqrf).
+__global__ void tril_zero_kernel(double2* M, int64_t ld, int64_t m) {
+  const int64_t c = blockIdx.x;
+  for (int64_t i = c + 1 + threadIdx.x; i < m; i += blockDim.x) M[i + c * ld] = make_double2(0.0, 0.0);
+}
+
+void tril_zero_launch(double2* M, int64_t ld, int64_t m, cudaStream_t s) {
+  ProfScope ps_(K_OTHER, 0.0, 0.0, s);
+  tril_zero_kernel<<<(unsigned)m, 128, 0, s>>>(M, ld, m);
+  count_launch();
+}
+
 __global__ void colscale_kernel(double2* X, int64_t ldx, int64_t n, double2* W, int64_t ldw, int64_t m,
                                 const double* xn) {
   const int64_t c = blockIdx.y;

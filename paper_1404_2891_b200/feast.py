@@ -37,6 +37,7 @@ EXPORTS = ["feast_init", "feast_workspace_bytes", "feast_bind_workspace", "feast
            "feast_iterate",
            "feast_node_stats", "feast_factor_cache", "feast_set_real_pencil",
            "feast_set_complex_symmetric", "feast_estimate_count", "feast_set_contour", "feast_filter",
+           "feast_estimate_count_bi", "feast_set_count_estimate", "feast_monitors", "feast_filter_gap",
            "feast_last_launch_count", "feast_profile", "feast_profile_summary",
            "feast_profile_records", "feast_last_error",
            "feast_version", "feast_destroy"]
@@ -81,6 +82,10 @@ def load_library(path: str = LIB_PATH):
     lib.feast_estimate_count.argtypes = [P, P, I64, P, I64, P, I64, P, I64, P]
     lib.feast_set_contour.argtypes = [P, I32, P, P, I32, I32]
     lib.feast_filter.argtypes = [P, I64, P, P]
+    lib.feast_estimate_count_bi.argtypes = [P, P, I64, P, I64, P, I64, P, I64, P, I64, P, I64, P, P]
+    lib.feast_set_count_estimate.argtypes = [P, I32]
+    lib.feast_monitors.argtypes = [P, P, P, P, P, P]
+    lib.feast_filter_gap.argtypes = [P, I64, P, I64, P, P, P, P, P, P]
     lib.feast_profile.argtypes = [P, I32]
     lib.feast_profile_summary.argtypes = [P, I32, P, P, P, P]
     lib.feast_profile_records.argtypes = [P, I64, P, P, P, P, P, P]
@@ -328,6 +333,54 @@ class Feast:
         self.status = self._check(self.lib.feast_estimate_count(self.h, pa, lda, pb, ldb, pu, ldu, pq, ldq,
                                                                 ctypes.byref(est)))
         return est.value, Q
+
+    def estimate_count_bi(self, A, B, U, V, Q=None, QL=None):
+        """Count estimate from eig(V^^H B U^) of Bi-FEAST steps 4-5 (reading R21):
+        returns (count, mu sorted by decreasing modulus, Q = U^, QL = V^)."""
+        import numpy as np
+        Q = empty_colmajor(self.n, self.m0, self.device) if Q is None else Q
+        QL = empty_colmajor(self.n, self.m0, self.device) if QL is None else QL
+        pa, lda = _ptr_ld(A, self.n, "A", self.device)
+        pb, ldb = _ptr_ld(B, self.n, "B", self.device)
+        pu, ldu = _ptr_ld(U, self.n, "U", self.device)
+        pv, ldv = _ptr_ld(V, self.n, "V", self.device)
+        pq, ldq = _ptr_ld(Q, self.n, "Q", self.device)
+        pl, ldl = _ptr_ld(QL, self.n, "QL", self.device)
+        mu = np.zeros(self.m0, dtype=np.complex128)
+        cnt = ctypes.c_int32()
+        self.status = self._check(self.lib.feast_estimate_count_bi(
+            self.h, pa, lda, pb, ldb, pu, ldu, pv, ldv, pq, ldq, pl, ldl, mu.ctypes.data_as(ctypes.c_void_p),
+            ctypes.byref(cnt)))
+        return cnt.value, mu, Q, QL
+
+    def set_count_estimate(self, enable: bool):
+        """Track the eig(V^^H B U^) count estimate in every Bi-FEAST iterate() (see monitors())."""
+        self._check(self.lib.feast_set_count_estimate(self.h, int(bool(enable))))
+
+    def monitors(self):
+        """Res_(k), trace_(k), number of candidates of the last iterate(), and (Bi-FEAST
+        with set_count_estimate) the count estimate and eig(V^^H B U^) sorted by modulus."""
+        import numpy as np
+        res, tr, nc, cnt = ctypes.c_double(), (ctypes.c_double * 2)(), ctypes.c_int32(), ctypes.c_int32()
+        mu = np.zeros(self.m0, dtype=np.complex128)
+        self._check(self.lib.feast_monitors(self.h, ctypes.byref(res), tr, ctypes.byref(nc),
+                                            mu.ctypes.data_as(ctypes.c_void_p), ctypes.byref(cnt)))
+        return {"res_k": res.value, "trace_k": complex(tr[0], tr[1]), "ncand": nc.value, "count": cnt.value,
+                "mu": mu if cnt.value >= 0 else None}
+
+    def filter_gap(self, lam, p):
+        """Filter-gap report of eigenvalues lam (host) for subspace size p."""
+        import numpy as np
+        lam = np.ascontiguousarray(np.atleast_1d(lam), dtype=np.complex128)
+        nl = len(lam)
+        a = np.zeros(nl)
+        order = np.zeros(nl, dtype=np.int32)
+        m, mp, eps, lg = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_double(), ctypes.c_double()
+        self._check(self.lib.feast_filter_gap(self.h, nl, lam.ctypes.data_as(ctypes.c_void_p), int(p),
+                                              a.ctypes.data_as(ctypes.c_void_p), order.ctypes.data_as(ctypes.c_void_p),
+                                              ctypes.byref(m), ctypes.byref(mp), ctypes.byref(eps), ctypes.byref(lg)))
+        return dict(abs_sorted=a, order=order.astype(np.int64), m=m.value, m_prime=mp.value, eps=eps.value,
+                    log10_gap=lg.value)
 
     def node_stats(self):
         zz, _, _, _ = self.nodes()

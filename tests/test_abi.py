@@ -181,3 +181,35 @@ def test_filter_endpoint_trapezoid_closed_forms():
     assert abs(out[0] - 1) < 1e-14 and abs(out[1] + 1 / 15) < 1e-14
     assert abs(np.max(np.abs(out[2:])) - 1 / 15) < 1e-12
     lib.feast_destroy(h)
+
+
+@pytest.mark.parametrize("c,r,a,n_e,rule,p", [(0j, 1.0, 1.0, 8, 0, 4), (0.2 + 0.1j, 0.3, 1.0, 16, 0, 10),
+                                              (0j, 0.4, 0.15, 16, 2, 7), (0.5, 0.25, 1.0, 32, 0, 3)])
+def test_filter_gap_matches_oracle(c, r, a, n_e, rule, p):
+    """feast_filter_gap (host code of the library, NEXT-3) equals the oracle's report:
+    same ordering, m, m' and eps / log10 gap on random spectra around the contour."""
+    lib = fb.load_library()
+    rc, h = _init(c=c, r=r, a=a, n_e=n_e, rule=rule)
+    assert rc == 0
+    z, w, _, _ = _nodes(h)
+    rng = np.random.default_rng(int(100 * r) + n_e)
+    rad = rng.uniform(0, 2.2, 40)
+    th = rng.uniform(0, 2 * np.pi, 40)
+    lam = c + r * rad * (np.cos(th) + 1j * a * np.sin(th))
+    inside = rad < 1
+    ref = oracle.filter_gap(z, w, lam, p, inside)
+    nl = len(lam)
+    lamc = np.ascontiguousarray(lam)
+    ab = np.zeros(nl)
+    order = np.zeros(nl, dtype=np.int32)
+    m, mp, eps, lg = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_double(), ctypes.c_double()
+    assert lib.feast_filter_gap(h, nl, lamc.ctypes.data_as(ctypes.c_void_p), p, ab.ctypes.data_as(ctypes.c_void_p),
+                                order.ctypes.data_as(ctypes.c_void_p), ctypes.byref(m), ctypes.byref(mp),
+                                ctypes.byref(eps), ctypes.byref(lg)) == 0
+    lib.feast_destroy(h)
+    assert list(order) == list(ref["order"])
+    # |rho| far outside is a sum of O(1) terms cancelling to ~1e-12: agreement to rounding of those
+    assert np.allclose(ab, ref["abs_sorted"], rtol=1e-10, atol=1e-14)
+    assert (m.value, mp.value) == (ref["m"], ref["m_prime"])
+    assert abs(eps.value - ref["eps"]) <= 1e-14 + 1e-8 * abs(ref["eps"])
+    assert abs(lg.value - ref["log10_gap"]) <= 1e-8
