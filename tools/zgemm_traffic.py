@@ -1,7 +1,7 @@
 """DRAM traffic of the dominant kernel (zgemm_dmma_kernel) per launch vs its algorithmic bytes.
 
-Two passes over the SAME bench step (C2 project + reduce, serialised profile mode, the launch
-sequence bench.py's roofline pass times):
+Two passes over the SAME bench step (project (+ left) + reduce of --config=Ck, serialised profile
+mode, the launch sequence bench.py's roofline pass times):
 
     python tools/zgemm_traffic.py alg  gpurun_out/zg_alg.json     # algorithmic bytes / flops
     ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
@@ -19,23 +19,37 @@ import sys
 sys.path.insert(0, ".")
 
 
-def run_step(mode):
+def run_step(mode, config):
     import numpy as np
     import torch
     import synth
-    from paper_1404_2891_b200 import Feast, feast as fb
-    P = synth.make_pencil("C2")
-    s = P.spec
-    f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, P.B is None)
-    d = lambda a: None if a is None else torch.from_numpy(np.asfortranarray(a)).to("cuda")
-    A, B, X = d(P.A), d(P.B), d(P.X0)
-    Q = torch.empty_like(X)
-    Ah = torch.empty((P.m0, P.m0), dtype=torch.complex128, device="cuda").t()
-    Bh = torch.empty_like(Ah)
+    from paper_1404_2891_b200 import Feast, empty_colmajor, feast as fb
+    spec = synth.CONFIGS[config]
+    bi = spec.mode == "bi"
+    if spec.n >= 4096:
+        P = synth.make_pencil_torch(config)
+        A, B, X = P.A, P.B, P.X0
+        P.V = P.lam = None
+    else:
+        P = synth.make_pencil(config)
+        d = lambda a: None if a is None else torch.from_numpy(np.asfortranarray(a)).to("cuda")
+        A, B, X = d(P.A), d(P.B), d(P.X0)
+    n, m0, s = P.n, P.m0, spec
+    V = fb.colmajor(torch.linalg.solve(X.conj().T @ X, X.conj().T).conj().T) if bi else None
+    del P
+    torch.cuda.empty_cache()
+    f = Feast(n, m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.BI if bi else fb.RIGHT, B is None)
+    Q = empty_colmajor(n, m0)
+    QL = empty_colmajor(n, m0) if bi else None
+    Ah = empty_colmajor(m0, m0)
+    Bh = empty_colmajor(m0, m0)
 
     def step():
-        f.project(A, B, X, Q)
-        f.reduce(A, B, Q, None, Ah, Bh)
+        if bi:
+            f.project_bi(A, B, X, V, Q, QL)
+        else:
+            f.project(A, B, X, Q)
+        f.reduce(A, B, Q, QL, Ah, Bh)
 
     f.profile(True, serial=True)
     step()                      # warm-up: lazy init, workspace, kernel attributes
@@ -52,7 +66,7 @@ def run_step(mode):
     return zg
 
 
-def merge(alg_path, ncu_path, out_path):
+def merge(alg_path, ncu_path, out_path, config):
     alg = json.load(open(alg_path))
     rows = []
     with open(ncu_path) as fh:
@@ -73,7 +87,7 @@ def merge(alg_path, ncu_path, out_path):
     rd = sum(m.get("dram__bytes_read.sum", 0) for m in per.values())
     ns = sum(m.get("gpu__time_duration.sum", 0) for m in per.values())
     out = {
-        "config": "C2",
+        "config": config,
         "kernel": "zgemm_dmma_kernel",
         "launches": n,
         "launches_alg": alg["launches"],
@@ -84,7 +98,7 @@ def merge(alg_path, ncu_path, out_path):
         "ncu_cold_cache_ms_per_step": ns * 1e-6,
         "ncu_tflops_cold_serialised": alg["flops"] / (ns * 1e-9) / 1e12 if ns else None,
         "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
-                  "--clock-control none -k regex:zgemm_dmma over one serialised C2 bench step "
+                  f"--clock-control none -k regex:zgemm_dmma over one serialised {config} bench step "
                   "(tools/zgemm_traffic.py)",
     }
     json.dump(out, open(out_path, "w"), indent=1)
@@ -93,11 +107,13 @@ def merge(alg_path, ncu_path, out_path):
 
 if __name__ == "__main__":
     mode = sys.argv[1]
+    cfg = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--config=")), "C2")
+    args = [a for a in sys.argv[2:] if not a.startswith("--config=")]
     if mode == "alg":
-        zg = run_step("alg")
-        json.dump(zg, open(sys.argv[2], "w"), indent=1)
+        zg = run_step("alg", cfg)
+        json.dump(zg, open(args[0], "w"), indent=1)
         print(zg)
     elif mode == "ncu":
-        run_step("ncu")
+        run_step("ncu", cfg)
     elif mode == "merge":
-        merge(sys.argv[2], sys.argv[3], sys.argv[4])
+        merge(args[0], args[1], args[2], cfg)
