@@ -10,5 +10,5 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 18000 
 python tools/zgemm_traffic.py alg gpurun_out/zg_alg_C4.json --config=C4 > gpurun_out/zg_alg_C4.log 2>&1
 timeout 1500 ncu --replay-mode application --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:zgemm_dmma --profile-from-start off --csv --log-file gpurun_out/zg_ncu_C4.csv python tools/zgemm_traffic.py ncu --config=C4 > gpurun_out/zg_ncu_C4.log 2>&1
 python tools/zgemm_traffic.py merge gpurun_out/zg_alg_C4.json gpurun_out/zg_ncu_C4.csv gpurun_out/zgemm_traffic_C4.json --config=C4 > gpurun_out/zg_merge_C4.log 2>&1
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:zgemm_dmma --launch-skip 600 --launch-count 2 -o gpurun_out/r2_zgemm_C4_full --profile-from-start off python tools/zgemm_traffic.py ncu --config=C4 > gpurun_out/r2_ncu_full.log 2>&1
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:zgemm_dmma --launch-skip 40 --launch-count 6 -o gpurun_out/r2_zgemm_C4_full --profile-from-start off python tools/zgemm_traffic.py ncu --config=C4 --batch=1 > gpurun_out/r2_ncu_full.log 2>&1
 tail -n 3 gpurun_out/r2_*.log gpurun_out/zg_*C4.log

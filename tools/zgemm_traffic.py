@@ -19,7 +19,7 @@ import sys
 sys.path.insert(0, ".")
 
 
-def run_step(mode, config):
+def run_step(mode, config, batch=0):
     import numpy as np
     import torch
     import synth
@@ -38,7 +38,7 @@ def run_step(mode, config):
     V = fb.colmajor(torch.linalg.solve(X.conj().T @ X, X.conj().T).conj().T) if bi else None
     del P
     torch.cuda.empty_cache()
-    f = Feast(n, m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.BI if bi else fb.RIGHT, B is None)
+    f = Feast(n, m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.BI if bi else fb.RIGHT, B is None, max_batch=batch)
     Q = empty_colmajor(n, m0)
     QL = empty_colmajor(n, m0) if bi else None
     Ah = empty_colmajor(m0, m0)
@@ -108,12 +108,13 @@ def merge(alg_path, ncu_path, out_path, config):
 if __name__ == "__main__":
     mode = sys.argv[1]
     cfg = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--config=")), "C2")
-    args = [a for a in sys.argv[2:] if not a.startswith("--config=")]
+    batch = int(next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--batch=")), "0"))
+    args = [a for a in sys.argv[2:] if not a.startswith("--")]
     if mode == "alg":
         zg = run_step("alg", cfg)
         json.dump(zg, open(args[0], "w"), indent=1)
         print(zg)
     elif mode == "ncu":
-        run_step("ncu", cfg)
+        run_step("ncu", cfg, batch)
     elif mode == "merge":
         merge(args[0], args[1], args[2], cfg)
