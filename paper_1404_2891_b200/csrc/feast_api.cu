@@ -69,7 +69,7 @@ struct feast_ctx {
   cudaEvent_t ev_a = nullptr, ev_p = nullptr;
   // concurrent node groups (group 0 uses stream / side / ev_a / ev_p)
   static constexpr int GMAX = 4;
-  bool laswp_perm = false;            // FEAST_LASWP=perm: permutation-gather row swaps
+  int laswp_variant = feast::LASWP_COALESCED;   // FEAST_LASWP=chain|perm: the round-1 swap kernels
   bool prof_serial = false;           // feast_profile(h, 2): one stream, no lookahead / groups
   int groups = 4;                     // concurrent node groups per batch (FEAST_GROUPS)
   bool group_streams = false;
@@ -456,10 +456,10 @@ void factor_block(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, cudaStream_
       const int wpp = (int)std::min<int64_t>(wp, ki + wi - kp);
       panel_at(h, v, kp, wpp, s);
       if (smem) {
-        if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, K0 + Wo, nbat, s, h->laswp_perm);
+        if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, K0 + Wo, nbat, s, h->laswp_variant);
       } else {   // the register-chunk panel already swapped its own columns
-        if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, kp, nbat, s, h->laswp_perm);
-        if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, kp + wpp, K0 + Wo, nbat, s, h->laswp_perm);
+        if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, kp, nbat, s, h->laswp_variant);
+        if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, kp + wpp, K0 + Wo, nbat, s, h->laswp_variant);
       }
       const int64_t cp = kp + wpp, remb = ki + wi - cp;
       if (remb > 0) {
@@ -566,7 +566,7 @@ struct LuRun {
         factor_block(h, v, 0, Wo, sm);
       }
       if (v.ev_first) cudaEventRecord(v.ev_first, sm);   // releases the next (staggered) group
-      if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, 0, (int)Wo, v.ipiv, Wo, ntot, nbat, sm, h->laswp_perm);
+      if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, 0, (int)Wo, v.ipiv, Wo, ntot, nbat, sm, h->laswp_variant);
       phase = 1;
       K0 = 0;
       return false;
@@ -592,8 +592,8 @@ struct LuRun {
       factor_block(h, v, K1, Wo1, sm);
     }
     // block K1's swaps on every column outside it
-    if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, 0, K1, nbat, sm, h->laswp_perm);
-    if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, K1 + Wo1, ntot, nbat, sm, h->laswp_perm);
+    if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, 0, K1, nbat, sm, h->laswp_variant);
+    if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, K1 + Wo1, ntot, nbat, sm, h->laswp_variant);
     K0 = K1;
     Wo = Wo1;
     return false;
@@ -1139,7 +1139,8 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   }
   if (const char* e = getenv("FEAST_LOOKAHEAD")) h->lookahead = e[0] != '0';
   if (const char* e = getenv("FEAST_GRAPH")) h->graphs = e[0] != '0';
-  if (const char* e = getenv("FEAST_LASWP")) h->laswp_perm = e[0] == 'p';
+  if (const char* e = getenv("FEAST_LASWP"))
+    h->laswp_variant = e[0] == 'p' ? feast::LASWP_PERM : (e[0] == 'c' && e[1] == 'h') ? feast::LASWP_CHAIN : feast::LASWP_COALESCED;
   if (const char* e = getenv("FEAST_STAGGER")) h->stagger = e[0] != '0';
   if (const char* e = getenv("FEAST_WIDE_ROWS")) h->wide_panel_rows = atol(e);
   if (const char* e = getenv("FEAST_GROUPS")) {
@@ -1748,6 +1749,8 @@ int feast_profile(feast_handle h, int32_t enable) {
   h->prof_serial = enable == 2;
   p.recs.clear();
   p.used = 0;
+  if (p.counters && p.counters_used) cudaMemset(p.counters, 0, p.counters_used * sizeof(unsigned long long));
+  p.counters_used = 0;
   return FEAST_OK;
 }
 
@@ -1758,11 +1761,18 @@ int feast_profile_summary(feast_handle h, int32_t kclass, int64_t* launches, dou
   CUDA_TRY(h, cudaDeviceSynchronize());
   int64_t c = 0;
   double t = 0, f = 0, b = 0;
-  for (const auto& r : feast::prof().recs) {
+  const auto& P = feast::prof();
+  std::vector<unsigned long long> cnt;
+  if (P.counters && P.counters_used > 0) {
+    cnt.resize(P.counters_used);
+    CUDA_TRY(h, cudaMemcpy(cnt.data(), P.counters, cnt.size() * 8, cudaMemcpyDeviceToHost));
+  }
+  for (const auto& r : P.recs) {
     if (r.cls != kclass) continue;
     float e = 0.f;
     CUDA_TRY(h, cudaEventElapsedTime(&e, r.a, r.b));
-    ++c; t += e; f += r.flops; b += r.bytes;
+    ++c; t += e; f += r.flops;
+    b += (r.dev_bytes >= 0 && r.dev_bytes < (int64_t)cnt.size()) ? (double)cnt[r.dev_bytes] : r.bytes;
   }
   if (launches) *launches = c;
   if (ms) *ms = t;

@@ -44,8 +44,12 @@ void panel_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double*
 // Apply the cnt (<= 1024) sequential swaps ipiv[k..k+cnt) to the columns [c0, c1).
 // use_perm: one composed permutation per CTA, gather + scatter per column (coalesced writes of
 // the rows k..k+cnt-1) instead of the per-column swap chain.
+// Row swaps ipiv[k..k+cnt) applied to columns [c0, c1) (variant: LASWP_COALESCED = slot-traced
+// gather/scatter with coalesced block rows (default), LASWP_CHAIN = one thread per column running
+// the swap chain, LASWP_PERM = permutation composed per CTA with a row table).
+enum { LASWP_COALESCED = 0, LASWP_CHAIN = 1, LASWP_PERM = 2 };
 void laswp_launch(Batched C, int64_t n, int64_t k, int cnt, const int32_t* ipiv, int64_t c0, int64_t c1, int batch,
-                  cudaStream_t s, bool use_perm = false);
+                  cudaStream_t s, int variant = LASWP_COALESCED);
 // Cluster panel with the panel resident in shared memory (rows never moved; see panel_smem.cu).
 bool panel_smem_fits(int64_t n, int w, int cs);
 int panel_smem_max_clusters(int64_t L, int w, int cs);

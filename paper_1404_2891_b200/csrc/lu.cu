@@ -450,16 +450,119 @@ __global__ void __launch_bounds__(32 * LP_WARPS) laswp_perm_kernel(Batched C, in
   }
 }
 
+// Row swaps, coalesced (BASELINE north_star "a row-swap kernel with coalesced 16-byte
+// access").  The cnt sequential swaps ipiv[k..k+cnt) act on the touched rows only: the block rows
+// k..k+cnt-1 and the pivot rows below.  Slot t names a DESTINATION row d_t (t < cnt: d_t = k + t;
+// t >= cnt: the pivot row ipiv[k + t - cnt] when it lies below the block); its source row is
+// found by tracing d_t back through the swaps in reverse order (each swap is an involution), all
+// slots in parallel (cnt steps per thread, no serial composition, no row table).  Slots whose row
+// does not move are dropped.  Then each warp moves whole columns: lane t gathers the source of
+// slot t into registers, then scatters to d_t, so the writes (and the reads of the pivot-row
+// slots) to the contiguous block rows of a column coalesce into 512-byte warp transactions of
+// 16-byte complex elements; the other half of the accesses are the scattered pivot rows (one
+// 32-byte sector each, unavoidable in column-major storage).  In profile mode every CTA adds the
+// bytes it moved (16 B read + 16 B written per moved element) to a device counter.
+constexpr int LC_WARPS = 8;
+template <int SPL>   // slots per lane: 2 cnt <= 32 SPL
+__global__ void __launch_bounds__(32 * LC_WARPS) laswp_coalesced_kernel(Batched C, int64_t n, int64_t k, int cnt,
+                                                                          const int32_t* __restrict__ ipiv_all,
+                                                                          int64_t c0, int64_t c1, int cols_per_cta,
+                                                                          unsigned long long* moved_bytes) {
+  __shared__ int32_t s_piv[16 * 32 / 2];
+  __shared__ int32_t s_src[16 * 32], s_dst[16 * 32];
+  __shared__ int s_nmov;
+  const int b = blockIdx.y;
+  const int32_t* ipiv = ipiv_all + (int64_t)b * n + k;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) s_piv[i] = ipiv[i] - (int)k;   // relative rows
+  if (threadIdx.x == 0) s_nmov = 0;
+  __syncthreads();
+  const int nslot = 2 * cnt;
+  int mov = 0;
+  for (int t = threadIdx.x; t < 32 * SPL; t += blockDim.x) {
+    int d = -1;
+    if (t < cnt) d = t;
+    else if (t < nslot) { const int p = s_piv[t - cnt]; d = p >= cnt ? p : -1; }
+    int src = d;
+    if (d >= 0)
+      for (int i = cnt - 1; i >= 0; --i) {   // the value that ends in row d came from src
+        const int p = s_piv[i];
+        src = src == i ? p : (src == p ? i : src);
+      }
+    // a pivot row named by several swaps appears in several slots: keep the first
+    if (t >= cnt && d >= 0)
+      for (int u = 0; u < t - cnt; ++u)
+        if (s_piv[u] == d) { d = -1; break; }
+    const bool mv = d >= 0 && src != d;
+    s_dst[t] = mv ? d : -1;
+    s_src[t] = mv ? src : 0;
+    mov += mv;
+  }
+  if (moved_bytes && mov) atomicAdd(&s_nmov, mov);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* base = C.p + (int64_t)b * C.stride + k;
+  const int64_t cbeg = c0 + (int64_t)blockIdx.x * cols_per_cta, cend = min(c1, cbeg + cols_per_cta);
+  // slot tables in registers for short swap sequences, read from shared memory for long ones
+  constexpr bool REG = SPL <= 4;
+  int dst_r[REG ? SPL : 1], src_r[REG ? SPL : 1];
+  if (REG)
+#pragma unroll
+    for (int u = 0; u < SPL; ++u) { dst_r[REG ? u : 0] = s_dst[lane + 32 * u]; src_r[REG ? u : 0] = s_src[lane + 32 * u]; }
+#define DST(u) (REG ? dst_r[REG ? (u) : 0] : s_dst[lane + 32 * (u)])
+#define SRC(u) (REG ? src_r[REG ? (u) : 0] : s_src[lane + 32 * (u)])
+  constexpr bool ILP2 = SPL <= 4;   // two columns in flight per warp when the slot registers allow
+  for (int64_t col = cbeg + warp; col < cend; col += (ILP2 ? 2 : 1) * LC_WARPS) {
+    // gather every moved slot of the column(s) first, then scatter (a bijection on the slots)
+    double2* C0 = base + col * C.ld;
+    const bool two = ILP2 && col + LC_WARPS < cend;
+    double2* C1 = base + (col + LC_WARPS) * C.ld;
+    double2 v0[SPL], v1[ILP2 ? SPL : 1];
+#pragma unroll
+    for (int u = 0; u < SPL; ++u)
+      if (DST(u) >= 0) {
+        v0[u] = C0[SRC(u)];
+        if (two) v1[ILP2 ? u : 0] = C1[SRC(u)];
+      }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < SPL; ++u)
+      if (DST(u) >= 0) {
+        C0[DST(u)] = v0[u];
+        if (two) C1[DST(u)] = v1[ILP2 ? u : 0];
+      }
+  }
+#undef DST
+#undef SRC
+  if (moved_bytes && threadIdx.x == 0 && s_nmov)
+    atomicAdd(moved_bytes, (unsigned long long)s_nmov * (unsigned long long)(cend > cbeg ? cend - cbeg : 0) * 32ull);
+}
+
+template <int SPL>
+void laswp_coalesced_launch(Batched C, int64_t n, int64_t k, int cnt, const int32_t* ipiv, int64_t c0, int64_t c1,
+                            int batch, cudaStream_t s, unsigned long long* moved) {
+  // columns per CTA: enough CTAs to cover the GPU once for the smallest ranges, and at most 64
+  // columns (eight per warp) so the per-CTA slot tracing (cnt steps) is amortised
+  const int64_t ncol = c1 - c0;
+  int cpc = 2 * LC_WARPS;
+  while (cpc < 64 && (ncol + 2 * cpc - 1) / (2 * cpc) * batch >= 2 * 148) cpc *= 2;
+  dim3 grid((unsigned)((ncol + cpc - 1) / cpc), (unsigned)batch);
+  laswp_coalesced_kernel<SPL><<<grid, 32 * LC_WARPS, 0, s>>>(C, n, k, cnt, ipiv, c0, c1, cpc, moved);
+}
+
 void laswp_launch(Batched C, int64_t n, int64_t k, int cnt, const int32_t* ipiv, int64_t c0, int64_t c1, int batch,
-                  cudaStream_t s, bool use_perm) {
+                  cudaStream_t s, int variant) {
   if (c1 <= c0 || cnt <= 0) return;
-  ProfScope ps_(K_LASWP, 0.0, (double)batch * (c1 - c0) * cnt * 64.0, s);
+  // algorithmic bytes: data-dependent (only moved rows count), filled by the kernel's counter
+  ProfScope ps_(K_LASWP, 0.0, 0.0, s);
   const int64_t L = n - k;
   const size_t smem = (size_t)(L + 4 * cnt) * sizeof(int32_t);
-  // Default: the per-column swap chain.  Measured on B200 (C2 project 17.9 vs 18.9 ms, C3 1710 vs
-  // 1730 ms) the permutation kernel loses in the overlapped schedule: its many CTAs and row tables
-  // compete with the trailing-update GEMMs more than the short chain kernel does.
-  if (use_perm && 2 * cnt <= 32 * 16 && smem <= 96 * 1024) {
+  if (variant == LASWP_COALESCED && cnt <= 256) {
+    unsigned long long* moved = ps_.bytes_counter();
+    if (cnt <= 32) laswp_coalesced_launch<2>(C, n, k, cnt, ipiv, c0, c1, batch, s, moved);
+    else if (cnt <= 64) laswp_coalesced_launch<4>(C, n, k, cnt, ipiv, c0, c1, batch, s, moved);
+    else if (cnt <= 128) laswp_coalesced_launch<8>(C, n, k, cnt, ipiv, c0, c1, batch, s, moved);
+    else laswp_coalesced_launch<16>(C, n, k, cnt, ipiv, c0, c1, batch, s, moved);
+  } else if (variant == LASWP_PERM && 2 * cnt <= 32 * 16 && smem <= 96 * 1024) {
     static std::atomic<uint64_t> configured{0};
     if (first_use_on_device(configured)) {
       cudaFuncSetAttribute(laswp_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);

@@ -17,6 +17,7 @@ struct ProfRec {
   double flops, bytes;
   cudaEvent_t a, b;
   cudaStream_t s;
+  int64_t dev_bytes = -1;   // index of a device byte counter the kernel fills (data-dependent traffic)
 };
 
 struct Prof {
@@ -24,6 +25,19 @@ struct Prof {
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> pool;
   size_t used = 0;
+  // device counters for kernels whose traffic depends on the data (row swaps: only the rows that
+  // actually move); allocated on first use while profiling, read back by feast_profile_summary
+  unsigned long long* counters = nullptr;
+  int64_t ncounters = 0, counters_used = 0;
+  unsigned long long* counter() {
+    if (!counters) {
+      ncounters = 1 << 20;
+      if (cudaMalloc(&counters, ncounters * sizeof(unsigned long long)) != cudaSuccess) { counters = nullptr; return nullptr; }
+      cudaMemset(counters, 0, ncounters * sizeof(unsigned long long));
+    }
+    if (counters_used >= ncounters) return nullptr;
+    return counters + counters_used++;
+  }
   cudaEvent_t get() {
     if (used == pool.size()) {
       cudaEvent_t e;
@@ -45,6 +59,13 @@ struct ProfScope {
       r.a = prof().get(); r.b = prof().get();
       cudaEventRecord(r.a, s);
     }
+  }
+  // a device counter of this launch's bytes (the kernel adds to it); nullptr when not profiling
+  unsigned long long* bytes_counter() {
+    if (!on) return nullptr;
+    unsigned long long* c = prof().counter();
+    if (c) r.dev_bytes = c - prof().counters;
+    return c;
   }
   ~ProfScope() {
     if (on) {

@@ -371,15 +371,22 @@ def test_row_sharded_rhs_partials():
     assert rel(total, P.B @ P.X0) <= 1e-13
 
 
-def test_permutation_laswp_variant(monkeypatch):
-    """The permutation-gather row-swap kernel (FEAST_LASWP=perm, coalesced writes of the panel
-    rows) gives the same projector as the default per-column swap chain."""
-    monkeypatch.setenv("FEAST_LASWP", "perm")
-    P = synth.make_pencil("C2", n=300, m0=20)
+@pytest.mark.parametrize("key,n,m0", [("C2", 300, 20), ("C3", 700, 24), ("C3", 1300, 9)])
+def test_row_swap_variants_bit_identical(monkeypatch, key, n, m0):
+    """Row swaps are pure data movement: the default coalesced kernel (slot-traced gather/scatter),
+    the per-column swap chain (FEAST_LASWP=chain) and the per-CTA permutation kernel
+    (FEAST_LASWP=perm) must give BIT-identical projectors, equal to the oracle's.  The C3 recipe
+    (random symmetric H + iD) pivots off the diagonal in most columns, so every swap path moves
+    rows; n = 1300 has ragged panels and several cluster sizes."""
+    P = synth.make_pencil(key, n=n, m0=m0)
     z, w = _oracle_nodes(P)
-    f = _handle(P)
-    Q = host(f.project(dev(P.A), dev(P.B), dev(P.X0)))
-    assert rel(Q, oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
+    out = {}
+    for v in ("coalesced", "chain", "perm"):
+        monkeypatch.setenv("FEAST_LASWP", v)
+        f = _handle(P)
+        out[v] = host(f.project(dev(P.A), dev(P.B), dev(P.X0)))
+    assert np.array_equal(out["coalesced"], out["chain"]) and np.array_equal(out["coalesced"], out["perm"])
+    assert rel(out["coalesced"], oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
 
 
 @pytest.mark.parametrize("one_row", ["0", "1"])
