@@ -615,16 +615,37 @@ void diag_apply(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t k, in
   feast::zgemm_launch(p, conj, feast::ZG_GEN, v.sm);
 }
 
+// Substitutions with the LU factors, two-level: 64-row blocks (the inverted 64x64 diagonal blocks
+// applied by in-place DMMA products, K = 64 updates inside an outer block) and outer blocks of
+// solve_nb() rows whose off-block update is ONE DMMA GEMM with K = solve_nb (the K = 64 updates of
+// a one-level sweep keep every CTA in its pipeline prologue / epilogue).
+int64_t solve_nb() {
+  static const int64_t v = [] {
+    const char* e = getenv("FEAST_SOLVE_NB");
+    const int64_t x = e ? atoll(e) : 256;
+    return (x >= 64 && x % 64 == 0) ? x : 256;
+  }();
+  return v;
+}
+
 // Y <- L^-1 Y (Y already row-permuted): used when the factors are cached (no augmented LU)
 void solve_right_fwd(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t m) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr);
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), NB = solve_nb();
   double2* C = v.Cw;
-  for (int64_t k = 0; k < n; k += h->nb) {
-    const int w = (int)std::min<int64_t>(h->nb, n - k);
-    diag_apply(h, v, Y, sy, k, w, 0, false, m);
-    const int64_t rest = n - k - w;
-    if (rest > 0) {
-      ZgemmArgs p{rest, m, w, C + (k + w) + k * ld, ld, st, Y + k, ld, sy, Y + k + w, ld, sy,
+  for (int64_t K0 = 0; K0 < n; K0 += NB) {
+    const int64_t K1 = std::min(n, K0 + NB);
+    for (int64_t k = K0; k < K1; k += h->nb) {
+      const int w = (int)std::min<int64_t>(h->nb, K1 - k);
+      diag_apply(h, v, Y, sy, k, w, 0, false, m);
+      const int64_t rest = K1 - k - w;
+      if (rest > 0) {   // inside the outer block
+        ZgemmArgs p{rest, m, w, C + (k + w) + k * ld, ld, st, Y + k, ld, sy, Y + k + w, ld, sy,
+                    make_double2(-1, 0), make_double2(1, 0), v.nbat};
+        feast::zgemm_launch(p, false, feast::ZG_SUB, v.sm);
+      }
+    }
+    if (K1 < n) {       // Y[K1:] -= L[K1:, K0:K1] Y[K0:K1]
+      ZgemmArgs p{n - K1, m, K1 - K0, C + K1 + K0 * ld, ld, st, Y + K0, ld, sy, Y + K1, ld, sy,
                   make_double2(-1, 0), make_double2(1, 0), v.nbat};
       feast::zgemm_launch(p, false, feast::ZG_SUB, v.sm);
     }
@@ -633,15 +654,24 @@ void solve_right_fwd(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t 
 
 // Y <- U^-1 Y  (Y = L^-1 P R already: the forward substitution ran inside the augmented LU)
 void solve_right_back(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t m) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr);
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), NB = solve_nb();
   double2* C = v.Cw;
-  const int64_t last = ((n - 1) / h->nb) * h->nb;
-  for (int64_t k = last; k >= 0; k -= h->nb) {
-    const int w = (int)std::min<int64_t>(h->nb, n - k);
-    diag_apply(h, v, Y, sy, k, w, 1, false, m);
-    if (k > 0) {
-      ZgemmArgs p{k, m, w, C + k * ld, ld, st, Y + k, ld, sy, Y, ld, sy, make_double2(-1, 0), make_double2(1, 0),
-                  v.nbat};
+  const int64_t lastK0 = ((n - 1) / NB) * NB;
+  for (int64_t K0 = lastK0; K0 >= 0; K0 -= NB) {
+    const int64_t K1 = std::min(n, K0 + NB);
+    const int64_t last = K0 + ((K1 - 1 - K0) / h->nb) * h->nb;
+    for (int64_t k = last; k >= K0; k -= h->nb) {
+      const int w = (int)std::min<int64_t>(h->nb, K1 - k);
+      diag_apply(h, v, Y, sy, k, w, 1, false, m);
+      if (k > K0) {     // Y[K0:k] -= U[K0:k, k:k+w] Y[k:k+w]
+        ZgemmArgs p{k - K0, m, w, C + K0 + k * ld, ld, st, Y + k, ld, sy, Y + K0, ld, sy, make_double2(-1, 0),
+                    make_double2(1, 0), v.nbat};
+        feast::zgemm_launch(p, false, feast::ZG_SUB, v.sm);
+      }
+    }
+    if (K0 > 0) {       // Y[0:K0] -= U[0:K0, K0:K1] Y[K0:K1]
+      ZgemmArgs p{K0, m, K1 - K0, C + K0 * ld, ld, st, Y + K0, ld, sy, Y, ld, sy, make_double2(-1, 0),
+                  make_double2(1, 0), v.nbat};
       feast::zgemm_launch(p, false, feast::ZG_SUB, v.sm);
     }
   }
@@ -649,26 +679,42 @@ void solve_right_back(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t
 
 // Y <- L^-H U^-H Y   (then the caller applies P^T): M^H = U^H L^H P  (P:438-439 same factors)
 void solve_left(feast_ctx* h, const Lu& v, double2* Y) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), m = h->mr, sy = ld * m;
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), m = h->mr, sy = ld * m, NB = solve_nb();
   double2* C = v.Cw;
-  for (int64_t k = 0; k < n; k += h->nb) {  // U^H: lower, non-unit
-    const int w = (int)std::min<int64_t>(h->nb, n - k);
-    diag_apply(h, v, Y, sy, k, w, 1, true, m);   // (U_kk^H)^-1 = (U_kk^-1)^H
-    const int64_t rest = n - k - w;
-    if (rest > 0) {
-      // Y[k+w:] -= (U[k:k+w, k+w:])^H Y[k:k+w]
-      ZgemmArgs p{rest, m, w, C + k + (k + w) * ld, ld, st, Y + k, ld, sy, Y + k + w, ld, sy,
+  for (int64_t K0 = 0; K0 < n; K0 += NB) {  // U^H: lower, non-unit
+    const int64_t K1 = std::min(n, K0 + NB);
+    for (int64_t k = K0; k < K1; k += h->nb) {
+      const int w = (int)std::min<int64_t>(h->nb, K1 - k);
+      diag_apply(h, v, Y, sy, k, w, 1, true, m);   // (U_kk^H)^-1 = (U_kk^-1)^H
+      const int64_t rest = K1 - k - w;
+      if (rest > 0) {   // Y[k+w:K1] -= (U[k:k+w, k+w:K1])^H Y[k:k+w]
+        ZgemmArgs p{rest, m, w, C + k + (k + w) * ld, ld, st, Y + k, ld, sy, Y + k + w, ld, sy,
+                    make_double2(-1, 0), make_double2(1, 0), v.nbat};
+        feast::zgemm_launch(p, true, feast::ZG_SUB, v.sm);
+      }
+    }
+    if (K1 < n) {       // Y[K1:] -= (U[K0:K1, K1:])^H Y[K0:K1]
+      ZgemmArgs p{n - K1, m, K1 - K0, C + K0 + K1 * ld, ld, st, Y + K0, ld, sy, Y + K1, ld, sy,
                   make_double2(-1, 0), make_double2(1, 0), v.nbat};
       feast::zgemm_launch(p, true, feast::ZG_SUB, v.sm);
     }
   }
-  const int64_t last = ((n - 1) / h->nb) * h->nb;
-  for (int64_t k = last; k >= 0; k -= h->nb) {  // L^H: upper, unit
-    const int w = (int)std::min<int64_t>(h->nb, n - k);
-    diag_apply(h, v, Y, sy, k, w, 0, true, m);   // (L_kk^H)^-1 = (L_kk^-1)^H
-    if (k > 0) {
-      // Y[0:k] -= (L[k:k+w, 0:k])^H Y[k:k+w]
-      ZgemmArgs p{k, m, w, C + k, ld, st, Y + k, ld, sy, Y, ld, sy, make_double2(-1, 0), make_double2(1, 0), v.nbat};
+  const int64_t lastK0 = ((n - 1) / NB) * NB;
+  for (int64_t K0 = lastK0; K0 >= 0; K0 -= NB) {  // L^H: upper, unit
+    const int64_t K1 = std::min(n, K0 + NB);
+    const int64_t last = K0 + ((K1 - 1 - K0) / h->nb) * h->nb;
+    for (int64_t k = last; k >= K0; k -= h->nb) {
+      const int w = (int)std::min<int64_t>(h->nb, K1 - k);
+      diag_apply(h, v, Y, sy, k, w, 0, true, m);   // (L_kk^H)^-1 = (L_kk^-1)^H
+      if (k > K0) {     // Y[K0:k] -= (L[k:k+w, K0:k])^H Y[k:k+w]
+        ZgemmArgs p{k - K0, m, w, C + k + K0 * ld, ld, st, Y + k, ld, sy, Y + K0, ld, sy, make_double2(-1, 0),
+                    make_double2(1, 0), v.nbat};
+        feast::zgemm_launch(p, true, feast::ZG_SUB, v.sm);
+      }
+    }
+    if (K0 > 0) {       // Y[0:K0] -= (L[K0:K1, 0:K0])^H Y[K0:K1]
+      ZgemmArgs p{K0, m, K1 - K0, C + K0, ld, st, Y + K0, ld, sy, Y, ld, sy, make_double2(-1, 0),
+                  make_double2(1, 0), v.nbat};
       feast::zgemm_launch(p, true, feast::ZG_SUB, v.sm);
     }
   }

@@ -458,3 +458,26 @@ def test_register_panel_height_spectral(n):
     rho = 1.0 / (1.0 + ((P.lam - s.c) / s.r) ** P.q)
     Qs = P.V @ (rho[:, None] * torch.linalg.solve(P.V, P.X0))
     assert float(torch.linalg.norm(Q - Qs) / torch.linalg.norm(Qs)) <= TOL
+
+
+@pytest.mark.parametrize("nb", ["64", "128", "256"])
+@pytest.mark.parametrize("n,m0", [(1000, 24), (1345, 8)])
+def test_two_level_substitutions(monkeypatch, nb, n, m0):
+    """Back substitution, left solves and (factor cache) forward substitution with outer blocks of
+    FEAST_SOLVE_NB rows (64 = the one-level sweep): right and left projectors from one LU, and the
+    cached-factor path, equal the oracle's on ragged sizes (n not a multiple of 64 or of the outer
+    block)."""
+    monkeypatch.setenv("FEAST_SOLVE_NB", nb)
+    P = synth.make_pencil("C4", n=n, m0=m0)
+    z, w = _oracle_nodes(P)
+    V = synth.random_block(n, m0, 17)
+    f = _handle(P, fb.BI)
+    Q, QL = f.project_bi(dev(P.A), None, dev(P.X0), dev(V))
+    assert rel(host(Q), oracle.project(P.A, None, P.X0, z, w)) <= TOL
+    assert rel(host(QL), oracle.project(P.A, None, V, z, w, left=True)) <= TOL
+    g = _handle(P)
+    g.factor_cache(True)
+    A, X = dev(P.A), dev(P.X0)
+    g.project(A, None, X)
+    Q2 = host(g.project(A, None, X))          # substitution-only call on the cached factors
+    assert rel(Q2, oracle.project(P.A, None, P.X0, z, w)) <= TOL
