@@ -63,6 +63,7 @@ struct feast_ctx {
   bool cache_on = false, cache_valid = false;   // factor-once reuse across calls
   const void *cache_A = nullptr, *cache_B = nullptr;
   int64_t nbo = 256;                  // outer block (trailing-update K); multiple of 64
+  int64_t solve_nb = 256;             // outer block of the substitutions (FEAST_SOLVE_NB, multiple of 64)
   int64_t wp = 32;                    // cluster-panel width (divides 64)
   int64_t wide_panel_rows = 768;      // 64-wide cluster panels once n - k <= this (FEAST_WIDE_ROWS)
   cudaStream_t side = nullptr;        // high-priority stream for the lookahead panel
@@ -617,20 +618,11 @@ void diag_apply(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t k, in
 
 // Substitutions with the LU factors, two-level: 64-row blocks (the inverted 64x64 diagonal blocks
 // applied by in-place DMMA products, K = 64 updates inside an outer block) and outer blocks of
-// solve_nb() rows whose off-block update is ONE DMMA GEMM with K = solve_nb (the K = 64 updates of
+// h->solve_nb rows whose off-block update is ONE DMMA GEMM with K = solve_nb (the K = 64 updates of
 // a one-level sweep keep every CTA in its pipeline prologue / epilogue).
-int64_t solve_nb() {
-  static const int64_t v = [] {
-    const char* e = getenv("FEAST_SOLVE_NB");
-    const int64_t x = e ? atoll(e) : 256;
-    return (x >= 64 && x % 64 == 0) ? x : 256;
-  }();
-  return v;
-}
-
 // Y <- L^-1 Y (Y already row-permuted): used when the factors are cached (no augmented LU)
 void solve_right_fwd(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t m) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), NB = solve_nb();
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), NB = h->solve_nb;
   double2* C = v.Cw;
   for (int64_t K0 = 0; K0 < n; K0 += NB) {
     const int64_t K1 = std::min(n, K0 + NB);
@@ -654,7 +646,7 @@ void solve_right_fwd(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t 
 
 // Y <- U^-1 Y  (Y = L^-1 P R already: the forward substitution ran inside the augmented LU)
 void solve_right_back(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t m) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), NB = solve_nb();
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), NB = h->solve_nb;
   double2* C = v.Cw;
   const int64_t lastK0 = ((n - 1) / NB) * NB;
   for (int64_t K0 = lastK0; K0 >= 0; K0 -= NB) {
@@ -679,7 +671,7 @@ void solve_right_back(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t
 
 // Y <- L^-H U^-H Y   (then the caller applies P^T): M^H = U^H L^H P  (P:438-439 same factors)
 void solve_left(feast_ctx* h, const Lu& v, double2* Y) {
-  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), m = h->mr, sy = ld * m, NB = solve_nb();
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), m = h->mr, sy = ld * m, NB = h->solve_nb;
   double2* C = v.Cw;
   for (int64_t K0 = 0; K0 < n; K0 += NB) {  // U^H: lower, non-unit
     const int64_t K1 = std::min(n, K0 + NB);
@@ -1192,6 +1184,10 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   if (const char* e = getenv("FEAST_GROUPS")) {
     const int v = atoi(e);
     if (v >= 1 && v <= feast_ctx::GMAX) h->groups = v;
+  }
+  if (const char* e = getenv("FEAST_SOLVE_NB")) {
+    const long v = atol(e);
+    if (v >= 64 && v % 64 == 0) h->solve_nb = v;
   }
   if (const char* e = getenv("FEAST_NBO")) {
     const long v = atol(e);
