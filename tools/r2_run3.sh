@@ -15,3 +15,5 @@ FEAST_SOLVE_NB=64 timeout 600 python bench.py --config C2 --steps 20 --warmup 5 
 timeout 1200 python tools/rank_share_timing.py C4 --out gpurun_out/r2_share_C4.json > gpurun_out/r2_share_C4.log 2>&1
 timeout 600 python tools/rank_share_timing.py C2 --steps 5 --out gpurun_out/r2_share_C2.json > gpurun_out/r2_share_C2.log 2>&1
 tail -n 4 gpurun_out/r2_gpu_tests_v3.log gpurun_out/r2_phase*.log gpurun_out/r2_share*.log
+timeout 900 python tools/timeline.py C4 --out gpurun_out/r2_tl_C4.csv > gpurun_out/r2_tl_C4.log 2>&1
+python tools/timeline_rate.py gpurun_out/r2_tl_C4.csv 40 > gpurun_out/r2_tl_C4_rate.log 2>&1

@@ -19,23 +19,44 @@ ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--batch", type=int, default=0)
 ap.add_argument("--world", type=int, default=1, help="time rank 0's node share of a P-rank job")
 args = ap.parse_args()
-P = synth.make_pencil(args.key, n=args.n)
+spec = synth.CONFIGS[args.key]
+bi = spec.mode == "bi"
+if (args.n or spec.n) >= 4096:
+    P = synth.make_pencil_torch(args.key, n=args.n)
+    A, B, X = P.A, P.B, P.X0
+else:
+    P = synth.make_pencil(args.key, n=args.n)
+    d = lambda a: None if a is None else torch.from_numpy(np.asfortranarray(a)).to("cuda")
+    A, B, X = d(P.A), d(P.B), d(P.X0)
 s = P.spec
-f = Feast(P.n, P.m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.RIGHT, P.B is None, max_batch=args.batch,
+V = fb.colmajor(torch.linalg.solve(X.conj().T @ X, X.conj().T).conj().T) if bi else None
+n, m0 = P.n, P.m0
+del P
+torch.cuda.empty_cache()
+f = Feast(n, m0, s.c, s.r, s.aspect, s.n_e, s.rule, fb.BI if bi else fb.RIGHT, B is None, max_batch=args.batch,
           world=args.world, partial=args.world > 1)
-d = lambda a: None if a is None else torch.from_numpy(np.asfortranarray(a)).to("cuda")
-A, B, X = d(P.A), d(P.B), d(P.X0)
-Q = f.project(A, B, X)
-f.project(A, B, X, Q)
+Q = fb.empty_colmajor(n, m0)
+QL = fb.empty_colmajor(n, m0) if bi else None
+
+
+def proj():
+    if bi:
+        f.project_bi(A, B, X, V, Q, QL)
+    else:
+        f.project(A, B, X, Q)
+
+
+proj()
+proj()
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(f.stream)
-f.project(A, B, X, Q)
+proj()
 e1.record(f.stream)
 torch.cuda.synchronize()
 print(f"{args.key}: project without events {e0.elapsed_time(e1):.3f} ms")
 f.profile(True)
-f.project(A, B, X, Q)
+proj()
 recs = f.profile_records()
 f.profile(False)
 wall = max(r[3] for r in recs)
