@@ -263,6 +263,17 @@ int feast_monitors(feast_handle h, double* res_k, double* trace_k, int32_t* ncan
 int feast_filter_gap(feast_handle h, int64_t nl, const double* lam, int64_t p, double* abs_sorted, int32_t* order,
                      int32_t* m_inside, int32_t* m_prime, double* eps, double* log10_gap);
 
+/* Asynchronous mode (enable = 1): feast_project / _left / _bi and feast_reduce return as soon as
+ * their work (including the node-sum collective) is enqueued on the stream, without a host
+ * synchronisation, so consecutive calls pipeline.  The pivot statistics of each projection are
+ * copied to pinned host memory on the stream; feast_sync (or feast_node_stats) waits for them
+ * and returns the status the synchronous call would have returned (FEAST_OK, FEAST_W_ILLCOND,
+ * FEAST_E_SINGULAR for the LAST projection).  Results are valid on the caller's stream order as
+ * usual.  feast_iterate and the count estimates read results on the host and always judge.
+ * Default 0 (every call synchronises and returns its own status). */
+int feast_set_async(feast_handle h, int32_t enable);
+int feast_sync(feast_handle h);
+
 /* Pivot diagnostics of the last projection (host outputs): min_rel_pivot[q] =
  * min|u_ii| / max|u_ii| per node (owned nodes only; others are set to -1), *worst_node =
  * index of the smallest ratio.  Either pointer may be NULL. */

@@ -130,6 +130,12 @@ struct feast_ctx {
   feast_allreduce_fn ar = nullptr;
   void* ar_user = nullptr;
   bool partial = false;               // feast_set_partial: return this rank's partial node sum
+  // feast_set_async: projector / reduce calls return once enqueued; the pivot statistics land in
+  // pinned host memory and are judged by feast_sync (or the next feast_node_stats)
+  bool async = false, pending = false;
+  double* h_stats = nullptr;          // pinned: 2 nu doubles
+  int32_t* h_info = nullptr;          // pinned: nu + 1 ints (the last: real-pencil violation flag)
+  cudaEvent_t ev_stats = nullptr;
   // NEXT-3: monitors of the last feast_iterate
   bool count_on = false;              // feast_set_count_estimate: eig(V^^H B U^) in Bi-FEAST iterations
   double mon_res = -1.0;
@@ -900,6 +906,8 @@ int node_sum(feast_ctx* h, double2* Q, int64_t ldq, double2* QL, int64_t ldql) {
   return FEAST_OK;
 }
 
+int judge_stats(feast_ctx* h);
+
 int project_impl(feast_ctx* h, const double2* A, int64_t lda, const double2* B, int64_t ldb, const double2* X,
                  int64_t ldx, const double2* V, int64_t ldv, double2* Q, int64_t ldq, double2* QL, int64_t ldql) {
   if (h->world > 1 && !h->partial && !h->ar)
@@ -961,15 +969,27 @@ int project_impl(feast_ctx* h, const double2* A, int64_t lda, const double2* B, 
   CUDA_TRY(h, cudaGetLastError());
   if (int e = node_sum(h, Q, ldq, QL, ldql)) return e;
   h->launches = feast::g_launches - t0;
-  // pivot diagnostics of the owned units, reported per node (both poles of an orbit share it)
-  std::vector<double> st(2 * (size_t)h->nu);
-  std::vector<int32_t> inf(h->nu);
-  int32_t viol = 0;
-  CUDA_TRY(h, cudaMemcpyAsync(st.data(), h->stats, st.size() * 8, cudaMemcpyDeviceToHost, h->stream));
-  CUDA_TRY(h, cudaMemcpyAsync(inf.data(), h->info, inf.size() * 4, cudaMemcpyDeviceToHost, h->stream));
-  if (h->real) CUDA_TRY(h, cudaMemcpyAsync(&viol, h->realviol, 4, cudaMemcpyDeviceToHost, h->stream));
-  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-  if (viol) return fail(h, FEAST_E_ARG, "real-pencil mode: A or B has a nonzero imaginary part%s");
+  // pivot diagnostics of the owned units into pinned host memory; judged now (synchronous calls)
+  // or by feast_sync (async mode: the call returns once everything is enqueued)
+  CUDA_TRY(h, cudaMemcpyAsync(h->h_stats, h->stats, 2 * (size_t)h->nu * 8, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(h->h_info, h->info, (size_t)h->nu * 4, cudaMemcpyDeviceToHost, h->stream));
+  h->h_info[h->nu] = 0;
+  if (h->real) CUDA_TRY(h, cudaMemcpyAsync(h->h_info + h->nu, h->realviol, 4, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaEventRecord(h->ev_stats, h->stream));
+  h->pending = true;
+  if (h->async) return FEAST_OK;
+  return judge_stats(h);
+}
+
+// Evaluate the pivot statistics of the last projection (waits for them): FEAST_E_SINGULAR if some
+// node's min|u_ii|/max|u_ii| < 1e-14 or an exact zero pivot, FEAST_W_ILLCOND below 1e-10.
+int judge_stats(feast_ctx* h) {
+  if (!h->pending) return FEAST_OK;
+  CUDA_TRY(h, cudaEventSynchronize(h->ev_stats));
+  h->pending = false;
+  const double* st = h->h_stats;
+  const int32_t* inf = h->h_info;
+  if (inf[h->nu]) return fail(h, FEAST_E_ARG, "real-pencil mode: A or B has a nonzero imaginary part%s");
   h->minrel.assign(h->q, -1.0);
   h->worst = -1;
   double wr = INFINITY;
@@ -1301,6 +1321,11 @@ int feast_bind_workspace(feast_handle h, void* p, size_t bytes) {
   if (bytes < need) return fail(h, FEAST_E_NOMEM, "workspace too small%s");
   if (((uintptr_t)p) & 255) return fail(h, FEAST_E_ARG, "workspace not 256-byte aligned%s");
   graph_reset(h);
+  if (!h->h_stats) {
+    CUDA_TRY(h, cudaMallocHost(&h->h_stats, 2 * (size_t)h->q * 8 + 64));
+    CUDA_TRY(h, cudaMallocHost(&h->h_info, ((size_t)h->q + 1) * 4 + 64));
+    CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_stats, cudaEventDisableTiming));
+  }
   h->ws = p;
   h->ws_bytes = bytes;
   layout(h, (char*)p);
@@ -1395,7 +1420,7 @@ int reduce_impl(feast_ctx* h, const void* A, int64_t lda, const void* B, int64_t
       }
     }
   }
-  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  if (!h->async) CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   h->launches = feast::g_launches - t0;
   return FEAST_OK;
 }
@@ -1421,9 +1446,10 @@ int feast_estimate_count(feast_handle h, const void* A, int64_t lda, const void*
   Join j_(h);
   const int64_t n = h->n, m = h->m0;
   // Q = rho(B^-1 A) U (this rank's nodes, then the node sum over ranks inside project_impl)
-  const int pst = project_impl(h, (const double2*)A, lda, (const double2*)B, ldb, (const double2*)U, ldu, nullptr, 0,
+  int pst = project_impl(h, (const double2*)A, lda, (const double2*)B, ldb, (const double2*)U, ldu, nullptr, 0,
                                (double2*)Q, ldq, nullptr, 0);
   if (pst < 0) return pst;
+  if (h->async && (pst = judge_stats(h)) < 0) return pst;   // these calls read their results now
   // Hutchinson trace estimate: m ~ tr rho(B^-1 A) ~ Re tr(U^H Q) / m0 (deterministic block sums)
   constexpr int NP = 64;
   feast::cdot_launch((const double2*)U, ldu, (const double2*)Q, ldq, n, m, h->SK, NP, h->stream);
@@ -1469,6 +1495,7 @@ int feast_iterate(feast_handle h, const void* A, int64_t lda, const void* B, int
                : project_impl(h, (const double2*)A, lda, (const double2*)B, ldb, (const double2*)X, ldx, nullptr, 0,
                               it.Qr, n, nullptr, 0);
   if (pst < 0) return pst;   // (node-summed over the ranks inside project_impl)
+  if (h->async && (pst = judge_stats(h)) < 0) return pst;
   // orthonormalise U^ (and V^) (reading R13), cuSOLVER Householder QR
   // FEAST_TIMING=1: host wall time of the iteration phases (stream-synchronised), to stderr
   static const bool timing = getenv("FEAST_TIMING") != nullptr;
@@ -1624,9 +1651,10 @@ int feast_estimate_count_bi(feast_handle h, const void* A, int64_t lda, const vo
   const int64_t n = h->n, m = h->m0, ld = h->ldc;
   const double2 one = make_double2(1, 0), zero = make_double2(0, 0);
   // Bi-FEAST steps 4-5: U^ = rho U, V^ = left projector of V (node sums over the ranks inside)
-  const int pst = project_impl(h, (const double2*)A, lda, (const double2*)B, ldb, (const double2*)U, ldu,
+  int pst = project_impl(h, (const double2*)A, lda, (const double2*)B, ldb, (const double2*)U, ldu,
                                (const double2*)V, ldv, (double2*)Q, ldq, (double2*)QL, ldql);
   if (pst < 0) return pst;
+  if (h->async && (pst = judge_stats(h)) < 0) return pst;   // these calls read their results now
   // V^^H B U^ (m0 x m0; B U^ on the rows this rank owns when sharded: partials all-reduced)
   const bool shard = h->world > 1 && h->ar != nullptr;
   const int64_t r0 = shard ? h->rank * n / h->world : 0, r1 = shard ? (h->rank + 1) * n / h->world : n, nr = r1 - r0;
@@ -1674,8 +1702,21 @@ int feast_filter_gap(feast_handle h, int64_t nl, const double* lam, int64_t p, d
   return FEAST_OK;
 }
 
+int feast_set_async(feast_handle h, int32_t enable) {
+  if (!h) return FEAST_E_ARG;
+  h->async = enable != 0;
+  return FEAST_OK;
+}
+
+int feast_sync(feast_handle h) {
+  if (!h) return FEAST_E_ARG;
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  return judge_stats(h);
+}
+
 int feast_node_stats(feast_handle h, double* min_rel_pivot, int32_t* worst_node) {
   if (!h) return FEAST_E_ARG;
+  if (h->pending) judge_stats(h);
   if (min_rel_pivot)
     for (int j = 0; j < h->q; ++j) min_rel_pivot[j] = j < (int)h->minrel.size() ? h->minrel[j] : -1.0;
   if (worst_node) *worst_node = h->worst;
@@ -1881,6 +1922,9 @@ void feast_destroy(feast_handle h) {
     cudaEventDestroy(h->ev_out);
   }
   if (h->itmem) cudaFree(h->itmem);
+  if (h->h_stats) cudaFreeHost(h->h_stats);
+  if (h->h_info) cudaFreeHost(h->h_info);
+  if (h->ev_stats) cudaEventDestroy(h->ev_stats);
   if (h->solp) cusolverDnDestroyParams(h->solp);
   if (h->sol) cusolverDnDestroy(h->sol);
   delete h;

@@ -38,6 +38,7 @@ EXPORTS = ["feast_init", "feast_workspace_bytes", "feast_bind_workspace", "feast
            "feast_node_stats", "feast_factor_cache", "feast_set_real_pencil",
            "feast_set_complex_symmetric", "feast_estimate_count", "feast_set_contour", "feast_filter",
            "feast_estimate_count_bi", "feast_set_count_estimate", "feast_monitors", "feast_filter_gap",
+           "feast_set_async", "feast_sync",
            "feast_last_launch_count", "feast_profile", "feast_profile_summary",
            "feast_profile_records", "feast_last_error",
            "feast_version", "feast_destroy"]
@@ -84,6 +85,8 @@ def load_library(path: str = LIB_PATH):
     lib.feast_filter.argtypes = [P, I64, P, P]
     lib.feast_estimate_count_bi.argtypes = [P, P, I64, P, I64, P, I64, P, I64, P, I64, P, I64, P, P]
     lib.feast_set_count_estimate.argtypes = [P, I32]
+    lib.feast_set_async.argtypes = [P, I32]
+    lib.feast_sync.argtypes = [P]
     lib.feast_monitors.argtypes = [P, P, P, P, P, P]
     lib.feast_filter_gap.argtypes = [P, I64, P, I64, P, P, P, P, P, P]
     lib.feast_profile.argtypes = [P, I32]
@@ -352,6 +355,15 @@ class Feast:
             self.h, pa, lda, pb, ldb, pu, ldu, pv, ldv, pq, ldq, pl, ldl, mu.ctypes.data_as(ctypes.c_void_p),
             ctypes.byref(cnt)))
         return cnt.value, mu, Q, QL
+
+    def set_async(self, enable: bool):
+        """Projector / reduce calls return once enqueued (no host synchronisation); sync() waits
+        and returns the last projection's status (raises on FEAST_E_SINGULAR)."""
+        self._check(self.lib.feast_set_async(self.h, int(bool(enable))))
+
+    def sync(self):
+        self.status = self._check(self.lib.feast_sync(self.h))
+        return self.status
 
     def set_count_estimate(self, enable: bool):
         """Track the eig(V^^H B U^) count estimate in every Bi-FEAST iterate() (see monitors())."""

@@ -481,3 +481,34 @@ def test_two_level_substitutions(monkeypatch, nb, n, m0):
     g.project(A, None, X)
     Q2 = host(g.project(A, None, X))          # substitution-only call on the cached factors
     assert rel(Q2, oracle.project(P.A, None, P.X0, z, w)) <= TOL
+
+
+def test_async_mode_pipelines_and_defers_status():
+    """feast_set_async: projector and reduce calls return once enqueued; results (read in stream
+    order) equal the oracle's; the singular-node status of a projection is reported by
+    feast_sync instead of the call."""
+    P = synth.make_pencil("C2", n=260, m0=12)
+    z, w = _oracle_nodes(P)
+    f = _handle(P)
+    f.set_async(True)
+    A, B = dev(P.A), dev(P.B)
+    X2 = synth.random_block(P.n, P.m0, 23)
+    Q1 = f.project(A, B, dev(P.X0))
+    Q2 = f.project(A, B, dev(X2))
+    Ah, Bh = f.reduce(A, B, Q2)
+    assert f.sync() == fb.OK
+    assert rel(host(Q1), oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
+    Q2o = oracle.project(P.A, P.B, X2, z, w)
+    assert rel(host(Q2), Q2o) <= TOL
+    assert rel(host(Ah), Q2o.conj().T @ P.A @ Q2o) <= 1e-10
+    # singular node: the call returns, feast_sync reports it
+    p = np.exp(1j * np.pi / 4)
+    Ad = np.diag([p, 0.1, 3.0, -0.2 + 0.1j]).astype(complex)
+    g = Feast(4, 2, 0j, 1.0, 1.0, 4, fb.RULE_TRAPEZOID, fb.RIGHT, True)
+    zz, _, _, _ = g.nodes()
+    Ad[0, 0] = zz[0]
+    g.set_async(True)
+    g.project(dev(Ad), None, dev(np.eye(4)[:, :2]))
+    with pytest.raises(FeastError) as e:
+        g.sync()
+    assert e.value.code == fb.E_SINGULAR
