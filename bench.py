@@ -271,6 +271,7 @@ def run_gpu(args):
     torch.cuda.empty_cache()
     f = Feast(n, m0, spec.c, spec.r, spec.aspect, spec.n_e, spec.rule, fb.BI if bi else fb.RIGHT, B is None,
               rank=rank, world=world)
+    f.set_async(True)      # steps pipeline on the stream; the status is checked by f.sync()
     stream = f.stream
     Q = empty_colmajor(n, m0)
     QL = empty_colmajor(n, m0) if bi else None
@@ -312,6 +313,7 @@ def run_gpu(args):
     e1.record(stream)
     barrier()
     clocks = clk.stop()
+    f.sync()               # raises if a node's shifted matrix was singular
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     gpu_launches = launches[0] * args.steps
     bounded = max(1, min(2, args.steps)) if ms > 2000 else max(1, min(3, args.steps))
