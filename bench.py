@@ -317,6 +317,17 @@ def run_gpu(args):
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     gpu_launches = launches[0] * args.steps
     bounded = max(1, min(2, args.steps)) if ms > 2000 else max(1, min(3, args.steps))
+    if args.timing_only:   # experiments (A/B of knobs): the timed steps alone, no extra passes
+        if rank == 0:
+            lu_solve, total = _flops(spec, n, m0, q)
+            print(json.dumps({"timing_only": True, "config": args.config, "n_gpus": world, "ms_per_step": ms,
+                              "value": 1e3 / ms, "lu_solve_frac_peak": lu_solve / (ms * 1e-3) / 1e12 /
+                              FP64_PEAK_TFLOPS / world, "clocks": clocks, "gpu_launches": gpu_launches,
+                              "env": {k: v for k, v in os.environ.items() if k.startswith("FEAST_")}}), flush=True)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
 
     # ---- per-kernel-class timing: CUDA events around every launch on its launching stream, in a
     # SERIALISED pass after the timed region (one stream, no lookahead / node groups / graph), so
@@ -448,6 +459,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dry-run", action="store_true", help="launcher / rank plumbing only (CPU, gloo)")
+    ap.add_argument("--timing-only", action="store_true", help="experiments: the timed steps only (no profile, "
+                                                               "e2e, iterate or oracle passes)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return _relaunch(args)

@@ -51,6 +51,7 @@ enum { LASWP_COALESCED = 0, LASWP_CHAIN = 1, LASWP_PERM = 2 };
 void laswp_launch(Batched C, int64_t n, int64_t k, int cnt, const int32_t* ipiv, int64_t c0, int64_t c1, int batch,
                   cudaStream_t s, int variant = LASWP_COALESCED);
 // Cluster panel with the panel resident in shared memory (rows never moved; see panel_smem.cu).
+int tall_variant();
 bool panel_smem_fits(int64_t n, int w, int cs);
 int panel_smem_max_clusters(int64_t L, int w, int cs);
 void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info, int batch,

@@ -20,6 +20,7 @@
 // way, every CTA forms U12 = L11^-1 (pivot rows) and applies the rank-W update to its own
 // non-pivot rows in shared memory (one smem read-modify-write per element per chunk).
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <float.h>
 #include <limits.h>
 
@@ -540,7 +541,7 @@ int panel_smem_max_clusters(int64_t L, int w, int cs) {
   const int Lc = (int)((L + cs - 1) / cs);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(16 * cs), 1, 1);
-  cfg.blockDim = dim3(Lc <= 2 * PT ? PT : 2 * PT, 1, 1);
+  cfg.blockDim = dim3(Lc <= 2 * PT ? PT : (Lc <= 4 * PT || tall_variant() != 2 ? 2 * PT : 4 * PT), 1, 1);
   const int wc = 8;
   cfg.dynamicSmemBytes = (size_t)Lc * (w > wc ? w - wc : 0) * sizeof(double2);
   cudaLaunchAttribute attr[1];
@@ -552,17 +553,27 @@ int panel_smem_max_clusters(int64_t L, int w, int cs) {
   cfg.numAttrs = 1;
   int nc = -1;
   auto k = Lc <= PT ? panel_smem_kernel<1, 8, PT, true>
-                    : (Lc <= 2 * PT ? panel_smem_kernel<2, 8, PT, true> : panel_smem_kernel<2, 8, 2 * PT, true>);
+                    : (Lc <= 2 * PT ? panel_smem_kernel<2, 8, PT, true>
+                                    : (Lc <= 4 * PT ? panel_smem_kernel<2, 8, 2 * PT, true>
+                                                    : (tall_variant() == 2 ? panel_smem_kernel<2, 8, 4 * PT, true>
+                                                                           : panel_smem_kernel<4, 8, 2 * PT, true>)));
   cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (cudaOccupancyMaxActiveClusters(&nc, k, &cfg) != cudaSuccess) { cudaGetLastError(); return -1; }
   return nc;
 }
 
+// FEAST_TALL_VARIANT: 4 (default) = 256 threads x 4 rows, 2 = 512 threads x 2 rows for panels of
+// 513..1024 rows per CTA; 0 = keep those panels on the register-chunk kernel (lu.cu)
+int tall_variant() {
+  static const int v = [] { const char* e = getenv("FEAST_TALL_VARIANT"); return e ? atoi(e) : 4; }();
+  return v;
+}
+
 bool panel_smem_fits(int64_t n, int w, int cs) {
   const int64_t Lc = (n + cs - 1) / cs;
   const int wc = 8;   // register chunk width (see panel_smem_launch)
-  return w <= WMAX && (size_t)Lc * (w > wc ? w - wc : 0) * sizeof(double2) <= 190 * 1024 && Lc <= 4 * PT;
+  return w <= WMAX && (size_t)Lc * (w > wc ? w - wc : 0) * sizeof(double2) <= 190 * 1024 && Lc <= 8 * PT;
 }
 
 void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info, int batch,
@@ -586,7 +597,11 @@ void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, do
   if (Lc <= PT) launch_s<1, 8, PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);
   else if (Lc <= 2 * PT && one_row) launch_s<1, 8, 2 * PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);
   else if (Lc <= 2 * PT) launch_s<2, 8, PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);
-  else launch_s<2, 8, 2 * PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);   // 512 rows: 256 threads x 2
+  else if (Lc <= 4 * PT) launch_s<2, 8, 2 * PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);   // 512 rows: 256 x 2
+  // 513..1024 rows per CTA (tall panels of n = 16384, w <= 16 so the w - 8 shared columns fit):
+  // 256 threads x 4 rows (registers capped at 255) or 512 threads x 2 rows (capped at 128)
+  else if (tall_variant() == 2) launch_s<2, 8, 4 * PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);
+  else launch_s<4, 8, 2 * PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);
 }
 
 }  // namespace feast
