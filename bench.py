@@ -345,11 +345,17 @@ def run_gpu(args):
     achieved = zg["flops"] / (zg["ms"] * 1e-3) / 1e12 if zg["ms"] > 0 else 0.0
     total_prof_ms = sum(v["ms"] for v in prof.values())
     traffic, traffic_src = None, None
+    traffic_ratio = None
     try:  # committed ncu capture of the same serialised step (tools/zgemm_traffic.py)
-        tr = json.load(open(os.path.join(ROOT, "profiles", "zgemm_traffic.json")))
+        tp = os.path.join("profiles", f"zgemm_traffic_{args.config}.json")
+        tr = json.load(open(os.path.join(ROOT, tp)))
         if tr.get("config") == args.config:
-            traffic = tr.get("dram_bytes_per_launch")
-            traffic_src = "profiles/zgemm_traffic.json: " + tr.get("source", "")
+            traffic_ratio = tr.get("traffic_over_algorithmic")
+            # DRAM bytes per launch: the captured ratio to the algorithmic bytes applied to this
+            # run's launches (the same kernels; the capture's own per-launch mean is in the file)
+            traffic = traffic_ratio * zg["bytes"] / max(1, zg["launches"]) if traffic_ratio else None
+            traffic_src = f"{tp} (ncu dram__bytes_read+write of every zgemm launch of one serialised step, " \
+                          f"{tr.get('launches')} launches: {traffic_ratio:.3f} x algorithmic bytes)"
     except Exception:  # noqa: BLE001
         pass
     hbm = _peaks().get("hbm_gbs")
@@ -357,7 +363,7 @@ def run_gpu(args):
                      for k, v in prof.items() if k in ("shift", "laswp", "perm", "accum")}
     roofline = {"bound": "tensor", "kernel": "zgemm_dmma_kernel (FP64 DMMA.8x8x4)", "achieved": achieved,
                 "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
-                "traffic": traffic, "peak_source": FP64_PEAK_NOTE,
+                "traffic": traffic, "traffic_over_algorithmic": traffic_ratio, "peak_source": FP64_PEAK_NOTE,
                 "launches_per_step": zg["launches"] / prof_steps,
                 "algorithmic_flops_per_launch": zg["flops"] / max(1, zg["launches"]),
                 "algorithmic_bytes_per_launch": zg["bytes"] / max(1, zg["launches"]),
