@@ -451,12 +451,12 @@ __global__ void __launch_bounds__(32 * LP_WARPS) laswp_perm_kernel(Batched C, in
 }
 
 // Row swaps, coalesced (BASELINE north_star "a row-swap kernel with coalesced 16-byte
-// access").  The cnt sequential swaps ipiv[k..k+cnt) act on the touched rows only: the block rows
-// k..k+cnt-1 and the pivot rows below.  Slot t names a DESTINATION row d_t (t < cnt: d_t = k + t;
-// t >= cnt: the pivot row ipiv[k + t - cnt] when it lies below the block); its source row is
-// found by tracing d_t back through the swaps in reverse order (each swap is an involution), all
-// slots in parallel (cnt steps per thread, no serial composition, no row table).  Slots whose row
-// does not move are dropped.  Then each warp moves whole columns: lane t gathers the source of
+// access").  The cnt sequential swaps ipiv[k..k+cnt) act on the touched rows only.  The swaps
+// that move something (ipiv != row) are compacted in order (warp ballots); slot t names a
+// DESTINATION row d_t — the block row i_j of swap j (slots < nz) or its pivot row p_j (slots
+// >= nz) — and its source row is found by tracing d_t back through the nz swaps in reverse order
+// (each swap is an involution), all slots in parallel (no serial composition, no row table).
+// Slots whose row does not move are dropped.  Then each warp moves whole columns: lane t gathers the source of
 // slot t into registers, then scatters to d_t, so the writes (and the reads of the pivot-row
 // slots) to the contiguous block rows of a column coalesce into 512-byte warp transactions of
 // 16-byte complex elements; the other half of the accesses are the scattered pivot rows (one
@@ -468,30 +468,47 @@ __global__ void __launch_bounds__(32 * LC_WARPS) laswp_coalesced_kernel(Batched 
                                                                           const int32_t* __restrict__ ipiv_all,
                                                                           int64_t c0, int64_t c1, int cols_per_cta,
                                                                           unsigned long long* moved_bytes) {
-  __shared__ int32_t s_piv[16 * 32 / 2];
+  __shared__ int32_t s_si[16 * 32 / 2], s_sp[16 * 32 / 2];   // the non-trivial swaps, in order
   __shared__ int32_t s_src[16 * 32], s_dst[16 * 32];
+  __shared__ int s_wcnt[LC_WARPS];
   __shared__ int s_nmov;
   const int b = blockIdx.y;
   const int32_t* ipiv = ipiv_all + (int64_t)b * n + k;
-  for (int i = threadIdx.x; i < cnt; i += blockDim.x) s_piv[i] = ipiv[i] - (int)k;   // relative rows
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // 1. ordered compaction of the swaps that move something (p != i): pivoting close to the diagonal
+  //    (the shifted matrices of the BASELINE pencils) leaves only a few of them
+  const int t0 = threadIdx.x;                                   // cnt <= 256 = blockDim
+  const int p0 = t0 < cnt ? ipiv[t0] - (int)k : t0;             // relative rows
+  const bool nontriv = t0 < cnt && p0 != t0;
+  const unsigned bal = __ballot_sync(0xffffffffu, nontriv);
+  if (lane == 0) s_wcnt[warp] = __popc(bal);
   if (threadIdx.x == 0) s_nmov = 0;
   __syncthreads();
-  const int nslot = 2 * cnt;
+  int off = 0, nz = 0;
+#pragma unroll
+  for (int q = 0; q < LC_WARPS; ++q) {
+    off += q < warp ? s_wcnt[q] : 0;
+    nz += s_wcnt[q];
+  }
+  if (nontriv) {
+    const int pos = off + __popc(bal & ((1u << lane) - 1u));
+    s_si[pos] = t0;
+    s_sp[pos] = p0;
+  }
+  __syncthreads();
+  // 2. slots: destination rows i_j (slots < nz: ascending block rows, coalesced when most rows
+  //    move) and p_j (slots >= nz); each traced back through the nz swaps to its source row.  A
+  //    row named twice gives two identical slots (same source, same value): harmless.
+  const int nslot = 2 * nz;
   int mov = 0;
   for (int t = threadIdx.x; t < 32 * SPL; t += blockDim.x) {
-    int d = -1;
-    if (t < cnt) d = t;
-    else if (t < nslot) { const int p = s_piv[t - cnt]; d = p >= cnt ? p : -1; }
+    const int d = t < nz ? s_si[t] : (t < nslot ? s_sp[t - nz] : -1);
     int src = d;
     if (d >= 0)
-      for (int i = cnt - 1; i >= 0; --i) {   // the value that ends in row d came from src
-        const int p = s_piv[i];
-        src = src == i ? p : (src == p ? i : src);
+      for (int j = nz - 1; j >= 0; --j) {   // the value that ends in row d came from src
+        const int a = s_si[j], c = s_sp[j];
+        src = src == a ? c : (src == c ? a : src);
       }
-    // a pivot row named by several swaps appears in several slots: keep the first
-    if (t >= cnt && d >= 0)
-      for (int u = 0; u < t - cnt; ++u)
-        if (s_piv[u] == d) { d = -1; break; }
     const bool mv = d >= 0 && src != d;
     s_dst[t] = mv ? d : -1;
     s_src[t] = mv ? src : 0;
@@ -499,7 +516,6 @@ __global__ void __launch_bounds__(32 * LC_WARPS) laswp_coalesced_kernel(Batched 
   }
   if (moved_bytes && mov) atomicAdd(&s_nmov, mov);
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* base = C.p + (int64_t)b * C.stride + k;
   const int64_t cbeg = c0 + (int64_t)blockIdx.x * cols_per_cta, cend = min(c1, cbeg + cols_per_cta);
   // slot tables in registers for short swap sequences, read from shared memory for long ones
