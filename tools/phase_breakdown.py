@@ -23,8 +23,14 @@ ap.add_argument("--out", default=None)
 args = ap.parse_args()
 spec = synth.CONFIGS[args.key]
 bi = spec.mode == "bi"
-P = synth.make_pencil_torch(args.key)
-A, B, X = P.A, P.B, P.X0
+if spec.n >= 4096:
+    P = synth.make_pencil_torch(args.key)
+    A, B, X = P.A, P.B, P.X0
+else:
+    import numpy as np
+    P = synth.make_pencil(args.key)
+    d = lambda a: None if a is None else torch.from_numpy(np.asfortranarray(a)).to("cuda")
+    A, B, X = d(P.A), d(P.B), d(P.X0)
 n, m0 = P.n, P.m0
 V = fb.colmajor(torch.linalg.solve(X.conj().T @ X, X.conj().T).conj().T) if bi else None
 del P
@@ -66,3 +72,14 @@ for name, sel in (("lu", recs[:last_panel + 1]), ("subst", recs[last_panel + 1:]
         print(f"   {c:6s} {v[0]:6d} launches {v[1]:10.2f} ms  {v[2]:.3e} flop  {tf:6.2f} TF/s")
 if args.out:
     json.dump(out, open(args.out, "w"), indent=1)
+# zgemm launches grouped by algorithmic flops per launch (one group = one launch shape)
+by = defaultdict(lambda: [0, 0.0, 0.0])
+for c, st, t0, t1, fl in recs:
+    if c == "zgemm":
+        g = by[round(fl, -3)]
+        g[0] += 1
+        g[1] += t1 - t0
+        g[2] += fl
+print("zgemm by launch shape (flops per launch): launches, ms, TF/s — top 25 by time")
+for fl, v in sorted(by.items(), key=lambda kv: -kv[1][1])[:25]:
+    print(f"   {fl:12.4e} flop/launch {v[0]:6d} launches {v[1]:9.3f} ms {v[2] / (v[1] * 1e-3) / 1e12:6.2f} TF/s")
