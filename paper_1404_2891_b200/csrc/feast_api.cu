@@ -64,6 +64,7 @@ struct feast_ctx {
   const void *cache_A = nullptr, *cache_B = nullptr;
   int64_t nbo = 256;                  // outer block (trailing-update K); multiple of 64
   int64_t solve_nb = 256;             // outer block of the substitutions (FEAST_SOLVE_NB, multiple of 64)
+  bool btrsm = true;                  // fused block triangular solves (FEAST_BTRSM=0: the K = 64 launch chains)
   int64_t wp = 32;                    // cluster-panel width (divides 64)
   int64_t wide_panel_rows = 768;      // 64-wide cluster panels once n - k <= this (FEAST_WIDE_ROWS)
   cudaStream_t side = nullptr;        // high-priority stream for the lookahead panel
@@ -363,6 +364,45 @@ struct Lu {
 };
 const double2* inv_ptr(const Lu& v, int64_t kb, int which) { return v.Inv + (kb * 2 + which) * 4096; }
 
+// Y[K0:K0+R) <- op(T[K0:K0+R, K0:K0+R])^-1 Y[K0:K0+R) for N columns, T = L (which = 0, unit lower)
+// or U (which = 1, upper) of the factored block, op = conjugate transpose when conj (the sweep
+// runs forward for L and U^H, backward for U and L^H): the fused DMMA block solve (btrsm.cu) on
+// 256-row pieces, the pieces coupled by DMMA GEMM updates with K = 256.  Y's row r is Y[r] (ld,
+// batch stride sy).
+void block_solve(feast_ctx* h, double2* Cw, const double2* Inv, int nbat, int which, bool conj, int64_t K0, int64_t R,
+                 double2* Y, int64_t ldy, int64_t sy, int64_t N, cudaStream_t s) {
+  const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr);
+  const bool fwd = (which == 0) != conj;
+  auto piece = [&](int64_t j, int64_t r) {
+    feast::BtrsmArgs a{Cw + (K0 + j) + (K0 + j) * ld, ld, st, Inv + ((K0 + j) / 64 * 2 + which) * 4096, 2 * 4096,
+                       h->inv_stride, Y + K0 + j, ldy, sy, r, N, nbat};
+    feast::btrsm_launch(a, fwd, conj, s);
+  };
+  if (fwd) {
+    for (int64_t j = 0; j < R; j += 256) {
+      const int64_t r = std::min<int64_t>(256, R - j), rest = R - j - r;
+      piece(j, r);
+      if (rest > 0) {   // Y[K0+j+r : K0+R) -= op(T)[those rows, K0+j : K0+j+r) Y[K0+j : +r)
+        const double2* A = conj ? Cw + (K0 + j) + (K0 + j + r) * ld : Cw + (K0 + j + r) + (K0 + j) * ld;
+        ZgemmArgs p{rest, N, r, A, ld, st, Y + K0 + j, ldy, sy, Y + K0 + j + r, ldy, sy, make_double2(-1, 0),
+                    make_double2(1, 0), nbat};
+        feast::zgemm_launch(p, conj, feast::ZG_SUB, s);
+      }
+    }
+  } else {
+    for (int64_t j = ((R - 1) / 256) * 256; j >= 0; j -= 256) {
+      const int64_t r = std::min<int64_t>(256, R - j);
+      piece(j, r);
+      if (j > 0) {      // Y[K0 : K0+j) -= op(T)[K0 : K0+j, K0+j : +r) Y[K0+j : +r)
+        const double2* A = conj ? Cw + (K0 + j) + K0 * ld : Cw + K0 + (K0 + j) * ld;
+        ZgemmArgs p{j, N, r, A, ld, st, Y + K0 + j, ldy, sy, Y + K0, ldy, sy, make_double2(-1, 0), make_double2(1, 0),
+                    nbat};
+        feast::zgemm_launch(p, conj, feast::ZG_SUB, s);
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- GEMM helpers
 // C = alpha op(A) B + beta C (single), with split-K when the output tile grid is too small
 // to fill the GPU (the reduced matrices Q^H (A Q) are m0 x m0 with K = n).
@@ -515,6 +555,9 @@ void outer_update(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, int64_t c0,
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), K1 = K0 + Wo;
   double2* C = v.Cw;
   const int nbat = v.nbat;
+  if (h->btrsm) {   // U12 = L11^-1 A12: the fused block solve
+    block_solve(h, C, v.Inv, nbat, 0, false, K0, Wo, C + c0 * ld, ld, st, nc, s);
+  } else
   for (int64_t ki = K0; ki < K1; ki += 64) {
     const int wi = (int)std::min<int64_t>(64, K1 - ki);
     ZgemmArgs u{wi, nc, wi, inv_ptr(v, ki / 64, 0), 64, h->inv_stride, C + ki + c0 * ld, ld, st, C + ki + c0 * ld, ld,
@@ -639,6 +682,8 @@ void solve_right_fwd(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t 
   double2* C = v.Cw;
   for (int64_t K0 = 0; K0 < n; K0 += NB) {
     const int64_t K1 = std::min(n, K0 + NB);
+    if (h->btrsm) block_solve(h, C, v.Inv, v.nbat, 0, false, K0, K1 - K0, Y, ld, sy, m, v.sm);
+    else
     for (int64_t k = K0; k < K1; k += h->nb) {
       const int w = (int)std::min<int64_t>(h->nb, K1 - k);
       diag_apply(h, v, Y, sy, k, w, 0, false, m);
@@ -665,6 +710,8 @@ void solve_right_back(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t
   for (int64_t K0 = lastK0; K0 >= 0; K0 -= NB) {
     const int64_t K1 = std::min(n, K0 + NB);
     const int64_t last = K0 + ((K1 - 1 - K0) / h->nb) * h->nb;
+    if (h->btrsm) block_solve(h, C, v.Inv, v.nbat, 1, false, K0, K1 - K0, Y, ld, sy, m, v.sm);
+    else
     for (int64_t k = last; k >= K0; k -= h->nb) {
       const int w = (int)std::min<int64_t>(h->nb, K1 - k);
       diag_apply(h, v, Y, sy, k, w, 1, false, m);
@@ -688,6 +735,8 @@ void solve_left(feast_ctx* h, const Lu& v, double2* Y) {
   double2* C = v.Cw;
   for (int64_t K0 = 0; K0 < n; K0 += NB) {  // U^H: lower, non-unit
     const int64_t K1 = std::min(n, K0 + NB);
+    if (h->btrsm) block_solve(h, C, v.Inv, v.nbat, 1, true, K0, K1 - K0, Y, ld, sy, m, v.sm);
+    else
     for (int64_t k = K0; k < K1; k += h->nb) {
       const int w = (int)std::min<int64_t>(h->nb, K1 - k);
       diag_apply(h, v, Y, sy, k, w, 1, true, m);   // (U_kk^H)^-1 = (U_kk^-1)^H
@@ -708,6 +757,8 @@ void solve_left(feast_ctx* h, const Lu& v, double2* Y) {
   for (int64_t K0 = lastK0; K0 >= 0; K0 -= NB) {  // L^H: upper, unit
     const int64_t K1 = std::min(n, K0 + NB);
     const int64_t last = K0 + ((K1 - 1 - K0) / h->nb) * h->nb;
+    if (h->btrsm) block_solve(h, C, v.Inv, v.nbat, 0, true, K0, K1 - K0, Y, ld, sy, m, v.sm);
+    else
     for (int64_t k = last; k >= K0; k -= h->nb) {
       const int w = (int)std::min<int64_t>(h->nb, K1 - k);
       diag_apply(h, v, Y, sy, k, w, 0, true, m);   // (L_kk^H)^-1 = (L_kk^-1)^H
@@ -1212,6 +1263,7 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
     const int v = atoi(e);
     if (v >= 1 && v <= feast_ctx::GMAX) h->groups = v;
   }
+  if (const char* e = getenv("FEAST_BTRSM")) h->btrsm = e[0] != '0';
   if (const char* e = getenv("FEAST_SOLVE_NB")) {
     const long v = atol(e);
     if (v >= 64 && v % 64 == 0) h->solve_nb = v;

@@ -21,6 +21,25 @@ void zgemm_launch(const ZgemmArgs& p, bool conjA, int mode, cudaStream_t s);
 // tile-variant selection (tools/zgemm_lab): 0 = the launcher's heuristic
 void zgemm_launch_variant(const ZgemmArgs& p, bool conjA, int mode, int variant, cudaStream_t s);
 
+// ---------------------------------------------------------------- block triangular solve (DMMA)
+// Y <- op(T)^-1 Y for an R x R (R <= 256) triangular block T made of 64 x 64 blocks whose diagonal
+// blocks' inverses are precomputed (trtri): one CTA per 32-column tile of Y keeps the R x 32 tile
+// in shared memory and runs the whole block solve (diagonal-inverse products and the in-block
+// updates) on DMMA, streaming the 64 x 64 operand blocks from L2.
+//   fwd   : blocks in increasing order (op(T) lower: L, or U^H), else decreasing (U, or L^H)
+//   conj  : op = conjugate transpose (the block (rb, kb) of op(T) is T[kb, rb]^H)
+//   T0    : T's top-left element (column-major, ld ldt), batch stride sT
+//   Inv0  : the first diagonal block's inverse (64 x 64, ld 64), the next at + inv_step, batch sInv
+//   Y0    : Y's first row (ld ldy), N columns, batch stride sY; R rows (ragged last 64-block ok)
+struct BtrsmArgs {
+  const double2* T0; int64_t ldt, sT;
+  const double2* Inv0; int64_t inv_step, sInv;
+  double2* Y0; int64_t ldy, sY;
+  int64_t R, N;
+  int batch;
+};
+void btrsm_launch(const BtrsmArgs& p, bool fwd, bool conj, cudaStream_t s);
+
 // ---------------------------------------------------------------- LU pieces
 // Batched matrices: matrix b at base + b*stride (complex elements), column-major, ld.
 struct Batched {
@@ -41,9 +60,6 @@ PanelCfg panel_config(int64_t n);
 void panel_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info,
                   int batch, const PanelCfg& cfg, cudaStream_t s);
 
-// Apply the cnt (<= 1024) sequential swaps ipiv[k..k+cnt) to the columns [c0, c1).
-// use_perm: one composed permutation per CTA, gather + scatter per column (coalesced writes of
-// the rows k..k+cnt-1) instead of the per-column swap chain.
 // Row swaps ipiv[k..k+cnt) applied to columns [c0, c1) (variant: LASWP_COALESCED = slot-traced
 // gather/scatter with coalesced block rows (default), LASWP_CHAIN = one thread per column running
 // the swap chain, LASWP_PERM = permutation composed per CTA with a row table).

@@ -460,14 +460,17 @@ def test_register_panel_height_spectral(n):
     assert float(torch.linalg.norm(Q - Qs) / torch.linalg.norm(Qs)) <= TOL
 
 
-@pytest.mark.parametrize("nb", ["64", "128", "256"])
+@pytest.mark.parametrize("btrsm", ["1", "0"])
+@pytest.mark.parametrize("nb", ["64", "128", "256", "512"])
 @pytest.mark.parametrize("n,m0", [(1000, 24), (1345, 8)])
-def test_two_level_substitutions(monkeypatch, nb, n, m0):
+def test_two_level_substitutions(monkeypatch, btrsm, nb, n, m0):
     """Back substitution, left solves and (factor cache) forward substitution with outer blocks of
-    FEAST_SOLVE_NB rows (64 = the one-level sweep): right and left projectors from one LU, and the
-    cached-factor path, equal the oracle's on ragged sizes (n not a multiple of 64 or of the outer
-    block)."""
+    FEAST_SOLVE_NB rows (64 = the one-level sweep; 512 = two fused 256-row block solves coupled by
+    a GEMM), with the fused DMMA block solve (btrsm) or the one-level launch chain: right and left
+    projectors from one LU, and the cached-factor path, equal the oracle's on ragged sizes (n not a
+    multiple of 64 or of the outer block)."""
     monkeypatch.setenv("FEAST_SOLVE_NB", nb)
+    monkeypatch.setenv("FEAST_BTRSM", btrsm)
     P = synth.make_pencil("C4", n=n, m0=m0)
     z, w = _oracle_nodes(P)
     V = synth.random_block(n, m0, 17)
@@ -512,3 +515,19 @@ def test_async_mode_pipelines_and_defers_status():
     with pytest.raises(FeastError) as e:
         g.sync()
     assert e.value.code == fb.E_SINGULAR
+
+
+@pytest.mark.parametrize("nbo", ["256", "512", "1024"])
+@pytest.mark.parametrize("btrsm", ["1", "0"])
+def test_outer_block_sizes(monkeypatch, nbo, btrsm):
+    """LU outer blocks of FEAST_NBO columns (U12 = L11^-1 A12 by the fused block solve in 256-row
+    pieces, or the one-level chain), ragged n, right and left projectors vs the oracle."""
+    monkeypatch.setenv("FEAST_NBO", nbo)
+    monkeypatch.setenv("FEAST_BTRSM", btrsm)
+    P = synth.make_pencil("C2", n=1100, m0=10)
+    z, w = _oracle_nodes(P)
+    V = synth.random_block(P.n, P.m0, 31)
+    f = _handle(P, fb.BI)
+    Q, QL = f.project_bi(dev(P.A), dev(P.B), dev(P.X0), dev(V))
+    assert rel(host(Q), oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
+    assert rel(host(QL), oracle.project(P.A, P.B, V, z, w, left=True)) <= TOL
