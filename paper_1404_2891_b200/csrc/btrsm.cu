@@ -4,18 +4,20 @@
 // inverses were formed by trtri (SURVEY §8(a) a3 "TRSM blocks", a4 substitutions).  The one-level
 // sequence this replaces is, per 64-row block kb, an in-place product Y_kb <- Inv_kb Y_kb and an
 // update GEMM Y_rest -= T[rest, kb] Y_kb (K = 64): seven dependent launches per 256-row block whose
-// CTAs spend most of their time filling and draining a 4-stage pipeline (5-20 TF/s measured).
-// Here ONE CTA per 32-column tile of Y keeps the R x 32 tile in shared memory for the whole block
-// solve and streams the <= 10 operand blocks (diagonal inverses and off-diagonal T blocks, 64 x 64
-// each, from L2) through one continuous cp.async ring, so the pipeline fills once per tile.
+// CTAs spend most of their time filling and draining a 4-stage pipeline.  Here ONE CTA per
+// 32-column tile of Y runs the whole block solve: the R x 32 tile lives in REGISTERS (each warp
+// owns a 16 x 16 piece of every 64-row block, in the DMMA accumulator layout), the <= 10 operand
+// blocks (diagonal inverses and off-diagonal T blocks, 64 x 64 each, from L2) stream through one
+// continuous cp.async ring, and shared memory holds only that ring and the solved 64-row block
+// in the B-operand layout (86 KB: two CTAs per SM, so one CTA's loads overlap the other's DMMA).
+//
+// The 64-row blocks are indexed by their position s in solve order (forward: block s; backward:
+// block nb - 1 - s), so every register array index is a compile-time constant; block s updates
+// the blocks s' > s in both directions.
 //
 // Arithmetic: the planar-complex DMMA product of zgemm_dmma.cu (four mma.m8n8k4.f64 per complex
 // 8x8x4 block, separate re / im accumulators, signs folded into the operands); op = conjugate
 // transpose reads the stored block T[kb, rb] "as rows" and negates its imaginary part.
-//
-// Shared memory (TN = 32 columns): Ys row-major R x 33 (the C-operand pattern of a DMMA fragment,
-// lanes (g, 2t+i), is bank-conflict free with ld = 33), Xs = the solved 64-row block in the
-// B-operand layout [n][k] (ld 68), and the A ring [stage][k][m] (ld 66): 135 + 35 + 51 KB.
 #include <cstdlib>
 
 #include "common.cuh"
@@ -28,13 +30,10 @@ namespace {
 constexpr int BT_TN = 32;          // columns of Y per CTA
 constexpr int BT_THREADS = 256;    // 8 warps: 4 (rows of 16) x 2 (columns of 16) of a 64 x 32 block
 constexpr int BT_ST = 3;           // A-ring stages (16 k each)
-constexpr int BT_LDY = BT_TN + 1;  // Ys[row][col]
 constexpr int BT_LDX = 64 + 4;     // Xs[col][k]
 constexpr int BT_LDA = 64 + 2;     // As[k][m]
 constexpr int BT_A_STAGE = 16 * BT_LDA;
-constexpr size_t bt_smem(int R) {
-  return ((size_t)R * BT_LDY + (size_t)BT_TN * BT_LDX + (size_t)BT_ST * BT_A_STAGE) * sizeof(double2);
-}
+constexpr size_t BT_SMEM = ((size_t)BT_TN * BT_LDX + (size_t)BT_ST * BT_A_STAGE) * sizeof(double2);
 
 __device__ __forceinline__ void dmma_bt(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -42,13 +41,12 @@ __device__ __forceinline__ void dmma_bt(double& c0, double& c1, double a, double
                : "d"(a), "d"(b));
 }
 
-template <bool FWD, bool CONJ>
-__global__ void __launch_bounds__(BT_THREADS, 1) btrsm_kernel(BtrsmArgs p) {
+template <bool FWD, bool CONJ, int MINB>
+__global__ void __launch_bounds__(BT_THREADS, MINB) btrsm_kernel(BtrsmArgs p) {
   extern __shared__ __align__(128) double2 sm[];
-  const int R = (int)p.R;
-  double2* Ys = sm;                                 // [R][BT_LDY]
-  double2* Xs = Ys + (size_t)R * BT_LDY;            // [BT_TN][BT_LDX]
+  double2* Xs = sm;                                 // [BT_TN][BT_LDX]: the solved block (B operand)
   double2* As = Xs + BT_TN * BT_LDX;                // [BT_ST][16][BT_LDA]
+  const int R = (int)p.R;
   const int z = blockIdx.y;
   const double2* __restrict__ T = p.T0 + (int64_t)z * p.sT;
   const double2* __restrict__ Inv = p.Inv0 + (int64_t)z * p.sInv;
@@ -59,31 +57,27 @@ __global__ void __launch_bounds__(BT_THREADS, 1) btrsm_kernel(BtrsmArgs p) {
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 1) * 16, wn = (warp & 1) * 16;
   const int nb = (R + 63) / 64;
+  auto blk_of = [&](int s) { return FWD ? s : nb - 1 - s; };       // solve position -> block index
   auto rows_of = [&](int b) { return min(64, R - 64 * b); };
 
-  // ---- the operand-block schedule: for each kb (in solve order) the diagonal inverse, then the
-  // off-diagonal blocks of the rows still to be updated.  Product q = (rb, kb); rb == kb: inverse.
-  // (at most 10 products for 4 blocks; generated on the fly from q)
-  auto product = [&](int q, int& rb, int& kb) {
-    // enumerate kb in solve order, each followed by its update rows
+  // product q enumerates (position s, target position s2): s2 == s is the diagonal inverse of s,
+  // s2 > s an update of block s2 by the solved block s
+  auto product = [&](int q, int& s, int& s2) {
     int idx = q;
-    for (int s = 0; s < nb; ++s) {
-      const int k = FWD ? s : nb - 1 - s;
-      const int nup = FWD ? nb - 1 - k : k;          // rows after (fwd) / before (bwd) k
-      if (idx == 0) { rb = k; kb = k; return; }
-      if (idx <= nup) { rb = FWD ? k + idx : k - idx; kb = k; return; }
+    for (int a = 0; a < nb; ++a) {
+      const int nup = nb - 1 - a;
+      if (idx <= nup) { s = a; s2 = a + idx; return; }
       idx -= nup + 1;
     }
-    rb = kb = -1;
+    s = s2 = 0;
   };
-  const int nprod = nb + nb * (nb - 1) / 2;
-  const int nchunk = 4 * nprod;
+  const int nchunk = 4 * (nb + nb * (nb - 1) / 2);
 
-  // ---- A-operand chunk loader: chunk c = product c / 4, k-slice (c % 4) * 16 .. +16 of the 64 x 64
-  // block op(T)[rb, kb] (diagonal: op(Inv_kb)), rows m < rows_of(rb), k < rows_of(kb) (else 0)
+  // A-operand chunk c: k-slice (c % 4) * 16 .. +16 of op(T)[blk(s2), blk(s)] (diagonal: op(Inv))
   auto load_chunk = [&](int c, int stage) {
-    int rb, kb;
-    product(c >> 2, rb, kb);
+    int s, s2;
+    product(c >> 2, s, s2);
+    const int rb = blk_of(s2), kb = blk_of(s);
     const int k0 = (c & 3) * 16;
     const int M = rows_of(rb), K = rows_of(kb);
     const double2* blk;
@@ -103,113 +97,136 @@ __global__ void __launch_bounds__(BT_THREADS, 1) btrsm_kernel(BtrsmArgs p) {
                    "l"(pred ? src : blk), "r"(pred ? 16 : 0));
     }
   };
-
-  // ---- Y tile -> Ys (rows >= R and columns >= tn zero)
-  for (int e = tid; e < R * BT_TN; e += BT_THREADS) {
-    const int r = e % R, c = e / R;   // consecutive threads: consecutive rows of a column (coalesced)
-    Ys[r * BT_LDY + c] = c < tn ? Y[r + (n0 + c) * p.ldy] : make_double2(0.0, 0.0);
-  }
 #pragma unroll
-  for (int s = 0; s < BT_ST - 1; ++s) {
-    if (s < nchunk) load_chunk(s, s);
+  for (int c = 0; c < BT_ST - 1; ++c) {
+    if (c < nchunk) load_chunk(c, c);
     asm volatile("cp.async.commit_group;\n" ::);
   }
 
+  // ---- the Y tile in registers: y[s][mi][nj][i] = Y[64 blk(s) + wm + 8 mi + g][wn + 8 nj + 2 t + i]
+  double2 y[4][2][2][2];
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int r = 64 * blk_of(s) + wm + 8 * mi + g, col = wn + 8 * nj + 2 * t + i;
+          y[s][mi][nj][i] = (s < nb && r < R && col < tn) ? Y[r + (n0 + col) * p.ldy] : make_double2(0.0, 0.0);
+        }
+
   double cre[2][2][2], cim[2][2][2];
-  auto zero_acc = [&]() {
+  constexpr double SI = CONJ ? -1.0 : 1.0;
+  int c = 0;   // next chunk to consume
+  // acc = op(A product) * Xs over the product's 4 chunks (the ring advances across products)
+  auto run_product = [&]() {
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
       for (int nj = 0; nj < 2; ++nj) cre[mi][nj][0] = cre[mi][nj][1] = cim[mi][nj][0] = cim[mi][nj][1] = 0.0;
-  };
-  zero_acc();
-  constexpr double SI = CONJ ? -1.0 : 1.0;
-
-  for (int c = 0; c < nchunk; ++c) {
-    int rb, kb;
-    product(c >> 2, rb, kb);
-    if ((c & 3) == 0 && rb == kb) {
-      // start of block kb: its rows are final (every earlier update wrote them) -> B layout
-      __syncthreads();
-      for (int e = tid; e < 64 * BT_TN; e += BT_THREADS) {
-        const int k = e & 63, col = e >> 6;
-        Xs[col * BT_LDX + k] = 64 * kb + k < R ? Ys[(64 * kb + k) * BT_LDY + col] : make_double2(0.0, 0.0);
-      }
-    }
-    // chunk c resident; then (every warp past chunk c - 1) refill its stage with chunk c + ST - 1
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(BT_ST - 2));
-    __syncthreads();
-    if (c + BT_ST - 1 < nchunk) load_chunk(c + BT_ST - 1, (c + BT_ST - 1) % BT_ST);
-    asm volatile("cp.async.commit_group;\n" ::);
-    const double2* as = As + (c % BT_ST) * BT_A_STAGE;
-    const int kk0 = (c & 3) * 16;
+#pragma unroll 1
+    for (int kc = 0; kc < 4; ++kc, ++c) {
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(BT_ST - 2));
+      __syncthreads();   // chunk c resident everywhere; every warp is past chunk c - 1
+      if (c + BT_ST - 1 < nchunk) load_chunk(c + BT_ST - 1, (c + BT_ST - 1) % BT_ST);
+      asm volatile("cp.async.commit_group;\n" ::);
+      const double2* as = As + (c % BT_ST) * BT_A_STAGE;
 #pragma unroll
-    for (int k4 = 0; k4 < 4; ++k4) {
-      double2 af[2], bf[2];
+      for (int k4 = 0; k4 < 4; ++k4) {
+        double2 af[2], bf[2];
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi) af[mi] = as[(4 * k4 + t) * BT_LDA + wm + 8 * mi + g];
+        for (int mi = 0; mi < 2; ++mi) af[mi] = as[(4 * k4 + t) * BT_LDA + wm + 8 * mi + g];
 #pragma unroll
-      for (int nj = 0; nj < 2; ++nj) bf[nj] = Xs[(wn + 8 * nj + g) * BT_LDX + kk0 + 4 * k4 + t];
+        for (int nj = 0; nj < 2; ++nj) bf[nj] = Xs[(wn + 8 * nj + g) * BT_LDX + 16 * kc + 4 * k4 + t];
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi) {
-        const double ar = af[mi].x, ai = SI * af[mi].y;
+        for (int mi = 0; mi < 2; ++mi) {
+          const double ar = af[mi].x, ai = SI * af[mi].y;
 #pragma unroll
-        for (int nj = 0; nj < 2; ++nj) {
-          dmma_bt(cre[mi][nj][0], cre[mi][nj][1], ar, bf[nj].x);
-          dmma_bt(cim[mi][nj][0], cim[mi][nj][1], ar, bf[nj].y);
-          dmma_bt(cre[mi][nj][0], cre[mi][nj][1], -ai, bf[nj].y);
-          dmma_bt(cim[mi][nj][0], cim[mi][nj][1], ai, bf[nj].x);
+          for (int nj = 0; nj < 2; ++nj) {
+            dmma_bt(cre[mi][nj][0], cre[mi][nj][1], ar, bf[nj].x);
+            dmma_bt(cim[mi][nj][0], cim[mi][nj][1], ar, bf[nj].y);
+            dmma_bt(cre[mi][nj][0], cre[mi][nj][1], -ai, bf[nj].y);
+            dmma_bt(cim[mi][nj][0], cim[mi][nj][1], ai, bf[nj].x);
+          }
         }
       }
     }
-    if ((c & 3) == 3) {
-      // end of product (rb, kb)
-      if (rb == kb) {
-        __syncthreads();   // every warp is done reading Xs (the right-hand side) for this block
+  };
+  // write one block's registers into Xs, the B operand
+  auto to_xs = [&](const double2 (&v)[2][2][2]) {
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
+    for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-          for (int nj = 0; nj < 2; ++nj)
+      for (int nj = 0; nj < 2; ++nj)
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              const int r = wm + 8 * mi + g, col = wn + 8 * nj + 2 * t + i;
-              const double2 v = make_double2(cre[mi][nj][i], cim[mi][nj][i]);
-              Xs[col * BT_LDX + r] = v;                       // solved block: operand of the updates
-              if (64 * kb + r < R) Ys[(64 * kb + r) * BT_LDY + col] = v;
-            }
-        __syncthreads();
-      } else {
+        for (int i = 0; i < 2; ++i) Xs[(wn + 8 * nj + 2 * t + i) * BT_LDX + wm + 8 * mi + g] = v[mi][nj][i];
+  };
+
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
+  for (int s = 0; s < 4; ++s) {
+    if (s >= nb) break;
+    // ---- diagonal block: X_s = op(Inv) Y_s
+    __syncthreads();                  // every warp is done reading Xs (the previous solved block)
+    to_xs(y[s]);
+    run_product();                    // (its first barrier publishes Xs)
+    __syncthreads();                  // every warp is done reading Xs as the right-hand side
 #pragma unroll
-          for (int nj = 0; nj < 2; ++nj)
+    for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              const int r = 64 * rb + wm + 8 * mi + g, col = wn + 8 * nj + 2 * t + i;
-              if (r < R) {
-                double2& y = Ys[r * BT_LDY + col];
-                y = make_double2(y.x - cre[mi][nj][i], y.y - cim[mi][nj][i]);
-              }
-            }
-      }
-      zero_acc();
+      for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) y[s][mi][nj][i] = make_double2(cre[mi][nj][i], cim[mi][nj][i]);
+    to_xs(y[s]);                      // the solved block: operand of the updates below
+    // ---- updates of the blocks still to be solved: Y_s2 -= op(T)[s2, s] X_s
+#pragma unroll
+    for (int s2 = s + 1; s2 < 4; ++s2) {
+      if (s2 >= nb) break;
+      run_product();
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            double2& v = y[s2][mi][nj][i];
+            v = make_double2(v.x - cre[mi][nj][i], v.y - cim[mi][nj][i]);
+          }
     }
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
-  __syncthreads();
-  for (int e = tid; e < R * BT_TN; e += BT_THREADS) {
-    const int r = e % R, col = e / R;
-    if (col < tn) Y[r + (n0 + col) * p.ldy] = Ys[r * BT_LDY + col];
-  }
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int r = 64 * blk_of(s) + wm + 8 * mi + g, col = wn + 8 * nj + 2 * t + i;
+          if (s < nb && r < R && col < tn) Y[r + (n0 + col) * p.ldy] = y[s][mi][nj][i];
+        }
 }
 
-template <bool FWD, bool CONJ>
+template <bool FWD, bool CONJ, int MINB>
 void launch_bt(const BtrsmArgs& p, cudaStream_t s) {
   static std::atomic<uint64_t> configured{0};
   if (first_use_on_device(configured))
-    cudaFuncSetAttribute(btrsm_kernel<FWD, CONJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bt_smem(256));
+    cudaFuncSetAttribute(btrsm_kernel<FWD, CONJ, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BT_SMEM);
   dim3 grid((unsigned)((p.N + BT_TN - 1) / BT_TN), (unsigned)p.batch);
-  btrsm_kernel<FWD, CONJ><<<grid, BT_THREADS, bt_smem((int)p.R), s>>>(p);
+  btrsm_kernel<FWD, CONJ, MINB><<<grid, BT_THREADS, BT_SMEM, s>>>(p);
+}
+
+// FEAST_BTRSM_MINB: 2 (default) = two CTAs per SM (registers capped at 128: ~1 KB of spills at the
+// product boundaries), 1 = one CTA per SM without spills
+int bt_minb() {
+  static const int v = [] { const char* e = getenv("FEAST_BTRSM_MINB"); return (e && e[0] == '1') ? 1 : 2; }();
+  return v;
+}
+template <bool FWD, bool CONJ>
+void launch_bt2(const BtrsmArgs& p, cudaStream_t s) {
+  if (bt_minb() == 1) launch_bt<FWD, CONJ, 1>(p, s); else launch_bt<FWD, CONJ, 2>(p, s);
 }
 
 }  // namespace
@@ -219,8 +236,8 @@ void btrsm_launch(const BtrsmArgs& p, bool fwd, bool conj, cudaStream_t s) {
   // algorithmic flops: a triangular solve of R rows against N columns, 4 R (R + 1) N (complex)
   ProfScope ps_(K_ZGEMM, 4.0 * (double)p.R * (double)(p.R + 1) * (double)p.N * p.batch,
                 16.0 * ((double)p.R * p.R / 2 + 2.0 * p.R * p.N) * p.batch, s);
-  if (fwd) { if (conj) launch_bt<true, true>(p, s); else launch_bt<true, false>(p, s); }
-  else { if (conj) launch_bt<false, true>(p, s); else launch_bt<false, false>(p, s); }
+  if (fwd) { if (conj) launch_bt2<true, true>(p, s); else launch_bt2<true, false>(p, s); }
+  else { if (conj) launch_bt2<false, true>(p, s); else launch_bt2<false, false>(p, s); }
   count_launch();
 }
 
