@@ -64,7 +64,11 @@ struct feast_ctx {
   const void *cache_A = nullptr, *cache_B = nullptr;
   int64_t nbo = 256;                  // outer block (trailing-update K); multiple of 64
   int64_t solve_nb = 256;             // outer block of the substitutions (FEAST_SOLVE_NB, multiple of 64)
-  bool btrsm = true;                  // fused block triangular solves (FEAST_BTRSM=0: the K = 64 launch chains)
+  // fused DMMA block triangular solves (btrsm.cu) instead of the 64-row launch chains (FEAST_BTRSM=1).
+  // Correct (tests) but not faster on B200: C2 17.26 vs 16.43 ms, C4 13.020 vs 13.022 s per step —
+  // its parallelism is N/32 x batch CTAs that each run the whole <= 256-row solve, which delays a
+  // node group's chain (C2) and under-fills the GPU in the substitutions (N = m0)
+  bool btrsm = false;
   int64_t wp = 32;                    // cluster-panel width (divides 64)
   int64_t wide_panel_rows = 768;      // 64-wide cluster panels once n - k <= this (FEAST_WIDE_ROWS)
   cudaStream_t side = nullptr;        // high-priority stream for the lookahead panel
@@ -1266,7 +1270,7 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   // large n: wider outer blocks (trailing updates with K = 512) and substitution blocks (measured
   // C3 / C4 / C5: -0.4 / -0.7 / -1.6 % per step with 512 instead of 256)
   if (n >= 8192) { h->nbo = 512; h->solve_nb = 512; }
-  if (const char* e = getenv("FEAST_BTRSM")) h->btrsm = e[0] != '0';
+  if (const char* e = getenv("FEAST_BTRSM")) h->btrsm = e[0] == '1';
   if (const char* e = getenv("FEAST_SOLVE_NB")) {
     const long v = atol(e);
     if (v >= 64 && v % 64 == 0) h->solve_nb = v;
