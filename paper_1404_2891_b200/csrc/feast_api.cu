@@ -69,6 +69,7 @@ struct feast_ctx {
   // its parallelism is N/32 x batch CTAs that each run the whole <= 256-row solve, which delays a
   // node group's chain (C2) and under-fills the GPU in the substitutions (N = m0)
   bool btrsm = false;
+  bool subst_join = true;             // FEAST_SUBST_JOIN=0: substitutions per node group
   int64_t wp = 32;                    // cluster-panel width (divides 64)
   int64_t wide_panel_rows = 768;      // 64-wide cluster panels once n - k <= this (FEAST_WIDE_ROWS)
   cudaStream_t side = nullptr;        // high-priority stream for the lookahead panel
@@ -884,10 +885,11 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
       all = true;
       for (auto& r : runs) all = r.step() && all;
     }
-    // pass 3: per group, the substitutions and the join
-    for (int g = 0; g < G; ++g) {
-      const int b0 = g * nbat / G;
-      const Lu& v = vs[g];
+    // pass 3: the substitutions.  The groups' LU sequences were enqueued round-robin and finish
+    // together, so by default (FEAST_SUBST_JOIN) the groups are joined first and the
+    // substitutions run ONCE over the whole batch on the handle's stream: G times fewer, G times
+    // wider launches (the substitution GEMMs have only m0 columns per node).
+    auto subst = [&](const Lu& v, int b0) {
       if (!reuse) {
         if (doL || h->cache_on)
           feast::perm_launch(v.ipiv, h->perm + (int64_t)b0 * n, h->iperm + (int64_t)b0 * n, n, v.nbat, v.sm);
@@ -908,9 +910,22 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
         feast::broadcast_copy_launch(bat(Yg, ld, ld * mr), Rl, ldrl, n, m, v.nbat, pair, v.sm);
         solve_left(h, v, Yg);
       }
-      if (g) {
-        cudaEventRecord(h->gev_done[g], v.sm);
+    };
+    if (h->subst_join && G > 1) {
+      for (int g = 1; g < G; ++g) {
+        cudaEventRecord(h->gev_done[g], vs[g].sm);
         cudaStreamWaitEvent(h->stream, h->gev_done[g], 0);
+      }
+      Lu all = vs[0];
+      all.nbat = nbat;
+      subst(all, 0);
+    } else {
+      for (int g = 0; g < G; ++g) {
+        subst(vs[g], g * nbat / G);
+        if (g) {
+          cudaEventRecord(h->gev_done[g], vs[g].sm);
+          cudaStreamWaitEvent(h->stream, h->gev_done[g], 0);
+        }
       }
     }
     // a5: Q (+)= sum_j w_j Y_j, QL (+)= sum_j conj(w_j) Z_j over the batch in node order
@@ -1271,6 +1286,7 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   // C3 / C4 / C5: -0.4 / -0.7 / -1.6 % per step with 512 instead of 256)
   if (n >= 8192) { h->nbo = 512; h->solve_nb = 512; }
   if (const char* e = getenv("FEAST_BTRSM")) h->btrsm = e[0] == '1';
+  if (const char* e = getenv("FEAST_SUBST_JOIN")) h->subst_join = e[0] != '0';
   if (const char* e = getenv("FEAST_SOLVE_NB")) {
     const long v = atol(e);
     if (v >= 64 && v % 64 == 0) h->solve_nb = v;

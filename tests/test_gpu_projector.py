@@ -531,3 +531,22 @@ def test_outer_block_sizes(monkeypatch, nbo, btrsm):
     Q, QL = f.project_bi(dev(P.A), dev(P.B), dev(P.X0), dev(V))
     assert rel(host(Q), oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
     assert rel(host(QL), oracle.project(P.A, P.B, V, z, w, left=True)) <= TOL
+
+
+@pytest.mark.parametrize("join", ["1", "0"])
+def test_substitution_join_modes(monkeypatch, join):
+    """Substitutions once over the whole batch after joining the node groups (default) or per
+    group (FEAST_SUBST_JOIN=0): right + left projectors and the cached-factor path vs the oracle."""
+    monkeypatch.setenv("FEAST_SUBST_JOIN", join)
+    P = synth.make_pencil("C4", n=520, m0=12)
+    z, w = _oracle_nodes(P)
+    V = synth.random_block(P.n, P.m0, 41)
+    f = _handle(P, fb.BI)
+    Q, QL = f.project_bi(dev(P.A), None, dev(P.X0), dev(V))
+    assert rel(host(Q), oracle.project(P.A, None, P.X0, z, w)) <= TOL
+    assert rel(host(QL), oracle.project(P.A, None, V, z, w, left=True)) <= TOL
+    g = _handle(P)
+    g.factor_cache(True)
+    A, X = dev(P.A), dev(P.X0)
+    g.project(A, None, X)
+    assert rel(host(g.project(A, None, X)), oracle.project(P.A, None, P.X0, z, w)) <= TOL
