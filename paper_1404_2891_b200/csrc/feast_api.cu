@@ -69,7 +69,9 @@ struct feast_ctx {
   // its parallelism is N/32 x batch CTAs that each run the whole <= 256-row solve, which delays a
   // node group's chain (C2) and under-fills the GPU in the substitutions (N = m0)
   bool btrsm = false;
-  bool subst_join = true;             // FEAST_SUBST_JOIN=0: substitutions per node group
+  // FEAST_SUBST_JOIN=1: substitutions once over the whole batch after joining the node groups
+  // (measured no faster: C2 16.52 vs 16.39 ms, C4 12.972 vs 12.967 s)
+  bool subst_join = false;
   int64_t wp = 32;                    // cluster-panel width (divides 64)
   int64_t wide_panel_rows = 768;      // 64-wide cluster panels once n - k <= this (FEAST_WIDE_ROWS)
   cudaStream_t side = nullptr;        // high-priority stream for the lookahead panel
@@ -885,10 +887,9 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
       all = true;
       for (auto& r : runs) all = r.step() && all;
     }
-    // pass 3: the substitutions.  The groups' LU sequences were enqueued round-robin and finish
-    // together, so by default (FEAST_SUBST_JOIN) the groups are joined first and the
-    // substitutions run ONCE over the whole batch on the handle's stream: G times fewer, G times
-    // wider launches (the substitution GEMMs have only m0 columns per node).
+    // pass 3: the substitutions, per node group on its stream (FEAST_SUBST_JOIN=1: the groups,
+    // whose LU sequences were enqueued round-robin and finish together, are joined first and the
+    // substitutions run once over the whole batch: G times fewer, G times wider launches).
     auto subst = [&](const Lu& v, int b0) {
       if (!reuse) {
         if (doL || h->cache_on)
@@ -1286,7 +1287,7 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   // C3 / C4 / C5: -0.4 / -0.7 / -1.6 % per step with 512 instead of 256)
   if (n >= 8192) { h->nbo = 512; h->solve_nb = 512; }
   if (const char* e = getenv("FEAST_BTRSM")) h->btrsm = e[0] == '1';
-  if (const char* e = getenv("FEAST_SUBST_JOIN")) h->subst_join = e[0] != '0';
+  if (const char* e = getenv("FEAST_SUBST_JOIN")) h->subst_join = e[0] == '1';
   if (const char* e = getenv("FEAST_SOLVE_NB")) {
     const long v = atol(e);
     if (v >= 64 && v % 64 == 0) h->solve_nb = v;

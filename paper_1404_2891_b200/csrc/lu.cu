@@ -572,7 +572,11 @@ void laswp_launch(Batched C, int64_t n, int64_t k, int cnt, const int32_t* ipiv,
   ProfScope ps_(K_LASWP, 0.0, 0.0, s);
   const int64_t L = n - k;
   const size_t smem = (size_t)(L + 4 * cnt) * sizeof(int32_t);
-  if (variant == LASWP_COALESCED && cnt <= 256) {
+  // coalesced kernel for the panels' swap sequences (cnt <= 64); the outer blocks' long sequences
+  // (cnt = 256..1024) stay on the chain kernel: with dense pivoting (the C3 recipe) the slot
+  // tracing and the 2 cnt slots per column make the coalesced kernel 3x slower there, while on the
+  // panels' short sequences it is 4x faster (ncu, profiles/r02/swap_ncu.txt)
+  if (variant == LASWP_COALESCED && cnt <= 64) {
     unsigned long long* moved = ps_.bytes_counter();
     if (cnt <= 32) laswp_coalesced_launch<2>(C, n, k, cnt, ipiv, c0, c1, batch, s, moved);
     else if (cnt <= 64) laswp_coalesced_launch<4>(C, n, k, cnt, ipiv, c0, c1, batch, s, moved);
