@@ -371,22 +371,29 @@ void stats_init_launch(double* stats, int32_t* info, int batch, cudaStream_t s) 
 // Apply the cnt (<= 1024) sequential swaps ipiv[k..k+cnt) to the columns [c0, c1) of every
 // matrix.  Thread per column; each swap exchanges two 16-byte complex entries.
 __global__ void laswp_kernel(Batched C, int64_t n, int64_t k, int cnt, const int32_t* __restrict__ ipiv_all,
-                             int64_t c0, int64_t c1) {
+                             int64_t c0, int64_t c1, unsigned long long* moved_bytes) {
   __shared__ int32_t pv[1024];
   const int b = blockIdx.y;
   const int32_t* ipiv = ipiv_all + (int64_t)b * n;
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) pv[i] = ipiv[k + i];
   __syncthreads();
   const int64_t col = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= c1) return;
-  double2* Cc = C.p + (int64_t)b * C.stride + col * C.ld;
-  for (int i = 0; i < cnt; ++i) {
-    const int64_t r1 = k + i, r2 = pv[i];
-    if (r1 != r2) {
-      const double2 t = Cc[r1];
-      Cc[r1] = Cc[r2];
-      Cc[r2] = t;
+  unsigned nsw = 0;
+  if (col < c1) {
+    double2* Cc = C.p + (int64_t)b * C.stride + col * C.ld;
+    for (int i = 0; i < cnt; ++i) {
+      const int64_t r1 = k + i, r2 = pv[i];
+      if (r1 != r2) {
+        const double2 t = Cc[r1];
+        Cc[r1] = Cc[r2];
+        Cc[r2] = t;
+        ++nsw;
+      }
     }
+  }
+  if (moved_bytes) {   // profile mode: 64 B per swap (two elements read and written)
+    const unsigned w = __reduce_add_sync(0xffffffffu, nsw);
+    if ((threadIdx.x & 31) == 0 && w) atomicAdd(moved_bytes, 64ull * w);
   }
 }
 
@@ -593,7 +600,7 @@ void laswp_launch(Batched C, int64_t n, int64_t k, int cnt, const int32_t* ipiv,
   } else {   // very tall trailing matrices (row table > 96 KB) or > 256 swaps: the swap chain per column
     const int threads = 128;
     dim3 grid((unsigned)((c1 - c0 + threads - 1) / threads), (unsigned)batch);
-    laswp_kernel<<<grid, threads, 0, s>>>(C, n, k, cnt, ipiv, c0, c1);
+    laswp_kernel<<<grid, threads, 0, s>>>(C, n, k, cnt, ipiv, c0, c1, ps_.bytes_counter());
   }
   count_launch();
 }
