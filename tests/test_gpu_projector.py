@@ -550,3 +550,20 @@ def test_substitution_join_modes(monkeypatch, join):
     A, X = dev(P.A), dev(P.X0)
     g.project(A, None, X)
     assert rel(host(g.project(A, None, X)), oracle.project(P.A, None, P.X0, z, w)) <= TOL
+
+
+def test_workspace_query_after_bind_keeps_layout():
+    """feast_workspace_bytes after feast_bind_workspace only reports the size: the bound layout,
+    the batch and a captured graph stay valid (it used to null the workspace pointers)."""
+    import ctypes
+    P = synth.make_pencil("C2", n=300, m0=16)
+    z, w = _oracle_nodes(P)
+    f = _handle(P)
+    A, B, X = dev(P.A), dev(P.B), dev(P.X0)
+    Q = f.project(A, B, X)
+    f.project(A, B, X, Q)                     # second identical call: captured into a graph
+    nb = ctypes.c_size_t()
+    assert f.lib.feast_workspace_bytes(f.h, ctypes.byref(nb)) == 0
+    assert nb.value <= f.workspace.numel()
+    Q2 = host(f.project(A, B, X, Q))          # graph replay on the same layout
+    assert rel(Q2, oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
