@@ -90,7 +90,10 @@ struct feast_ctx {
   cudaEvent_t gev_first[GMAX] = {};
   cudaStream_t gx[GMAX] = {};         // per group: the stream of the diagonal-block inverses
   cudaEvent_t gev_t[GMAX] = {}, gev_x[GMAX] = {};
-  bool stagger = false;  // true: group g starts once group g-1 has factored its first block
+  // FEAST_STAGGER = d > 0: node group g starts once group g-1 has finished d outer steps, so the
+  // groups' latency-bound LU tails (and start-up panels) overlap other groups' GEMM-heavy blocks
+  // instead of coinciding (round-robin enqueue keeps them in lockstep otherwise)
+  int stagger = 0;
   int64_t ldc = 0;
   // workspace
   void* ws = nullptr;
@@ -604,6 +607,11 @@ struct LuRun {
   std::function<void(cudaStream_t)> rest;
   int phase = 0;          // 0: not started, 1: outer blocks, 2: done
   int64_t K0 = 0, Wo = 0;
+  int steps = 0;          // outer steps enqueued (ev_first is recorded after h->stagger of them)
+
+  void record_first(cudaStream_t sm) {
+    if (v.ev_first && ++steps == h->stagger) cudaEventRecord(v.ev_first, sm);   // releases the next group
+  }
 
   bool step() {
     const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), ntot = n + aug;
@@ -629,17 +637,22 @@ struct LuRun {
         if (rest) rest(sm);
         factor_block(h, v, 0, Wo, sm);
       }
-      if (v.ev_first) cudaEventRecord(v.ev_first, sm);   // releases the next (staggered) group
       if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, 0, (int)Wo, v.ipiv, Wo, ntot, nbat, sm, h->laswp_variant);
+      record_first(sm);
       phase = 1;
       K0 = 0;
       return false;
     }
-    if (K0 >= n) { phase = 2; return true; }
+    if (K0 >= n) {
+      phase = 2;
+      while (v.ev_first && steps < h->stagger) record_first(sm);
+      return true;
+    }
     const int64_t K1 = K0 + Wo;
     if (K1 >= n) {
       outer_update(h, v, K0, Wo, n, aug, sm);      // last block: augmented columns only
       phase = 2;
+      while (v.ev_first && steps < h->stagger) record_first(sm);   // short LU: release the next group
       return true;
     }
     const int64_t Wo1 = std::min<int64_t>(NBO, n - K1);
@@ -660,6 +673,7 @@ struct LuRun {
     if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, K1 + Wo1, ntot, nbat, sm, h->laswp_variant);
     K0 = K1;
     Wo = Wo1;
+    record_first(sm);
     return false;
   }
 };
@@ -857,8 +871,7 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
            h->info + (j + b0), b1 - b0, g ? h->gs[g] : h->stream, g ? h->gside[g] : h->side, g ? h->gev_a[g] : h->ev_a,
            g ? h->gev_p[g] : h->ev_p, (h->stagger && g + 1 < G) ? h->gev_first[g] : nullptr,
            h->prof_serial ? nullptr : h->gx[g], h->gev_t[g], h->gev_x[g]};
-      // (gev_first is recorded only by an LuRun: the factor-cache path waits on the fork)
-      if (g) cudaStreamWaitEvent(v.sm, (h->stagger && !reuse) ? h->gev_first[g - 1] : h->ev_fork, 0);
+      if (g) cudaStreamWaitEvent(v.sm, h->ev_fork, 0);
       vs.push_back(v);
       if (!reuse) {
         feast::stats_init_launch(v.stats, v.info, v.nbat, v.sm);
@@ -882,10 +895,23 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
         runs.push_back(LuRun{h, v, solve ? ncr : 0, rest});
       }
     }
-    // pass 2: the groups' LU sequences enqueued round-robin, one outer block each per turn
+    // pass 2: the groups' LU sequences enqueued round-robin, one outer block each per turn; with
+    // FEAST_STAGGER = d, group g joins once group g - 1 has enqueued d outer steps (its stream then
+    // waits on the event group g - 1 records after them)
+    std::vector<char> started(runs.size(), 0);
     for (bool all = runs.empty(); !all;) {
       all = true;
-      for (auto& r : runs) all = r.step() && all;
+      for (size_t g = 0; g < runs.size(); ++g) {
+        if (!started[g]) {
+          if (g > 0 && h->stagger > 0) {
+            const LuRun& prev = runs[g - 1];
+            if (prev.phase != 2 && prev.steps < h->stagger) { all = false; continue; }
+            cudaStreamWaitEvent(runs[g].v.sm, h->gev_first[g - 1], 0);
+          }
+          started[g] = 1;
+        }
+        all = runs[g].step() && all;
+      }
     }
     // pass 3: the substitutions, per node group on its stream (FEAST_SUBST_JOIN=1: the groups,
     // whose LU sequences were enqueued round-robin and finish together, are joined first and the
@@ -1277,7 +1303,7 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   if (const char* e = getenv("FEAST_GRAPH")) h->graphs = e[0] != '0';
   if (const char* e = getenv("FEAST_LASWP"))
     h->laswp_variant = e[0] == 'p' ? feast::LASWP_PERM : (e[0] == 'c' && e[1] == 'h') ? feast::LASWP_CHAIN : feast::LASWP_COALESCED;
-  if (const char* e = getenv("FEAST_STAGGER")) h->stagger = e[0] != '0';
+  if (const char* e = getenv("FEAST_STAGGER")) h->stagger = std::max(0, atoi(e));
   if (const char* e = getenv("FEAST_WIDE_ROWS")) h->wide_panel_rows = atol(e);
   if (const char* e = getenv("FEAST_GROUPS")) {
     const int v = atoi(e);

@@ -567,3 +567,21 @@ def test_workspace_query_after_bind_keeps_layout():
     assert nb.value <= f.workspace.numel()
     Q2 = host(f.project(A, B, X, Q))          # graph replay on the same layout
     assert rel(Q2, oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
+
+
+@pytest.mark.parametrize("stagger", ["1", "2", "5"])
+def test_staggered_node_groups(monkeypatch, stagger):
+    """FEAST_STAGGER = d: node group g starts after group g - 1 finished d outer LU steps (the
+    groups' latency-bound tails overlap other groups' GEMMs); d larger than the number of steps
+    degenerates to sequential groups.  Right + left projectors vs the oracle, and a repeated call
+    (graph capture / replay of the event dependencies)."""
+    monkeypatch.setenv("FEAST_STAGGER", stagger)
+    P = synth.make_pencil("C2", n=700, m0=12)
+    z, w = _oracle_nodes(P)
+    V = synth.random_block(P.n, P.m0, 43)
+    f = _handle(P, fb.BI)
+    A, B, X, Vd = dev(P.A), dev(P.B), dev(P.X0), dev(V)
+    Qo, QLo = oracle.project(P.A, P.B, P.X0, z, w), oracle.project(P.A, P.B, V, z, w, left=True)
+    for _ in range(3):
+        Q, QL = f.project_bi(A, B, X, Vd)
+        assert rel(host(Q), Qo) <= TOL and rel(host(QL), QLo) <= TOL
