@@ -77,7 +77,7 @@ struct feast_ctx {
   cudaStream_t side = nullptr;        // high-priority stream for the lookahead panel
   cudaEvent_t ev_a = nullptr, ev_p = nullptr;
   // concurrent node groups (group 0 uses stream / side / ev_a / ev_p)
-  static constexpr int GMAX = 4;
+  static constexpr int GMAX = 8;
   int laswp_variant = feast::LASWP_COALESCED;   // FEAST_LASWP=chain|perm: the round-1 swap kernels
   bool prof_serial = false;           // feast_profile(h, 2): one stream, no lookahead / groups
   int groups = 4;                     // concurrent node groups per batch (FEAST_GROUPS)
