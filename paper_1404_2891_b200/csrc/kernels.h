@@ -16,6 +16,7 @@ struct ZgemmArgs {
   double2 alpha, beta;
   int batch;                          // batch index z adds z*sA, z*sB, z*sC
   int inplace = 0;                    // 1: C aliases B (requires M <= 64: one CTA row of tiles)
+  int swz = 0;                        // > 1: tile rasterisation in groups of swz tile rows (set by the launcher)
 };
 void zgemm_launch(const ZgemmArgs& p, bool conjA, int mode, cudaStream_t s);
 // tile-variant selection (tools/zgemm_lab): 0 = the launcher's heuristic

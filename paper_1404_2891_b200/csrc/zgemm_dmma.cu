@@ -69,12 +69,24 @@ __global__ void __launch_bounds__(32 * WGM * WGN, MINB) zgemm_dmma_kernel(ZgemmA
   double2* As = smem;
   double2* Bs = smem + ST * A_STAGE;
 
-  const int64_t z = blockIdx.z;
+  const int64_t M = p.M, N = p.N, K = p.K;
+  // tile coordinates: plain (grid x = N tiles, y = M tiles, z = batch) or, for large grids
+  // (swz > 1), grid (swz, N tiles, M-tile groups x batch): the scheduler walks x fastest, so the
+  // CTAs resident at once cover swz tile rows x ~444/swz tile columns of C and re-read their A
+  // row tiles and B column tiles from L2 instead of DRAM
+  unsigned mt = blockIdx.y, nt = blockIdx.x, zb = blockIdx.z;
+  if (p.swz > 1) {
+    const unsigned groups = (unsigned)(((p.M + BM - 1) / BM + p.swz - 1) / p.swz);
+    zb = blockIdx.z / groups;
+    mt = (blockIdx.z - zb * groups) * (unsigned)p.swz + blockIdx.x;
+    nt = blockIdx.y;
+    if ((int64_t)mt * BM >= p.M) return;   // ragged last group (the whole CTA leaves before any barrier)
+  }
+  const int64_t m0 = (int64_t)mt * BM, n0 = (int64_t)nt * BN;
+  const int64_t z = zb;
   const double2* __restrict__ A = p.A + z * p.sA;
   const double2* __restrict__ B = p.B + z * p.sB;
   double2* __restrict__ C = p.C + z * p.sC;
-  const int64_t M = p.M, N = p.N, K = p.K;
-  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = (warp / WGN) * T::TM, wn = (warp % WGN) * T::TN;
   const int g = lane >> 2, t = lane & 3;
@@ -237,11 +249,19 @@ void launch3(const ZgemmArgs& p, cudaStream_t s) {
   if (first_use_on_device(configured)) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_BYTES);
   }
-  dim3 grid((unsigned)((p.N + BN - 1) / BN), (unsigned)((p.M + BM - 1) / BM), (unsigned)p.batch);
+  const int64_t tn = (p.N + BN - 1) / BN, tm = (p.M + BM - 1) / BM;
+  const dim3 grid = p.swz > 1 ? dim3((unsigned)p.swz, (unsigned)tn, (unsigned)((tm + p.swz - 1) / p.swz * p.batch))
+                              : dim3((unsigned)tn, (unsigned)tm, (unsigned)p.batch);
   kern<<<grid, T::THREADS, T::SMEM_BYTES, s>>>(p);
   count_launch();
 }
 
+
+// FEAST_SWZ: tile rows per rasterisation group of large non-in-place grids (default 16; 0/1 = off)
+int swz_rows() {
+  static const int v = [] { const char* e = getenv("FEAST_SWZ"); return e ? atoi(e) : 16; }();
+  return v;
+}
 
 template <bool CONJA, int MODE>
 void launch_t(const ZgemmArgs& p, cudaStream_t s) {
@@ -249,7 +269,14 @@ void launch_t(const ZgemmArgs& p, cudaStream_t s) {
   // leave most SMs idle (the substitutions' Y_k <- T_kk^-1 Y_k with N = m0)
   if (p.inplace && (p.N + 31) / 32 * p.batch < 148) launch3<64, 16, 4, 1, 4, 2, CONJA, MODE>(p, s);
   else if (p.inplace) launch3<64, 32, 2, 2, 4, 2, CONJA, MODE>(p, s);
-  else launch3<32, 32, 2, 2, 4, 3, CONJA, MODE>(p, s);
+  else {
+    // large grids: rasterise in groups of swz_rows() tile rows (a wave of 444 resident CTAs then
+    // spans ~16 x 28 tiles: each A row tile and B column tile is fetched from DRAM once per patch)
+    ZgemmArgs q = p;
+    const int g = swz_rows();
+    if (g > 1 && (p.M + 31) / 32 >= 2 * g && (p.N + 31) / 32 >= 2 * g) q.swz = g;
+    launch3<32, 32, 2, 2, 4, 3, CONJA, MODE>(q, s);
+  }
 }
 
 // tile variants kept for tools/zgemm_lab (0 = the production choice above)
