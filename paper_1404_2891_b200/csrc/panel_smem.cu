@@ -586,7 +586,12 @@ void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, do
   // held while the latency-bound panel runs next to the trailing-update GEMMs.
   // rows per CTA: <= 2 PT (two per thread) for panels up to 32 wide; <= PT for wider ones so the
   // w - 8 shared-memory columns stay within ~112 KB
-  const int rowcap = w > 32 ? PT : 2 * PT;
+  int rowcap = w > 32 ? PT : 2 * PT;
+  // FEAST_PANEL_ROWS: a larger row cap (fewer CTAs per panel cluster, e.g. 512 rows = 4 CTAs for a
+  // 2048-row panel) where the w - 8 shared-memory columns still fit
+  static const int rows_env = [] { const char* e = getenv("FEAST_PANEL_ROWS"); return e ? atoi(e) : 0; }();
+  if (rows_env > rowcap && rows_env <= 8 * PT && (size_t)rows_env * (w > 8 ? w - 8 : 0) * 16 <= 190 * 1024)
+    rowcap = rows_env;
   while (cs > 1 && (n - k + cs / 2 - 1) / (cs / 2) <= rowcap) cs /= 2;
   const int64_t Lc = (n - k + cs - 1) / cs;
   // register chunk: 8 columns (a 16-column chunk spills at 2 rows per thread)
