@@ -72,6 +72,7 @@ struct feast_ctx {
   // FEAST_SUBST_JOIN=1: substitutions once over the whole batch after joining the node groups
   // (measured no faster: C2 16.52 vs 16.39 ms, C4 12.972 vs 12.967 s)
   bool subst_join = false;
+  bool panel_swap = true;             // swaps fused into the shared-memory panel (FEAST_PANEL_SWAP=0: separate)
   int64_t wp = 32;                    // cluster-panel width (divides 64)
   int64_t wide_panel_rows = 768;      // 64-wide cluster panels once n - k <= this (FEAST_WIDE_ROWS)
   cudaStream_t side = nullptr;        // high-priority stream for the lookahead panel
@@ -483,12 +484,13 @@ int ablate() {
   return a;
 }
 
-void panel_at(feast_ctx* h, const Lu& v, int64_t k, int w, cudaStream_t s) {
+// sc0 < sc1: the shared-memory panel also applies its swaps to the columns [sc0, sc1)
+void panel_at(feast_ctx* h, const Lu& v, int64_t k, int w, cudaStream_t s, int64_t sc0 = 0, int64_t sc1 = 0) {
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr);
   if (ablate() & 1) { feast::ipiv_identity_launch(v.ipiv, n, k, w, v.nbat, s); return; }
   if (smem_panel_for(h, k))
     feast::panel_smem_launch(bat(v.Cw, ld, st), n, k, w, v.ipiv, v.stats, v.info, v.nbat, h->smem_cs_max, s,
-                             h->panel_one_row);
+                             h->panel_one_row, sc0, sc1);
   else
     feast::panel_launch(bat(v.Cw, ld, st), n, k, w, v.ipiv, v.stats, v.info, v.nbat, h->pcfg, s);
 }
@@ -518,9 +520,13 @@ void factor_block(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, cudaStream_
     // the in-block U12 (warp TRSM) and update (DMMA) between them
     for (int64_t kp = ki; kp < ki + wi; kp += wp) {
       const int wpp = (int)std::min<int64_t>(wp, ki + wi - kp);
-      panel_at(h, v, kp, wpp, s);
+      // shared-memory panels apply their swaps to the outer block's columns themselves
+      // (FEAST_PANEL_SWAP=0: a separate swap launch)
+      const bool fused = smem && h->panel_swap && !(ablate() & 5);
+      panel_at(h, v, kp, wpp, s, fused ? K0 : 0, fused ? K0 + Wo : 0);
       if (smem) {
-        if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, K0 + Wo, nbat, s, h->laswp_variant);
+        if (!fused && !(ablate() & 4))
+          feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, K0 + Wo, nbat, s, h->laswp_variant);
       } else {   // the register-chunk panel already swapped its own columns
         if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, K0, kp, nbat, s, h->laswp_variant);
         if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, kp, wpp, v.ipiv, kp + wpp, K0 + Wo, nbat, s, h->laswp_variant);
@@ -1314,6 +1320,7 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   if (n >= 8192) { h->nbo = 512; h->solve_nb = 512; }
   if (const char* e = getenv("FEAST_BTRSM")) h->btrsm = e[0] == '1';
   if (const char* e = getenv("FEAST_SUBST_JOIN")) h->subst_join = e[0] == '1';
+  if (const char* e = getenv("FEAST_PANEL_SWAP")) h->panel_swap = e[0] != '0';
   if (const char* e = getenv("FEAST_SOLVE_NB")) {
     const long v = atol(e);
     if (v >= 64 && v % 64 == 0) h->solve_nb = v;

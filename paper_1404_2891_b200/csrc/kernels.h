@@ -71,9 +71,10 @@ void laswp_launch(Batched C, int64_t n, int64_t k, int cnt, const int32_t* ipiv,
 int tall_variant();
 bool panel_smem_fits(int64_t n, int w, int cs);
 int panel_smem_max_clusters(int64_t L, int w, int cs);
+// sc0 < sc1: the panel's row swaps are also applied to the columns [sc0, sc1) (fused; no laswp launch)
 void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info, int batch,
                        int cs, cudaStream_t s,
-                       bool one_row = false);
+                       bool one_row = false, int64_t sc0 = 0, int64_t sc1 = 0);
 
 // Triangular solve op(T) X = X in place, T = nb x nb diagonal block (nb <= 64),
 // X = nb x ncols.  lower_op: op(T) lower (forward); unit: unit diagonal; conjT: op = ^H.

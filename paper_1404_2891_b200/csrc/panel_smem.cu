@@ -118,7 +118,7 @@ __device__ unsigned long long g_ctrace[2][16];
 
 template <int S, int WC, int NT, bool CLU>   // CLU: cluster of > 1 CTAs (else the single-CTA path)
 __global__ void __launch_bounds__(NT, 1)
-panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__ ipiv_all,
+panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int64_t sc0, int64_t sc1, int32_t* __restrict__ ipiv_all,
                   double* __restrict__ stats_all, int32_t* __restrict__ info_all) {
   cg::cluster_group cluster = cg::this_cluster();
   const int CS = (int)cluster.num_blocks();
@@ -148,6 +148,7 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
   __shared__ double2 wrow[2][NT / 32][WC + 1];
   __shared__ __align__(8) unsigned long long mbar[4];   // slots[0], slots[1], U12s, load
   __shared__ int pos2row[WMAX], cur[WMAX];
+  __shared__ int32_t lpiv[WMAX];                 // this panel's LAPACK ipiv (absolute rows)
 
   PTRACE(0);
 #ifdef FEAST_PANEL_TRACE
@@ -476,32 +477,55 @@ panel_smem_kernel(Batched Cb, int64_t n, int64_t k, int w, int32_t* __restrict__
   if (ctr)
     for (int i = 0; i < 16; ++i) g_ctrace[threadIdx.x == 0 ? 0 : 1][i] = (unsigned long long)ct_[i];
 #endif
-  // ---- LAPACK ipiv from the pivot sequence (rows / positions relative to k)
-  if (crank == 0 && tid == 0) {
+  // ---- LAPACK ipiv from the pivot sequence (rows / positions relative to k): every CTA derives
+  // it (the pivot sequence pvt is identical in all of them); CTA 0 publishes it
+  if (tid == 0) {
     for (int i = 0; i < w; ++i) { pos2row[i] = i; cur[i] = i; }
     int32_t* ipiv = ipiv_all + (int64_t)b * n + k;
     for (int col = 0; col < w; ++col) {
       const int p = pvt[col];
       const int lp = p < w ? cur[p] : p;
       const int rc = pos2row[col];
-      ipiv[col] = (int32_t)(k + lp);
+      lpiv[col] = (int32_t)(k + lp);
+      if (crank == 0) ipiv[col] = (int32_t)(k + lp);
       if (lp < w) pos2row[lp] = rc;
       if (rc < w) cur[rc] = lp;
       pos2row[col] = p;
       if (p < w) cur[p] = col;
     }
-    stats_all[2 * b] = fmin(stats_all[2 * b], sqrt(pmin));
-    stats_all[2 * b + 1] = fmax(stats_all[2 * b + 1], sqrt(pmax));
-    if (info && !info_all[b]) info_all[b] = info;
+    if (crank == 0) {
+      stats_all[2 * b] = fmin(stats_all[2 * b], sqrt(pmin));
+      stats_all[2 * b + 1] = fmax(stats_all[2 * b + 1], sqrt(pmax));
+      if (info && !info_all[b]) info_all[b] = info;
+    }
   }
   PTRACE(3);
-  // No trailing cluster barrier: every remote write into this CTA's shared memory was a
-  // st.async that this CTA waited for (the last column's slots), so it may exit.
+  // ---- fused row swaps (sc0 < sc1): the panel's w sequential swaps applied to the columns
+  // [sc0, sc1) of the outer block (the panel's own columns included: rows never moved inside the
+  // kernel), one column per thread of the cluster — replaces a separate swap launch on the
+  // panel chain.  The cluster barrier (release / acquire) makes every CTA's panel stores visible.
+  if (sc1 > sc0) {
+    if (CLU) cluster.sync(); else __syncthreads();
+    double2* Cm = Cb.p + (int64_t)b * Cb.stride;
+    for (int64_t col = sc0 + (int64_t)crank * NT + tid; col < sc1; col += (int64_t)CS * NT) {
+      double2* Cc = Cm + col * ld;
+      for (int i = 0; i < w; ++i) {
+        const int64_t r1 = k + i, r2 = lpiv[i];
+        if (r1 != r2) {
+          const double2 t0 = Cc[r1];
+          Cc[r1] = Cc[r2];
+          Cc[r2] = t0;
+        }
+      }
+    }
+  }
+  // No further cluster barrier: every remote write into this CTA's shared memory was a st.async
+  // that this CTA waited for (the last column's slots), so it may exit.
 }
 
 template <int S, int WC, int NT>
-void launch_s(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info, int batch, int cs,
-              cudaStream_t s) {
+void launch_s(Batched C, int64_t n, int64_t k, int w, int64_t sc0, int64_t sc1, int32_t* ipiv, double* stats,
+              int32_t* info, int batch, int cs, cudaStream_t s) {
   const int64_t L = n - k;
   const int Lc = (int)((L + cs - 1) / cs);
   const size_t smem = (size_t)Lc * (w > WC ? w - WC : 0) * sizeof(double2);
@@ -523,8 +547,8 @@ void launch_s(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* sta
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cs > 1) cudaLaunchKernelEx(&cfg, panel_smem_kernel<S, WC, NT, true>, C, n, k, w, ipiv, stats, info);
-  else cudaLaunchKernelEx(&cfg, panel_smem_kernel<S, WC, NT, false>, C, n, k, w, ipiv, stats, info);
+  if (cs > 1) cudaLaunchKernelEx(&cfg, panel_smem_kernel<S, WC, NT, true>, C, n, k, w, sc0, sc1, ipiv, stats, info);
+  else cudaLaunchKernelEx(&cfg, panel_smem_kernel<S, WC, NT, false>, C, n, k, w, sc0, sc1, ipiv, stats, info);
   count_launch();
 }
 
@@ -578,7 +602,7 @@ bool panel_smem_fits(int64_t n, int w, int cs) {
 
 void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, double* stats, int32_t* info, int batch,
                        int cs, cudaStream_t s,
-                       bool one_row) {
+                       bool one_row, int64_t sc0, int64_t sc1) {
   const double L_ = (double)(n - k);
   ProfScope ps_(K_PANEL, (double)batch * (4.0 * L_ * w * w - 4.0 * w * (double)w * w / 3.0), 0.0, s);
   // Shrink the cluster as the panel gets shorter (L = n - k): the smallest cluster that keeps
@@ -599,14 +623,14 @@ void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, do
   // per column and in the chunk-end update, but the CTA takes most of the register file, so no
   // trailing-update GEMM CTA shares its SM): chosen by the caller when few nodes are factored
   // and the panel chain, not GEMM throughput, bounds the step
-  if (Lc <= PT) launch_s<1, 8, PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);
-  else if (Lc <= 2 * PT && one_row) launch_s<1, 8, 2 * PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);
-  else if (Lc <= 2 * PT) launch_s<2, 8, PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);
-  else if (Lc <= 4 * PT) launch_s<2, 8, 2 * PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);   // 512 rows: 256 x 2
+  if (Lc <= PT) launch_s<1, 8, PT>(C, n, k, w, sc0, sc1, ipiv, stats, info, batch, cs, s);
+  else if (Lc <= 2 * PT && one_row) launch_s<1, 8, 2 * PT>(C, n, k, w, sc0, sc1, ipiv, stats, info, batch, cs, s);
+  else if (Lc <= 2 * PT) launch_s<2, 8, PT>(C, n, k, w, sc0, sc1, ipiv, stats, info, batch, cs, s);
+  else if (Lc <= 4 * PT) launch_s<2, 8, 2 * PT>(C, n, k, w, sc0, sc1, ipiv, stats, info, batch, cs, s);   // 512 rows: 256 x 2
   // 513..1024 rows per CTA (tall panels of n = 16384, w <= 16 so the w - 8 shared columns fit):
   // 256 threads x 4 rows (registers capped at 255) or 512 threads x 2 rows (capped at 128)
-  else if (tall_variant() == 2) launch_s<2, 8, 4 * PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);
-  else launch_s<4, 8, 2 * PT>(C, n, k, w, ipiv, stats, info, batch, cs, s);
+  else if (tall_variant() == 2) launch_s<2, 8, 4 * PT>(C, n, k, w, sc0, sc1, ipiv, stats, info, batch, cs, s);
+  else launch_s<4, 8, 2 * PT>(C, n, k, w, sc0, sc1, ipiv, stats, info, batch, cs, s);
 }
 
 }  // namespace feast

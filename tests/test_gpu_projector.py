@@ -374,18 +374,21 @@ def test_row_sharded_rhs_partials():
 @pytest.mark.parametrize("key,n,m0", [("C2", 300, 20), ("C3", 700, 24), ("C3", 1300, 9)])
 def test_row_swap_variants_bit_identical(monkeypatch, key, n, m0):
     """Row swaps are pure data movement: the default coalesced kernel (slot-traced gather/scatter),
-    the per-column swap chain (FEAST_LASWP=chain) and the per-CTA permutation kernel
-    (FEAST_LASWP=perm) must give BIT-identical projectors, equal to the oracle's.  The C3 recipe
+    the per-column swap chain (FEAST_LASWP=chain), the per-CTA permutation kernel
+    (FEAST_LASWP=perm) and the panels' swaps done by a separate launch instead of inside the
+    panel kernel (FEAST_PANEL_SWAP=0) must give BIT-identical projectors, equal to the oracle's.  The C3 recipe
     (random symmetric H + iD) pivots off the diagonal in most columns, so every swap path moves
     rows; n = 1300 has ragged panels and several cluster sizes."""
     P = synth.make_pencil(key, n=n, m0=m0)
     z, w = _oracle_nodes(P)
     out = {}
-    for v in ("coalesced", "chain", "perm"):
-        monkeypatch.setenv("FEAST_LASWP", v)
+    for v in ("coalesced", "chain", "perm", "unfused"):
+        monkeypatch.setenv("FEAST_LASWP", v if v != "unfused" else "coalesced")
+        monkeypatch.setenv("FEAST_PANEL_SWAP", "0" if v == "unfused" else "1")
         f = _handle(P)
         out[v] = host(f.project(dev(P.A), dev(P.B), dev(P.X0)))
-    assert np.array_equal(out["coalesced"], out["chain"]) and np.array_equal(out["coalesced"], out["perm"])
+    for v in ("chain", "perm", "unfused"):
+        assert np.array_equal(out["coalesced"], out[v]), v
     assert rel(out["coalesced"], oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
 
 
