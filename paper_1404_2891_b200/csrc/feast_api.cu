@@ -91,6 +91,9 @@ struct feast_ctx {
   cudaEvent_t gev_first[GMAX] = {};
   cudaStream_t gx[GMAX] = {};         // per group: the stream of the diagonal-block inverses
   cudaEvent_t gev_t[GMAX] = {}, gev_x[GMAX] = {};
+  cudaStream_t gl[GMAX] = {};         // per group: the stream of the L-column swaps (FEAST_LSWAP_SIDE)
+  cudaEvent_t gev_l[GMAX] = {}, gev_lj[GMAX] = {};
+  bool lswap_side = true;
   // FEAST_STAGGER = d > 0: node group g starts once group g-1 has finished d outer steps, so the
   // groups' latency-bound LU tails (and start-up panels) overlap other groups' GEMM-heavy blocks
   // instead of coinciding (round-robin enqueue keeps them in lockstep otherwise)
@@ -372,6 +375,8 @@ struct Lu {
   cudaEvent_t ev_first;  // recorded after the first block is factored (nullptr: none)
   cudaStream_t sx;       // diagonal-block inverses off the panel chain (nullptr: on the chain)
   cudaEvent_t ev_t, ev_x;
+  cudaStream_t sl = nullptr;   // the outer blocks' swaps of the L columns, off the chain (nullptr: on it)
+  cudaEvent_t ev_l = nullptr, ev_lj = nullptr;
 };
 const double2* inv_ptr(const Lu& v, int64_t kb, int which) { return v.Inv + (kb * 2 + which) * 4096; }
 
@@ -618,6 +623,14 @@ struct LuRun {
   void record_first(cudaStream_t sm) {
     if (v.ev_first && ++steps == h->stagger) cudaEventRecord(v.ev_first, sm);   // releases the next group
   }
+  void finish(cudaStream_t sm) {
+    phase = 2;
+    while (v.ev_first && steps < h->stagger) record_first(sm);   // short LU: release the next group
+    if (v.sl) {                                                  // the L-column swaps are done
+      cudaEventRecord(v.ev_lj, v.sl);
+      cudaStreamWaitEvent(sm, v.ev_lj, 0);
+    }
+  }
 
   bool step() {
     const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), ntot = n + aug;
@@ -650,15 +663,13 @@ struct LuRun {
       return false;
     }
     if (K0 >= n) {
-      phase = 2;
-      while (v.ev_first && steps < h->stagger) record_first(sm);
+      finish(sm);
       return true;
     }
     const int64_t K1 = K0 + Wo;
     if (K1 >= n) {
       outer_update(h, v, K0, Wo, n, aug, sm);      // last block: augmented columns only
-      phase = 2;
-      while (v.ev_first && steps < h->stagger) record_first(sm);   // short LU: release the next group
+      finish(sm);
       return true;
     }
     const int64_t Wo1 = std::min<int64_t>(NBO, n - K1);
@@ -674,9 +685,18 @@ struct LuRun {
       outer_update(h, v, K0, Wo, K1 + Wo1, ntot - K1 - Wo1, sm);
       factor_block(h, v, K1, Wo1, sm);
     }
-    // block K1's swaps on every column outside it
-    if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, 0, K1, nbat, sm, h->laswp_variant);
-    if (!(ablate() & 4)) feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, K1 + Wo1, ntot, nbat, sm, h->laswp_variant);
+    // block K1's swaps on every column outside it: the L columns [0, K1) are read only by the
+    // substitutions, so their swaps run on a side stream (in order, joined when the LU ends)
+    if (!(ablate() & 4)) {
+      cudaStream_t sl = sm;
+      if (v.sl) {
+        cudaEventRecord(v.ev_l, sm);
+        cudaStreamWaitEvent(v.sl, v.ev_l, 0);
+        sl = v.sl;
+      }
+      feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, 0, K1, nbat, sl, h->laswp_variant);
+      feast::laswp_launch(bat(C, ld, st), n, K1, (int)Wo1, v.ipiv, K1 + Wo1, ntot, nbat, sm, h->laswp_variant);
+    }
     K0 = K1;
     Wo = Wo1;
     record_first(sm);
@@ -876,7 +896,8 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
       Lu v{h->Cw + b0 * st, h->Inv + b0 * h->inv_stride, h->ipiv + (int64_t)b0 * n, h->stats + 2 * (j + b0),
            h->info + (j + b0), b1 - b0, g ? h->gs[g] : h->stream, g ? h->gside[g] : h->side, g ? h->gev_a[g] : h->ev_a,
            g ? h->gev_p[g] : h->ev_p, (h->stagger && g + 1 < G) ? h->gev_first[g] : nullptr,
-           h->prof_serial ? nullptr : h->gx[g], h->gev_t[g], h->gev_x[g]};
+           h->prof_serial ? nullptr : h->gx[g], h->gev_t[g], h->gev_x[g],
+           (h->prof_serial || !h->lswap_side) ? nullptr : h->gl[g], h->gev_l[g], h->gev_lj[g]};
       if (g) cudaStreamWaitEvent(v.sm, h->ev_fork, 0);
       vs.push_back(v);
       if (!reuse) {
@@ -1321,6 +1342,7 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   if (const char* e = getenv("FEAST_BTRSM")) h->btrsm = e[0] == '1';
   if (const char* e = getenv("FEAST_SUBST_JOIN")) h->subst_join = e[0] == '1';
   if (const char* e = getenv("FEAST_PANEL_SWAP")) h->panel_swap = e[0] != '0';
+  if (const char* e = getenv("FEAST_LSWAP_SIDE")) h->lswap_side = e[0] != '0';
   if (const char* e = getenv("FEAST_SOLVE_NB")) {
     const long v = atol(e);
     if (v >= 64 && v % 64 == 0) h->solve_nb = v;
@@ -1351,6 +1373,10 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
              cudaEventCreateWithFlags(&h->gev_a[g], cudaEventDisableTiming) == cudaSuccess &&
              cudaEventCreateWithFlags(&h->gev_p[g], cudaEventDisableTiming) == cudaSuccess &&
              cudaEventCreateWithFlags(&h->gev_done[g], cudaEventDisableTiming) == cudaSuccess;
+      for (int g = 0; g < feast_ctx::GMAX && ok; ++g)
+        ok = cudaStreamCreateWithPriority(&h->gl[g], cudaStreamNonBlocking, lo) == cudaSuccess &&
+             cudaEventCreateWithFlags(&h->gev_l[g], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&h->gev_lj[g], cudaEventDisableTiming) == cudaSuccess;
       for (int g = 0; g < feast_ctx::GMAX && ok; ++g)
         ok = cudaEventCreateWithFlags(&h->gev_first[g], cudaEventDisableTiming) == cudaSuccess &&
              cudaStreamCreateWithFlags(&h->gx[g], cudaStreamNonBlocking) == cudaSuccess &&
@@ -2027,6 +2053,9 @@ void feast_destroy(feast_handle h) {
   if (h->ev_rhs) cudaEventDestroy(h->ev_rhs);
   for (int g = 0; g < feast_ctx::GMAX; ++g) {
     if (h->gev_first[g]) cudaEventDestroy(h->gev_first[g]);
+    if (h->gl[g]) cudaStreamDestroy(h->gl[g]);
+    if (h->gev_l[g]) cudaEventDestroy(h->gev_l[g]);
+    if (h->gev_lj[g]) cudaEventDestroy(h->gev_lj[g]);
     if (h->gx[g]) cudaStreamDestroy(h->gx[g]);
     if (h->gev_t[g]) cudaEventDestroy(h->gev_t[g]);
     if (h->gev_x[g]) cudaEventDestroy(h->gev_x[g]);

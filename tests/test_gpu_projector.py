@@ -375,19 +375,22 @@ def test_row_sharded_rhs_partials():
 def test_row_swap_variants_bit_identical(monkeypatch, key, n, m0):
     """Row swaps are pure data movement: the default coalesced kernel (slot-traced gather/scatter),
     the per-column swap chain (FEAST_LASWP=chain), the per-CTA permutation kernel
-    (FEAST_LASWP=perm) and the panels' swaps done by a separate launch instead of inside the
-    panel kernel (FEAST_PANEL_SWAP=0) must give BIT-identical projectors, equal to the oracle's.  The C3 recipe
+    (FEAST_LASWP=perm), the panels' swaps done by a separate launch instead of inside the panel
+    kernel (FEAST_PANEL_SWAP=0) and the L-column swaps on the main stream instead of the side
+    stream (FEAST_LSWAP_SIDE=0) must give BIT-identical projectors, equal to the oracle's.  The C3 recipe
     (random symmetric H + iD) pivots off the diagonal in most columns, so every swap path moves
     rows; n = 1300 has ragged panels and several cluster sizes."""
     P = synth.make_pencil(key, n=n, m0=m0)
     z, w = _oracle_nodes(P)
     out = {}
-    for v in ("coalesced", "chain", "perm", "unfused"):
-        monkeypatch.setenv("FEAST_LASWP", v if v != "unfused" else "coalesced")
+    for v in ("coalesced", "chain", "perm", "unfused", "lswap_main"):
+        monkeypatch.setenv("FEAST_LASWP", v if v in ("coalesced", "chain", "perm") else "coalesced")
         monkeypatch.setenv("FEAST_PANEL_SWAP", "0" if v == "unfused" else "1")
+        monkeypatch.setenv("FEAST_LSWAP_SIDE", "0" if v == "lswap_main" else "1")
         f = _handle(P)
         out[v] = host(f.project(dev(P.A), dev(P.B), dev(P.X0)))
-    for v in ("chain", "perm", "unfused"):
+        f.project(dev(P.A), dev(P.B), dev(P.X0))   # graph capture of the multi-stream sequence
+    for v in ("chain", "perm", "unfused", "lswap_main"):
         assert np.array_equal(out["coalesced"], out[v]), v
     assert rel(out["coalesced"], oracle.project(P.A, P.B, P.X0, z, w)) <= TOL
 
