@@ -376,6 +376,9 @@ def run_gpu(args):
                 "per_class_ms_per_step": {k: v["ms"] / prof_steps for k, v in prof.items()},
                 "per_class_launches_per_step": {k: v["launches"] / prof_steps for k, v in prof.items()},
                 "hbm_kernels_gbs": per_class_gbs,
+                "hbm_kernels_note": "laswp counts only the rows that actually move (device counter): the BASELINE "
+                                    "pencils pivot (almost) on the diagonal, so it moves ~nothing; the swap kernels' "
+                                    "bandwidth on a pivot-heavy pencil is in profiles/r02/swap_ncu.txt",
                 "hbm_peak_gbs": hbm, "hbm_peak_source": "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)"}
 
     # ---- end to end through the public API with pinned host buffers: every step copies the

@@ -1974,8 +1974,10 @@ int feast_profile(feast_handle h, int32_t enable) {
   h->prof_serial = enable == 2;
   p.recs.clear();
   p.used = 0;
+  if (p.on) p.ensure_counters();
   if (p.counters && p.counters_used) cudaMemset(p.counters, 0, p.counters_used * sizeof(unsigned long long));
   p.counters_used = 0;
+  CUDA_TRY(h, cudaDeviceSynchronize());
   return FEAST_OK;
 }
 

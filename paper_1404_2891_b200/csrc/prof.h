@@ -29,13 +29,15 @@ struct Prof {
   // actually move); allocated on first use while profiling, read back by feast_profile_summary
   unsigned long long* counters = nullptr;
   int64_t ncounters = 0, counters_used = 0;
+  // allocated by feast_profile (outside every event pair: cudaMalloc / cudaMemset synchronise)
+  void ensure_counters() {
+    if (counters) return;
+    ncounters = 1 << 20;
+    if (cudaMalloc(&counters, ncounters * sizeof(unsigned long long)) != cudaSuccess) { counters = nullptr; return; }
+    cudaMemset(counters, 0, ncounters * sizeof(unsigned long long));
+  }
   unsigned long long* counter() {
-    if (!counters) {
-      ncounters = 1 << 20;
-      if (cudaMalloc(&counters, ncounters * sizeof(unsigned long long)) != cudaSuccess) { counters = nullptr; return nullptr; }
-      cudaMemset(counters, 0, ncounters * sizeof(unsigned long long));
-    }
-    if (counters_used >= ncounters) return nullptr;
+    if (!counters || counters_used >= ncounters) return nullptr;
     return counters + counters_used++;
   }
   cudaEvent_t get() {
