@@ -107,3 +107,60 @@ def test_two_ranks_one_gpu_full_results(tmp_path):
             assert np.min(np.abs(inside - x)) <= 1e-10 * s1.r
         lams.append(np.sort_complex(got))
     assert len(lams[0]) == len(lams[1]) and np.max(np.abs(lams[0] - lams[1])) <= 1e-12
+
+
+def _nccl_worker(rank, port, outdir):
+    """ONE process, an NCCL process group of size 1 (NCCL cannot put two ranks on one GPU), and
+    two handles that each believe world = 2 (ranks 0 and 1): every node sum then goes through the
+    real NCCL all-reduce on the library's raw staging block and stream (identity for one rank), so
+    each handle returns its own ranks' partial sum, and the two partials add up to the full Q."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import torch.distributed as dist
+
+    import synth
+    from gpu_util import dev, host
+    from paper_1404_2891_b200 import Feast, feast as fb
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    res = {}
+    P4 = synth.make_pencil("C4", n=300, m0=24)   # B = I: no row-sharded a1 (identity sum would drop rows)
+    s4 = P4.spec
+    V0 = P4.X0 @ np.linalg.inv(P4.X0.conj().T @ P4.X0).conj().T
+    A, X, V = dev(P4.A), dev(P4.X0), dev(V0)
+    for r in range(2):
+        g = Feast(P4.n, P4.m0, s4.c, s4.r, s4.aspect, s4.n_e, s4.rule, fb.BI, True, rank=r, world=2, partial=True)
+        assert g.lib.feast_set_partial(g.h, 0) == 0          # full node sums, through NCCL:
+        g._ar = fb.ALLREDUCE_FN(fb.make_allreduce_callback(g.device))
+        assert g.lib.feast_set_allreduce(g.h, g._ar, None) == 0
+        for call in range(3):                      # eager, captured, replayed graph
+            Q, QL = g.project_bi(A, None, X, V)
+            res[f"Q{r}_{call}"], res[f"QL{r}_{call}"] = host(Q), host(QL)
+    np.savez(os.path.join(outdir, "nccl.npz"), **res)
+    dist.destroy_process_group()
+
+
+def test_nccl_allreduce_callback_partials(tmp_path):
+    """The node sum through the binding's callback on the NCCL backend (the multi-GPU bench's
+    collective): each world = 2 handle's result equals the oracle's sum over that rank's nodes
+    (R17: rank r owns [r q/2, (r+1) q/2)), unchanged across graph capture and replay; the two
+    partials add up to the oracle's Q / Q_L."""
+    import oracle
+    import synth
+    mp.spawn(_nccl_worker, args=(_free_port(), str(tmp_path)), nprocs=1, join=True)
+    d = np.load(tmp_path / "nccl.npz")
+    P4 = synth.make_pencil("C4", n=300, m0=24)
+    s4 = P4.spec
+    z, w = oracle.nodes(s4.c, s4.r, s4.aspect, s4.n_e, s4.rule)
+    V0 = P4.X0 @ np.linalg.inv(P4.X0.conj().T @ P4.X0).conj().T
+    q = len(z)
+    rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)
+    for r in range(2):
+        j0, j1 = r * q // 2, (r + 1) * q // 2
+        Qo = oracle.project(P4.A, None, P4.X0, z, w, j0, j1)
+        QLo = oracle.project(P4.A, None, V0, z, w, j0, j1, left=True)
+        for call in range(3):
+            assert rel(d[f"Q{r}_{call}"], Qo) <= TOL and rel(d[f"QL{r}_{call}"], QLo) <= TOL
+    Qfull = oracle.project(P4.A, None, P4.X0, z, w)
+    assert rel(d["Q0_2"] + d["Q1_2"], Qfull) <= TOL

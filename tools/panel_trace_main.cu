@@ -7,7 +7,7 @@
 #ifndef NO_TRACE_READ
 namespace feast { void panel_trace_read(unsigned long long* out); void panel_ctrace_read(unsigned long long* out); }
 #else
-namespace feast { inline void panel_trace_read(unsigned long long*) {} }
+namespace feast { inline void panel_trace_read(unsigned long long*) {} inline void panel_ctrace_read(unsigned long long*) {} }
 #endif
 int main(int argc, char** argv) {
   int W = argc > 1 ? atoi(argv[1]) : 64, CS = argc > 2 ? atoi(argv[2]) : 16;
