@@ -908,7 +908,8 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
         const int64_t w0 = std::min<int64_t>(first_block(h), n);
         const double2* zj = h->zd + j + b0;
         feast::shift_launch(bat(v.Cw, ld, st), A, lda, B, ldb, zj, n, v.nbat, v.sm, 0, w0);
-        auto rest = [&, zj, v](cudaStream_t sr) {
+        // (invoked later, from the round-robin pass 2: the block-scoped values are captured by copy)
+        auto rest = [&, zj, v, w0](cudaStream_t sr) {
           feast::shift_launch(bat(v.Cw, ld, st), A, lda, B, ldb, zj, n, v.nbat, sr, w0, n);
           if (rhs_wait) cudaStreamWaitEvent(sr, rhs_wait, 0);
           if (doR)

@@ -83,3 +83,18 @@ for c, st, t0, t1, fl in recs:
 print("zgemm by launch shape (flops per launch): launches, ms, TF/s — top 25 by time")
 for fl, v in sorted(by.items(), key=lambda kv: -kv[1][1])[:25]:
     print(f"   {fl:12.4e} flop/launch {v[0]:6d} launches {v[1]:9.3f} ms {v[2] / (v[1] * 1e-3) / 1e12:6.2f} TF/s")
+# per phase: launch shapes ranked by time lost against the big trailing updates' rate
+REF = 36.19   # TF/s of the C4 trailing updates (profiles/r02/phase_C4.txt)
+for name, sel in (("lu", recs[:last_panel + 1]), ("subst", recs[last_panel + 1:])):
+    byp = defaultdict(lambda: [0, 0.0, 0.0])
+    for c, st, t0, t1, fl in sel:
+        if c == "zgemm":
+            g = byp[round(fl, -3)]
+            g[0] += 1
+            g[1] += t1 - t0
+            g[2] += fl
+    loss = {k: v[1] - v[2] / (REF * 1e9) for k, v in byp.items()}
+    print(f"{name}: zgemm time lost vs {REF} TF/s: {sum(loss.values()):.2f} ms — top 20 shapes by loss")
+    for fl, v in sorted(byp.items(), key=lambda kv: -loss[kv[0]])[:20]:
+        print(f"   {fl:12.4e} flop/launch {v[0]:6d} launches {v[1]:9.3f} ms {v[2] / (v[1] * 1e-3) / 1e12:6.2f} TF/s"
+              f"  lost {loss[fl]:8.2f} ms")
