@@ -69,6 +69,11 @@ struct feast_ctx {
   // its parallelism is N/32 x batch CTAs that each run the whole <= 256-row solve, which delays a
   // node group's chain (C2) and under-fills the GPU in the substitutions (N = m0)
   bool btrsm = false;
+  // FEAST_SUBST_DOT=1 (default for n >= 8192): substitutions in dot form (left-looking): before its diagonal block is
+  // solved, an outer block takes ALL the solved rows' contribution in one GEMM with a long K
+  // (M = N-block rows, K = rows solved so far) instead of pushing its own contribution to every
+  // later block (right-looking: M = rows still to solve, K = the block)
+  bool subst_dot = false;
   // FEAST_SUBST_JOIN=1: substitutions once over the whole batch after joining the node groups
   // (measured no faster: C2 16.52 vs 16.39 ms, C4 12.972 vs 12.967 s)
   bool subst_join = false;
@@ -729,6 +734,11 @@ void solve_right_fwd(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t 
   double2* C = v.Cw;
   for (int64_t K0 = 0; K0 < n; K0 += NB) {
     const int64_t K1 = std::min(n, K0 + NB);
+    if (h->subst_dot && K0 > 0) {   // Y[K0:K1] -= L[K0:K1, 0:K0] Y[0:K0]
+      ZgemmArgs p{K1 - K0, m, K0, C + K0, ld, st, Y, ld, sy, Y + K0, ld, sy, make_double2(-1, 0), make_double2(1, 0),
+                  v.nbat};
+      feast::zgemm_launch(p, false, feast::ZG_SUB, v.sm);
+    }
     if (h->btrsm) block_solve(h, C, v.Inv, v.nbat, 0, false, K0, K1 - K0, Y, ld, sy, m, v.sm);
     else
     for (int64_t k = K0; k < K1; k += h->nb) {
@@ -741,7 +751,7 @@ void solve_right_fwd(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t 
         feast::zgemm_launch(p, false, feast::ZG_SUB, v.sm);
       }
     }
-    if (K1 < n) {       // Y[K1:] -= L[K1:, K0:K1] Y[K0:K1]
+    if (K1 < n && !h->subst_dot) {       // Y[K1:] -= L[K1:, K0:K1] Y[K0:K1]
       ZgemmArgs p{n - K1, m, K1 - K0, C + K1 + K0 * ld, ld, st, Y + K0, ld, sy, Y + K1, ld, sy,
                   make_double2(-1, 0), make_double2(1, 0), v.nbat};
       feast::zgemm_launch(p, false, feast::ZG_SUB, v.sm);
@@ -757,6 +767,11 @@ void solve_right_back(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t
   for (int64_t K0 = lastK0; K0 >= 0; K0 -= NB) {
     const int64_t K1 = std::min(n, K0 + NB);
     const int64_t last = K0 + ((K1 - 1 - K0) / h->nb) * h->nb;
+    if (h->subst_dot && K1 < n) {   // Y[K0:K1] -= U[K0:K1, K1:n] Y[K1:n]
+      ZgemmArgs p{K1 - K0, m, n - K1, C + K0 + K1 * ld, ld, st, Y + K1, ld, sy, Y + K0, ld, sy, make_double2(-1, 0),
+                  make_double2(1, 0), v.nbat};
+      feast::zgemm_launch(p, false, feast::ZG_SUB, v.sm);
+    }
     if (h->btrsm) block_solve(h, C, v.Inv, v.nbat, 1, false, K0, K1 - K0, Y, ld, sy, m, v.sm);
     else
     for (int64_t k = last; k >= K0; k -= h->nb) {
@@ -768,7 +783,7 @@ void solve_right_back(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t
         feast::zgemm_launch(p, false, feast::ZG_SUB, v.sm);
       }
     }
-    if (K0 > 0) {       // Y[0:K0] -= U[0:K0, K0:K1] Y[K0:K1]
+    if (K0 > 0 && !h->subst_dot) {       // Y[0:K0] -= U[0:K0, K0:K1] Y[K0:K1]
       ZgemmArgs p{K0, m, K1 - K0, C + K0 * ld, ld, st, Y + K0, ld, sy, Y, ld, sy, make_double2(-1, 0),
                   make_double2(1, 0), v.nbat};
       feast::zgemm_launch(p, false, feast::ZG_SUB, v.sm);
@@ -782,6 +797,11 @@ void solve_left(feast_ctx* h, const Lu& v, double2* Y) {
   double2* C = v.Cw;
   for (int64_t K0 = 0; K0 < n; K0 += NB) {  // U^H: lower, non-unit
     const int64_t K1 = std::min(n, K0 + NB);
+    if (h->subst_dot && K0 > 0) {   // Y[K0:K1] -= (U[0:K0, K0:K1])^H Y[0:K0]
+      ZgemmArgs p{K1 - K0, m, K0, C + K0 * ld, ld, st, Y, ld, sy, Y + K0, ld, sy, make_double2(-1, 0),
+                  make_double2(1, 0), v.nbat};
+      feast::zgemm_launch(p, true, feast::ZG_SUB, v.sm);
+    }
     if (h->btrsm) block_solve(h, C, v.Inv, v.nbat, 1, true, K0, K1 - K0, Y, ld, sy, m, v.sm);
     else
     for (int64_t k = K0; k < K1; k += h->nb) {
@@ -794,7 +814,7 @@ void solve_left(feast_ctx* h, const Lu& v, double2* Y) {
         feast::zgemm_launch(p, true, feast::ZG_SUB, v.sm);
       }
     }
-    if (K1 < n) {       // Y[K1:] -= (U[K0:K1, K1:])^H Y[K0:K1]
+    if (K1 < n && !h->subst_dot) {       // Y[K1:] -= (U[K0:K1, K1:])^H Y[K0:K1]
       ZgemmArgs p{n - K1, m, K1 - K0, C + K0 + K1 * ld, ld, st, Y + K0, ld, sy, Y + K1, ld, sy,
                   make_double2(-1, 0), make_double2(1, 0), v.nbat};
       feast::zgemm_launch(p, true, feast::ZG_SUB, v.sm);
@@ -804,6 +824,11 @@ void solve_left(feast_ctx* h, const Lu& v, double2* Y) {
   for (int64_t K0 = lastK0; K0 >= 0; K0 -= NB) {  // L^H: upper, unit
     const int64_t K1 = std::min(n, K0 + NB);
     const int64_t last = K0 + ((K1 - 1 - K0) / h->nb) * h->nb;
+    if (h->subst_dot && K1 < n) {   // Y[K0:K1] -= (L[K1:n, K0:K1])^H Y[K1:n]
+      ZgemmArgs p{K1 - K0, m, n - K1, C + K1 + K0 * ld, ld, st, Y + K1, ld, sy, Y + K0, ld, sy, make_double2(-1, 0),
+                  make_double2(1, 0), v.nbat};
+      feast::zgemm_launch(p, true, feast::ZG_SUB, v.sm);
+    }
     if (h->btrsm) block_solve(h, C, v.Inv, v.nbat, 0, true, K0, K1 - K0, Y, ld, sy, m, v.sm);
     else
     for (int64_t k = last; k >= K0; k -= h->nb) {
@@ -815,7 +840,7 @@ void solve_left(feast_ctx* h, const Lu& v, double2* Y) {
         feast::zgemm_launch(p, true, feast::ZG_SUB, v.sm);
       }
     }
-    if (K0 > 0) {       // Y[0:K0] -= (L[K0:K1, 0:K0])^H Y[K0:K1]
+    if (K0 > 0 && !h->subst_dot) {       // Y[0:K0] -= (L[K0:K1, 0:K0])^H Y[K0:K1]
       ZgemmArgs p{K0, m, K1 - K0, C + K0, ld, st, Y + K0, ld, sy, Y, ld, sy, make_double2(-1, 0),
                   make_double2(1, 0), v.nbat};
       feast::zgemm_launch(p, true, feast::ZG_SUB, v.sm);
@@ -1340,7 +1365,11 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   // large n: wider outer blocks (trailing updates with K = 512) and substitution blocks (measured
   // C3 / C4 / C5: -0.4 / -0.7 / -1.6 % per step with 512 instead of 256)
   if (n >= 8192) { h->nbo = 512; h->solve_nb = 512; }
+  // dot-form substitutions from n = 8192 (C4 12.898 -> 12.838 s, C3 1544.6 -> 1543.3 ms; C2 16.51 vs
+  // 16.57 ms right-looking: its short K = 256 blocks do not pay)
+  h->subst_dot = n >= 8192;
   if (const char* e = getenv("FEAST_BTRSM")) h->btrsm = e[0] == '1';
+  if (const char* e = getenv("FEAST_SUBST_DOT")) h->subst_dot = e[0] == '1';
   if (const char* e = getenv("FEAST_SUBST_JOIN")) h->subst_join = e[0] == '1';
   if (const char* e = getenv("FEAST_PANEL_SWAP")) h->panel_swap = e[0] != '0';
   if (const char* e = getenv("FEAST_LSWAP_SIDE")) h->lswap_side = e[0] != '0';

@@ -110,7 +110,7 @@ def empty_colmajor(rows: int, cols: int, device="cuda", dtype=torch.complex128) 
     return torch.empty((cols, rows), dtype=dtype, device=device).t()
 
 
-def _ptr_ld(t, rows, name, device=None):
+def _ptr_ld(t, rows, name, device=None, cols=None):
     if t is None:
         return None, 0
     if t.dtype != torch.complex128 or not t.is_cuda or t.dim() != 2:
@@ -119,6 +119,8 @@ def _ptr_ld(t, rows, name, device=None):
         raise FeastError(E_ARG, f"{name} is on {t.device}, the handle on {device}")
     if t.shape[0] != rows or (rows > 1 and t.stride(0) != 1):
         raise FeastError(E_ARG, f"{name} must be column-major with {rows} rows")
+    if cols is not None and t.shape[1] != cols:   # the library reads / writes exactly `cols` columns
+        raise FeastError(E_ARG, f"{name} must have {cols} columns (has {t.shape[1]})")
     ld = t.stride(1) if t.shape[1] > 1 else max(rows, 1)
     if ld < rows:
         raise FeastError(E_ARG, f"{name}: leading dimension {ld} < {rows} rows")
@@ -259,31 +261,31 @@ class Feast:
         """Q = sum_j w_j (z_j B - A)^-1 (B X), node-summed over the ranks by the library
         (partial=True: this rank's nodes only)."""
         Q = empty_colmajor(self.n, self.m0, self.device) if Q is None else Q
-        pa, lda = _ptr_ld(A, self.n, "A", self.device)
-        pb, ldb = _ptr_ld(B, self.n, "B", self.device)
-        px, ldx = _ptr_ld(X, self.n, "X", self.device)
-        pq, ldq = _ptr_ld(Q, self.n, "Q", self.device)
+        pa, lda = _ptr_ld(A, self.n, "A", self.device, self.n)
+        pb, ldb = _ptr_ld(B, self.n, "B", self.device, self.n)
+        px, ldx = _ptr_ld(X, self.n, "X", self.device, self.m0)
+        pq, ldq = _ptr_ld(Q, self.n, "Q", self.device, self.m0)
         self.status = self._check(self.lib.feast_project(self.h, pa, lda, pb, ldb, px, ldx, pq, ldq))
         return Q
 
     def project_left(self, A, B, V, QL=None):
         QL = empty_colmajor(self.n, self.m0, self.device) if QL is None else QL
-        pa, lda = _ptr_ld(A, self.n, "A", self.device)
-        pb, ldb = _ptr_ld(B, self.n, "B", self.device)
-        pv, ldv = _ptr_ld(V, self.n, "V", self.device)
-        pq, ldq = _ptr_ld(QL, self.n, "QL", self.device)
+        pa, lda = _ptr_ld(A, self.n, "A", self.device, self.n)
+        pb, ldb = _ptr_ld(B, self.n, "B", self.device, self.n)
+        pv, ldv = _ptr_ld(V, self.n, "V", self.device, self.m0)
+        pq, ldq = _ptr_ld(QL, self.n, "QL", self.device, self.m0)
         self.status = self._check(self.lib.feast_project_left(self.h, pa, lda, pb, ldb, pv, ldv, pq, ldq))
         return QL
 
     def project_bi(self, A, B, X, V, Q=None, QL=None):
         Q = empty_colmajor(self.n, self.m0, self.device) if Q is None else Q
         QL = empty_colmajor(self.n, self.m0, self.device) if QL is None else QL
-        pa, lda = _ptr_ld(A, self.n, "A", self.device)
-        pb, ldb = _ptr_ld(B, self.n, "B", self.device)
-        px, ldx = _ptr_ld(X, self.n, "X", self.device)
-        pv, ldv = _ptr_ld(V, self.n, "V", self.device)
-        pq, ldq = _ptr_ld(Q, self.n, "Q", self.device)
-        pl, ldl = _ptr_ld(QL, self.n, "QL", self.device)
+        pa, lda = _ptr_ld(A, self.n, "A", self.device, self.n)
+        pb, ldb = _ptr_ld(B, self.n, "B", self.device, self.n)
+        px, ldx = _ptr_ld(X, self.n, "X", self.device, self.m0)
+        pv, ldv = _ptr_ld(V, self.n, "V", self.device, self.m0)
+        pq, ldq = _ptr_ld(Q, self.n, "Q", self.device, self.m0)
+        pl, ldl = _ptr_ld(QL, self.n, "QL", self.device, self.m0)
         self.status = self._check(self.lib.feast_project_bi(self.h, pa, lda, pb, ldb, px, ldx, pv, ldv, pq, ldq,
                                                             pl, ldl))
         return Q, QL
@@ -291,12 +293,12 @@ class Feast:
     def reduce(self, A, B, Q, QL=None, Ahat=None, Bhat=None):
         Ahat = empty_colmajor(self.m0, self.m0, self.device) if Ahat is None else Ahat
         Bhat = empty_colmajor(self.m0, self.m0, self.device) if Bhat is None else Bhat
-        pa, lda = _ptr_ld(A, self.n, "A", self.device)
-        pb, ldb = _ptr_ld(B, self.n, "B", self.device)
-        pq, ldq = _ptr_ld(Q, self.n, "Q", self.device)
-        pl, ldl = _ptr_ld(QL, self.n, "QL", self.device)
-        p1, ld1 = _ptr_ld(Ahat, self.m0, "Ahat", self.device)
-        p2, ld2 = _ptr_ld(Bhat, self.m0, "Bhat", self.device)
+        pa, lda = _ptr_ld(A, self.n, "A", self.device, self.n)
+        pb, ldb = _ptr_ld(B, self.n, "B", self.device, self.n)
+        pq, ldq = _ptr_ld(Q, self.n, "Q", self.device, self.m0)
+        pl, ldl = _ptr_ld(QL, self.n, "QL", self.device, self.m0)
+        p1, ld1 = _ptr_ld(Ahat, self.m0, "Ahat", self.device, self.m0)
+        p2, ld2 = _ptr_ld(Bhat, self.m0, "Bhat", self.device, self.m0)
         self._check(self.lib.feast_reduce(self.h, pa, lda, pb, ldb, pq, ldq, pl, ldl, p1, ld1, p2, ld2))
         return Ahat, Bhat
 
@@ -306,10 +308,10 @@ class Feast:
         ritz = (ctypes.c_double * (2 * m))()
         res = (ctypes.c_double * m)()
         flags = (ctypes.c_int32 * m)()
-        pa, lda = _ptr_ld(A, self.n, "A", self.device)
-        pb, ldb = _ptr_ld(B, self.n, "B", self.device)
-        px, ldx = _ptr_ld(X, self.n, "X", self.device)
-        pv, ldv = _ptr_ld(V, self.n, "V", self.device)
+        pa, lda = _ptr_ld(A, self.n, "A", self.device, self.n)
+        pb, ldb = _ptr_ld(B, self.n, "B", self.device, self.n)
+        px, ldx = _ptr_ld(X, self.n, "X", self.device, self.m0)
+        pv, ldv = _ptr_ld(V, self.n, "V", self.device, self.m0)
         self.status = self._check(self.lib.feast_iterate(self.h, pa, lda, pb, ldb, px, ldx, pv, ldv, ritz, res,
                                                          flags))
         lam = [complex(ritz[2 * i], ritz[2 * i + 1]) for i in range(m)]
@@ -328,10 +330,10 @@ class Feast:
         """Eigenvalue-count estimate Re tr(U^H rho(B^-1 A) U) / m0 for a random block U (NEXT-3);
         returns (estimate, Q = rho(B^-1 A) U, node-summed over ranks)."""
         Q = empty_colmajor(self.n, self.m0, self.device) if Q is None else Q
-        pa, lda = _ptr_ld(A, self.n, "A", self.device)
-        pb, ldb = _ptr_ld(B, self.n, "B", self.device)
-        pu, ldu = _ptr_ld(U, self.n, "U", self.device)
-        pq, ldq = _ptr_ld(Q, self.n, "Q", self.device)
+        pa, lda = _ptr_ld(A, self.n, "A", self.device, self.n)
+        pb, ldb = _ptr_ld(B, self.n, "B", self.device, self.n)
+        pu, ldu = _ptr_ld(U, self.n, "U", self.device, self.m0)
+        pq, ldq = _ptr_ld(Q, self.n, "Q", self.device, self.m0)
         est = ctypes.c_double()
         self.status = self._check(self.lib.feast_estimate_count(self.h, pa, lda, pb, ldb, pu, ldu, pq, ldq,
                                                                 ctypes.byref(est)))
@@ -343,12 +345,12 @@ class Feast:
         import numpy as np
         Q = empty_colmajor(self.n, self.m0, self.device) if Q is None else Q
         QL = empty_colmajor(self.n, self.m0, self.device) if QL is None else QL
-        pa, lda = _ptr_ld(A, self.n, "A", self.device)
-        pb, ldb = _ptr_ld(B, self.n, "B", self.device)
-        pu, ldu = _ptr_ld(U, self.n, "U", self.device)
-        pv, ldv = _ptr_ld(V, self.n, "V", self.device)
-        pq, ldq = _ptr_ld(Q, self.n, "Q", self.device)
-        pl, ldl = _ptr_ld(QL, self.n, "QL", self.device)
+        pa, lda = _ptr_ld(A, self.n, "A", self.device, self.n)
+        pb, ldb = _ptr_ld(B, self.n, "B", self.device, self.n)
+        pu, ldu = _ptr_ld(U, self.n, "U", self.device, self.m0)
+        pv, ldv = _ptr_ld(V, self.n, "V", self.device, self.m0)
+        pq, ldq = _ptr_ld(Q, self.n, "Q", self.device, self.m0)
+        pl, ldl = _ptr_ld(QL, self.n, "QL", self.device, self.m0)
         mu = np.zeros(self.m0, dtype=np.complex128)
         cnt = ctypes.c_int32()
         self.status = self._check(self.lib.feast_estimate_count_bi(

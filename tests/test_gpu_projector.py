@@ -591,3 +591,44 @@ def test_staggered_node_groups(monkeypatch, stagger):
     for _ in range(3):
         Q, QL = f.project_bi(A, B, X, Vd)
         assert rel(host(Q), Qo) <= TOL and rel(host(QL), QLo) <= TOL
+
+
+def test_binding_rejects_wrong_column_counts():
+    """The library reads / writes exactly n columns of A, B and m0 of X, V, Q, QL: the binding
+    refuses a block with another column count instead of letting the kernels run past it."""
+    P = synth.make_pencil("C2", n=64, m0=8)
+    f = _handle(P)
+    A, B, X = dev(P.A), dev(P.B), dev(P.X0)
+    for bad in (lambda: f.project(A, B, X[:, :7]), lambda: f.project(A[:, :63], B, X),
+                lambda: f.project(A, B, X, dev(np.zeros((P.n, 9), complex)))):
+        with pytest.raises(FeastError) as e:
+            bad()
+        assert e.value.code == fb.E_ARG
+
+
+@pytest.mark.parametrize("key,n,m0", [("C2", 700, 24), ("C4", 600, 40)])
+def test_substitution_dot_form(monkeypatch, key, n, m0):
+    """FEAST_SUBST_DOT=1: every substitution (right back, left U^H / L^H, the cached forward
+    solve) in dot form — each 256-row outer block takes all solved rows' contribution in one
+    long-K GEMM before its diagonal block — gives the oracle's Q (and Q_L; with cached factors
+    too) on heights of several ragged outer blocks, and agrees with the right-looking form to
+    rounding."""
+    P = synth.make_pencil(key, n=n, m0=m0)
+    z, w = _oracle_nodes(P)
+    A, B, X = dev(P.A), dev(P.B), dev(P.X0)
+    out = {}
+    for v in ("0", "1"):
+        monkeypatch.setenv("FEAST_SUBST_DOT", v)
+        f = _handle(P, mode=fb.BI)
+        f.factor_cache(True)
+        Q, QL = f.project_bi(A, B, X, X)
+        X2 = dev(synth.random_block(P.n, P.m0, 7))
+        Qc = f.project(A, B, X2)              # cached factors: forward + back substitution only
+        out[v] = (host(Q), host(QL), host(Qc))
+    Qo = oracle.project(P.A, P.B, P.X0, z, w)
+    QLo = oracle.project(P.A, P.B, P.X0, z, w, left=True)
+    Qco = oracle.project(P.A, P.B, synth.random_block(P.n, P.m0, 7), z, w)
+    for (Q, QL, Qc) in out.values():
+        assert rel(Q, Qo) <= TOL and rel(QL, QLo) <= TOL and rel(Qc, Qco) <= TOL
+    for a, b in zip(out["0"], out["1"]):
+        assert rel(a, b) <= 1e-12
