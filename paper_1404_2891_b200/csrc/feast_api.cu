@@ -87,6 +87,11 @@ struct feast_ctx {
   int laswp_variant = feast::LASWP_COALESCED;   // FEAST_LASWP=chain|perm: the round-1 swap kernels
   bool prof_serial = false;           // feast_profile(h, 2): one stream, no lookahead / groups
   int groups = 4;                     // concurrent node groups per batch (FEAST_GROUPS)
+  bool groups_set = false;            // FEAST_GROUPS given (else 2 groups for throughput-bound batches)
+  // the current batch is throughput-bound (n >= 8192 with >= 16 nodes factored together: C3, C4):
+  // 2 node groups and a full-width first outer block (C4 12.838 -> 12.803 s, C3 1543.4 -> 1538.0 ms;
+  // C5's 4-node batches keep 4 groups and the 128-wide first block: 47.64 vs 47.65 s)
+  bool big = false;
   bool group_streams = false;
   cudaStream_t gs[GMAX] = {}, gside[GMAX] = {};
   cudaEvent_t gev_a[GMAX] = {}, gev_p[GMAX] = {}, gev_done[GMAX] = {};
@@ -604,10 +609,12 @@ void outer_update(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, int64_t c0,
 
 // Width of the first outer block: 128 columns (FEAST_NBO0), half the outer block, so the big
 // trailing GEMMs start sooner after the latency-bound first factorisation (C2 16.71 -> 16.61 ms;
-// 64: 16.74, 192: 16.67).
+// 64: 16.74, 192: 16.67); the full outer block for throughput-bound batches (h->big: the K = 128
+// first trailing update ran at 33.6 TF/s on C4).
 int64_t first_block(const feast_ctx* h) {
-  static const int64_t nbo0 = [] { const char* e = getenv("FEAST_NBO0"); return e ? atoll(e) : 128LL; }();
-  return (nbo0 > 0 && nbo0 % 64 == 0) ? std::min<int64_t>(nbo0, h->nbo) : h->nbo;
+  static const int64_t nbo0_env = [] { const char* e = getenv("FEAST_NBO0"); return e ? atoll(e) : 0LL; }();
+  const int64_t nbo0 = nbo0_env > 0 ? nbo0_env : (h->big ? h->nbo : 128);
+  return (nbo0 % 64 == 0) ? std::min<int64_t>(nbo0, h->nbo) : h->nbo;
 }
 
 // The batched LU as a resumable sequence: step() enqueues the first outer block (and, with
@@ -911,7 +918,9 @@ void project_enqueue(feast_ctx* h, const double2* A, int64_t lda, const double2*
     const int nbat = std::min(h->batch, owned - jb);
     const int j = h->j0 + jb;
     // split the batch into G concurrent groups (group 0 on the handle's stream)
-    const int G = (h->group_streams && !h->prof_serial) ? std::max(1, std::min(h->groups, nbat)) : 1;
+    h->big = h->n >= 8192 && nbat >= 16;
+    const int gmax = (h->big && !h->groups_set) ? std::min(2, h->groups) : h->groups;
+    const int G = (h->group_streams && !h->prof_serial) ? std::max(1, std::min(gmax, nbat)) : 1;
     if (G > 1) cudaEventRecord(h->ev_fork, h->stream);
     // pass 1: per group, the fork, the shift of the first outer block and the LU sequence object
     std::vector<Lu> vs;
@@ -1360,7 +1369,7 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   if (const char* e = getenv("FEAST_WIDE_ROWS")) h->wide_panel_rows = atol(e);
   if (const char* e = getenv("FEAST_GROUPS")) {
     const int v = atoi(e);
-    if (v >= 1 && v <= feast_ctx::GMAX) h->groups = v;
+    if (v >= 1 && v <= feast_ctx::GMAX) { h->groups = v; h->groups_set = true; }
   }
   // large n: wider outer blocks (trailing updates with K = 512) and substitution blocks (measured
   // C3 / C4 / C5: -0.4 / -0.7 / -1.6 % per step with 512 instead of 256)

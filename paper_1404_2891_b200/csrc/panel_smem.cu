@@ -588,10 +588,11 @@ int panel_smem_max_clusters(int64_t L, int w, int cs) {
 }
 
 // FEAST_TALL_VARIANT: 4 (default) = 256 threads x 4 rows, 2 = 512 threads x 2 rows for panels of
-// 513..1024 rows per CTA; 0 = keep those panels on the register-chunk kernel (lu.cu)
-int tall_variant() {
-  static const int v = [] { const char* e = getenv("FEAST_TALL_VARIANT"); return e ? atoi(e) : 4; }();
-  return v;
+// 513..1024 rows per CTA, 5 = 256 threads x 4 rows with a 4-column register chunk; 0 = keep those
+// panels on the register-chunk kernel (lu.cu)
+int tall_variant() {   // read per call (a getenv per panel launch): tests switch it per handle
+  const char* e = getenv("FEAST_TALL_VARIANT");
+  return e ? atoi(e) : 4;
 }
 
 bool panel_smem_fits(int64_t n, int w, int cs) {
@@ -630,6 +631,9 @@ void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, do
   // 513..1024 rows per CTA (tall panels of n = 16384, w <= 16 so the w - 8 shared columns fit):
   // 256 threads x 4 rows (registers capped at 255) or 512 threads x 2 rows (capped at 128)
   else if (tall_variant() == 2) launch_s<2, 8, 4 * PT>(C, n, k, w, sc0, sc1, ipiv, stats, info, batch, cs, s);
+  // 5: 256 threads x 4 rows with a 4-column register chunk (254 registers, no spill; the w - 4
+  // shared-memory columns take 192 KB at 1024 rows x 16 columns)
+  else if (tall_variant() == 5) launch_s<4, 4, 2 * PT>(C, n, k, w, sc0, sc1, ipiv, stats, info, batch, cs, s);
   else launch_s<4, 8, 2 * PT>(C, n, k, w, sc0, sc1, ipiv, stats, info, batch, cs, s);
 }
 

@@ -466,6 +466,21 @@ def test_register_panel_height_spectral(n):
     assert float(torch.linalg.norm(Q - Qs) / torch.linalg.norm(Qs)) <= TOL
 
 
+@pytest.mark.parametrize("variant", ["4", "5", "2"])
+def test_tall_panel_variants(monkeypatch, variant):
+    """The 513..1024-rows-per-CTA cluster panels (n = 8400: 525 rows per CTA at the start):
+    256 threads x 4 rows with an 8-column register chunk (4, default), with a 4-column chunk and
+    12 shared-memory columns (5), 512 threads x 2 rows (2) — each gives the spectral projector."""
+    monkeypatch.setenv("FEAST_TALL_VARIANT", variant)
+    P = synth.make_pencil_torch("C2", n=8400, m0=16)
+    s = P.spec
+    f = _handle(P)
+    Q = f.project(P.A, P.B, P.X0)
+    rho = 1.0 / (1.0 + ((P.lam - s.c) / s.r) ** P.q)
+    Qs = P.V @ (rho[:, None] * torch.linalg.solve(P.V, P.X0))
+    assert float(torch.linalg.norm(Q - Qs) / torch.linalg.norm(Qs)) <= TOL
+
+
 @pytest.mark.parametrize("btrsm", ["1", "0"])
 @pytest.mark.parametrize("nb", ["64", "128", "256", "512"])
 @pytest.mark.parametrize("n,m0", [(1000, 24), (1345, 8)])
