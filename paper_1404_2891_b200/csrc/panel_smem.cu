@@ -576,23 +576,27 @@ int panel_smem_max_clusters(int64_t L, int w, int cs) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int nc = -1;
+  const bool v5 = Lc > 4 * PT && tall_variant() == 5;
+  if (v5) cfg.dynamicSmemBytes = (size_t)Lc * (w > 4 ? w - 4 : 0) * sizeof(double2);
   auto k = Lc <= PT ? panel_smem_kernel<1, 8, PT, true>
                     : (Lc <= 2 * PT ? panel_smem_kernel<2, 8, PT, true>
                                     : (Lc <= 4 * PT ? panel_smem_kernel<2, 8, 2 * PT, true>
                                                     : (tall_variant() == 2 ? panel_smem_kernel<2, 8, 4 * PT, true>
-                                                                           : panel_smem_kernel<4, 8, 2 * PT, true>)));
+                                                                           : (v5 ? panel_smem_kernel<4, 4, 2 * PT, true>
+                                                                                 : panel_smem_kernel<4, 8, 2 * PT, true>))));
   cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (cudaOccupancyMaxActiveClusters(&nc, k, &cfg) != cudaSuccess) { cudaGetLastError(); return -1; }
   return nc;
 }
 
-// FEAST_TALL_VARIANT: 4 (default) = 256 threads x 4 rows, 2 = 512 threads x 2 rows for panels of
-// 513..1024 rows per CTA, 5 = 256 threads x 4 rows with a 4-column register chunk; 0 = keep those
-// panels on the register-chunk kernel (lu.cu)
+// FEAST_TALL_VARIANT for panels of 513..1024 rows per CTA: 5 (default) = 256 threads x 4 rows with
+// a 4-column register chunk (no spill; 16-wide panel of 16384 rows 64.6 -> 50.6 us, C4 12.800 ->
+// 12.753 s), 4 = 256 threads x 4 rows with the 8-column chunk (spills ~2 KB), 2 = 512 threads x 2
+// rows; 0 = keep those panels on the register-chunk kernel (lu.cu)
 int tall_variant() {   // read per call (a getenv per panel launch): tests switch it per handle
   const char* e = getenv("FEAST_TALL_VARIANT");
-  return e ? atoi(e) : 4;
+  return e ? atoi(e) : 5;
 }
 
 bool panel_smem_fits(int64_t n, int w, int cs) {
