@@ -482,7 +482,7 @@ void gemm_gen(feast_ctx* h, int64_t M, int64_t N, int64_t K, bool conjA, const d
 bool smem_panel_for(const feast_ctx* h, int64_t k) {
   if (h->smem_cs_max <= 0) return false;
   const int64_t rows = (h->n - k + h->smem_cs_max - 1) / h->smem_cs_max;   // per CTA
-  return rows <= 256 || (rows <= 1024 && feast::tall_variant() != 0);
+  return rows <= 256 || (rows <= 1024 && feast::tall_variant() != 0) || (rows <= 2048 && feast::very_tall_panels());
 }
 // Panels taller than 256 rows per CTA (n - k > 16 x 256) are 16 wide: the w - 8 columns a CTA
 // keeps in shared memory must fit 190 KB at up to 1024 rows per CTA.
@@ -530,7 +530,8 @@ void factor_block(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, cudaStream_
     const bool smem = smem_panel_for(h, ki);
     // once the panel is short (L <= wide_panel_rows: clusters of <= 8 CTAs x 128 rows), a 64-wide
     // block is one cluster panel: no in-block trsm / update / second swap launch on the chain
-    const int64_t wp = !smem ? 64 : ((h->n - ki <= h->wide_panel_rows) ? 64 : (tall_panel(h, ki) ? 16 : h->wp));
+    const int64_t vt_rows = (h->n - ki + h->smem_cs_max - 1) / h->smem_cs_max;   // rows per CTA
+    const int64_t wp = !smem ? 64 : ((h->n - ki <= h->wide_panel_rows) ? 64 : (vt_rows > 1024 ? 8 : (tall_panel(h, ki) ? 16 : h->wp)));
     // the 64-block is factored as narrow cluster panels of wp columns (small SM footprint), with
     // the in-block U12 (warp TRSM) and update (DMMA) between them
     for (int64_t kp = ki; kp < ki + wi; kp += wp) {

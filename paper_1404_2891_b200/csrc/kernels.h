@@ -69,6 +69,7 @@ void laswp_launch(Batched C, int64_t n, int64_t k, int cnt, const int32_t* ipiv,
                   cudaStream_t s, int variant = LASWP_COALESCED);
 // Cluster panel with the panel resident in shared memory (rows never moved; see panel_smem.cu).
 int tall_variant();
+bool very_tall_panels();   // 1025..2048 rows per CTA on the cluster kernel (FEAST_VTALL)
 bool panel_smem_fits(int64_t n, int w, int cs);
 int panel_smem_max_clusters(int64_t L, int w, int cs);
 // sc0 < sc1: the panel's row swaps are also applied to the columns [sc0, sc1) (fused; no laswp launch)

@@ -594,6 +594,16 @@ int panel_smem_max_clusters(int64_t L, int w, int cs) {
 // a 4-column register chunk (no spill; 16-wide panel of 16384 rows 64.6 -> 50.6 us, C4 12.800 ->
 // 12.753 s), 4 = 256 threads x 4 rows with the 8-column chunk (spills ~2 KB), 2 = 512 threads x 2
 // rows; 0 = keep those panels on the register-chunk kernel (lu.cu)
+// Panels of 1025..2048 rows per CTA (n - k up to 32768: C5's first half) on the cluster kernel
+// too — 8 wide, 256 threads x 8 rows with a 4-column register chunk and the other 4 columns in
+// shared memory (128 KB; ptxas spills ~4.7 KB at 255 registers, still far faster than the
+// register-chunk kernel's ~23 us per column): C5 47.64 -> 47.06 s.  FEAST_VTALL=0: the
+// register-chunk kernel (lu.cu) beyond 1024 rows per CTA.
+bool very_tall_panels() {
+  const char* e = getenv("FEAST_VTALL");
+  return !e || e[0] != '0';
+}
+
 int tall_variant() {   // read per call (a getenv per panel launch): tests switch it per handle
   const char* e = getenv("FEAST_TALL_VARIANT");
   return e ? atoi(e) : 5;
@@ -634,6 +644,7 @@ void panel_smem_launch(Batched C, int64_t n, int64_t k, int w, int32_t* ipiv, do
   else if (Lc <= 4 * PT) launch_s<2, 8, 2 * PT>(C, n, k, w, sc0, sc1, ipiv, stats, info, batch, cs, s);   // 512 rows: 256 x 2
   // 513..1024 rows per CTA (tall panels of n = 16384, w <= 16 so the w - 8 shared columns fit):
   // 256 threads x 4 rows (registers capped at 255) or 512 threads x 2 rows (capped at 128)
+  else if (Lc > 8 * PT) launch_s<8, 4, 2 * PT>(C, n, k, w, sc0, sc1, ipiv, stats, info, batch, cs, s);   // very tall
   else if (tall_variant() == 2) launch_s<2, 8, 4 * PT>(C, n, k, w, sc0, sc1, ipiv, stats, info, batch, cs, s);
   // 5: 256 threads x 4 rows with a 4-column register chunk (254 registers, no spill; the w - 4
   // shared-memory columns take 192 KB at 1024 rows x 16 columns)

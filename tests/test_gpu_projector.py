@@ -466,6 +466,23 @@ def test_register_panel_height_spectral(n):
     assert float(torch.linalg.norm(Q - Qs) / torch.linalg.norm(Qs)) <= TOL
 
 
+@pytest.mark.parametrize("vtall", ["1", "0"])
+def test_very_tall_panels(monkeypatch, vtall):
+    """Panels of 1025..2048 rows per CTA (C5's first half at n = 32768) on the cluster kernel
+    (FEAST_VTALL=1: 8-wide panels, 256 threads x 8 rows) or on the register-chunk kernel: with
+    clusters capped at 8 CTAs, n = 8400 starts at 1050 rows per CTA and walks every panel regime
+    down to one CTA; spectral identity with the closed-form filter."""
+    monkeypatch.setenv("FEAST_VTALL", vtall)
+    monkeypatch.setenv("FEAST_CS_MAX", "8")
+    P = synth.make_pencil_torch("C2", n=8400, m0=16)
+    s = P.spec
+    f = _handle(P)
+    Q = f.project(P.A, P.B, P.X0)
+    rho = 1.0 / (1.0 + ((P.lam - s.c) / s.r) ** P.q)
+    Qs = P.V @ (rho[:, None] * torch.linalg.solve(P.V, P.X0))
+    assert float(torch.linalg.norm(Q - Qs) / torch.linalg.norm(Qs)) <= TOL
+
+
 @pytest.mark.parametrize("variant", ["4", "5", "2"])
 def test_tall_panel_variants(monkeypatch, variant):
     """The 513..1024-rows-per-CTA cluster panels (n = 8400: 525 rows per CTA at the start):

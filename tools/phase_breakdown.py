@@ -95,6 +95,9 @@ for name, sel in (("lu", recs[:last_panel + 1]), ("subst", recs[last_panel + 1:]
             g[2] += fl
     loss = {k: v[1] - v[2] / (REF * 1e9) for k, v in byp.items()}
     print(f"{name}: zgemm time lost vs {REF} TF/s: {sum(loss.values()):.2f} ms — top 20 shapes by loss")
+    if args.out:
+        out.setdefault("shapes", {})[name] = [[fl, v[0], v[1]] for fl, v in byp.items()]
+        json.dump(out, open(args.out, "w"), indent=1)
     for fl, v in sorted(byp.items(), key=lambda kv: -loss[kv[0]])[:20]:
         print(f"   {fl:12.4e} flop/launch {v[0]:6d} launches {v[1]:9.3f} ms {v[2] / (v[1] * 1e-3) / 1e12:6.2f} TF/s"
               f"  lost {loss[fl]:8.2f} ms")
