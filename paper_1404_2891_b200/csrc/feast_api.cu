@@ -74,6 +74,16 @@ struct feast_ctx {
   // (M = N-block rows, K = rows solved so far) instead of pushing its own contribution to every
   // later block (right-looking: M = rows still to solve, K = the block)
   bool subst_dot = false;
+  // FEAST_U12_DOT: the outer U12 = L11^-1 A12 in dot form (left-looking): the 64-row block i of
+  // the outer block first takes the solved blocks' contribution in ONE GEMM (M = 64, K = 64 i)
+  // and is then multiplied by its 64x64 inverse — C read / written once per block instead of the
+  // right-looking K = 64 updates of every later block (M = NBO - 64 (i + 1)).  1: when the dot
+  // grid (64-row tiles x N tiles x batch) fills a wave of 444 CTAs; 2: always (tests); 0: off
+  int u12_dot = 0;
+  // FEAST_SUBST_INNER_DOT: the 64-row blocks INSIDE a substitution outer block in dot form too
+  // (M = 64, K = the block's solved rows, C read / written once per block); 1: with subst_dot when
+  // the grid (64-row tiles x N tiles x batch) fills a wave of 444 CTAs; 2: always (tests); 0: off
+  int inner_dot = 1;
   // FEAST_SUBST_JOIN=1: substitutions once over the whole batch after joining the node groups
   // (measured no faster: C2 16.52 vs 16.39 ms, C4 12.972 vs 12.967 s)
   bool subst_join = false;
@@ -589,6 +599,18 @@ void outer_update(feast_ctx* h, const Lu& v, int64_t K0, int64_t Wo, int64_t c0,
   const int nbat = v.nbat;
   if (h->btrsm) {   // U12 = L11^-1 A12: the fused block solve
     block_solve(h, C, v.Inv, nbat, 0, false, K0, Wo, C + c0 * ld, ld, st, nc, s);
+  } else if (h->u12_dot == 2 || (h->u12_dot == 1 && 2 * ((nc + 31) / 32) * nbat >= 444)) {
+    for (int64_t ki = K0; ki < K1; ki += 64) {   // dot form: Y_i -= L[i, 0:i] Y[0:i]; Y_i <- L_ii^-1 Y_i
+      const int wi = (int)std::min<int64_t>(64, K1 - ki);
+      if (ki > K0) {
+        ZgemmArgs p{wi, nc, ki - K0, C + ki + K0 * ld, ld, st, C + K0 + c0 * ld, ld, st, C + ki + c0 * ld, ld, st,
+                    make_double2(-1, 0), make_double2(1, 0), nbat};
+        feast::zgemm_launch(p, false, feast::ZG_SUB, s);
+      }
+      ZgemmArgs u{wi, nc, wi, inv_ptr(v, ki / 64, 0), 64, h->inv_stride, C + ki + c0 * ld, ld, st, C + ki + c0 * ld,
+                  ld, st, make_double2(1, 0), make_double2(0, 0), nbat, 1};
+      feast::zgemm_launch(u, false, feast::ZG_GEN, s);
+    }
   } else
   for (int64_t ki = K0; ki < K1; ki += 64) {
     const int wi = (int)std::min<int64_t>(64, K1 - ki);
@@ -736,10 +758,15 @@ void diag_apply(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t k, in
 // applied by in-place DMMA products, K = 64 updates inside an outer block) and outer blocks of
 // h->solve_nb rows whose off-block update is ONE DMMA GEMM with K = solve_nb (the K = 64 updates of
 // a one-level sweep keep every CTA in its pipeline prologue / epilogue).
+bool inner_dot(const feast_ctx* h, int nbat, int64_t m) {
+  return h->inner_dot == 2 || (h->inner_dot == 1 && h->subst_dot && 2 * ((m + 31) / 32) * nbat >= 444);
+}
+
 // Y <- L^-1 Y (Y already row-permuted): used when the factors are cached (no augmented LU)
 void solve_right_fwd(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t m) {
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), NB = h->solve_nb;
   double2* C = v.Cw;
+  const bool idot = inner_dot(h, v.nbat, m);
   for (int64_t K0 = 0; K0 < n; K0 += NB) {
     const int64_t K1 = std::min(n, K0 + NB);
     if (h->subst_dot && K0 > 0) {   // Y[K0:K1] -= L[K0:K1, 0:K0] Y[0:K0]
@@ -751,9 +778,14 @@ void solve_right_fwd(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t 
     else
     for (int64_t k = K0; k < K1; k += h->nb) {
       const int w = (int)std::min<int64_t>(h->nb, K1 - k);
+      if (idot && k > K0) {   // Y[k:k+w] -= L[k:k+w, K0:k] Y[K0:k]
+        ZgemmArgs p{w, m, k - K0, C + k + K0 * ld, ld, st, Y + K0, ld, sy, Y + k, ld, sy, make_double2(-1, 0),
+                    make_double2(1, 0), v.nbat};
+        feast::zgemm_launch(p, false, feast::ZG_SUB, v.sm);
+      }
       diag_apply(h, v, Y, sy, k, w, 0, false, m);
       const int64_t rest = K1 - k - w;
-      if (rest > 0) {   // inside the outer block
+      if (!idot && rest > 0) {   // inside the outer block
         ZgemmArgs p{rest, m, w, C + (k + w) + k * ld, ld, st, Y + k, ld, sy, Y + k + w, ld, sy,
                     make_double2(-1, 0), make_double2(1, 0), v.nbat};
         feast::zgemm_launch(p, false, feast::ZG_SUB, v.sm);
@@ -771,6 +803,7 @@ void solve_right_fwd(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t 
 void solve_right_back(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t m) {
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), NB = h->solve_nb;
   double2* C = v.Cw;
+  const bool idot = inner_dot(h, v.nbat, m);
   const int64_t lastK0 = ((n - 1) / NB) * NB;
   for (int64_t K0 = lastK0; K0 >= 0; K0 -= NB) {
     const int64_t K1 = std::min(n, K0 + NB);
@@ -784,8 +817,13 @@ void solve_right_back(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t
     else
     for (int64_t k = last; k >= K0; k -= h->nb) {
       const int w = (int)std::min<int64_t>(h->nb, K1 - k);
+      if (idot && k + w < K1) {   // Y[k:k+w] -= U[k:k+w, k+w:K1] Y[k+w:K1]
+        ZgemmArgs p{w, m, K1 - k - w, C + k + (k + w) * ld, ld, st, Y + k + w, ld, sy, Y + k, ld, sy,
+                    make_double2(-1, 0), make_double2(1, 0), v.nbat};
+        feast::zgemm_launch(p, false, feast::ZG_SUB, v.sm);
+      }
       diag_apply(h, v, Y, sy, k, w, 1, false, m);
-      if (k > K0) {     // Y[K0:k] -= U[K0:k, k:k+w] Y[k:k+w]
+      if (!idot && k > K0) {     // Y[K0:k] -= U[K0:k, k:k+w] Y[k:k+w]
         ZgemmArgs p{k - K0, m, w, C + K0 + k * ld, ld, st, Y + k, ld, sy, Y + K0, ld, sy, make_double2(-1, 0),
                     make_double2(1, 0), v.nbat};
         feast::zgemm_launch(p, false, feast::ZG_SUB, v.sm);
@@ -803,6 +841,7 @@ void solve_right_back(feast_ctx* h, const Lu& v, double2* Y, int64_t sy, int64_t
 void solve_left(feast_ctx* h, const Lu& v, double2* Y) {
   const int64_t n = h->n, ld = h->ldc, st = ld * (n + h->mr), m = h->mr, sy = ld * m, NB = h->solve_nb;
   double2* C = v.Cw;
+  const bool idot = inner_dot(h, v.nbat, m);
   for (int64_t K0 = 0; K0 < n; K0 += NB) {  // U^H: lower, non-unit
     const int64_t K1 = std::min(n, K0 + NB);
     if (h->subst_dot && K0 > 0) {   // Y[K0:K1] -= (U[0:K0, K0:K1])^H Y[0:K0]
@@ -814,9 +853,14 @@ void solve_left(feast_ctx* h, const Lu& v, double2* Y) {
     else
     for (int64_t k = K0; k < K1; k += h->nb) {
       const int w = (int)std::min<int64_t>(h->nb, K1 - k);
+      if (idot && k > K0) {   // Y[k:k+w] -= (U[K0:k, k:k+w])^H Y[K0:k]
+        ZgemmArgs p{w, m, k - K0, C + K0 + k * ld, ld, st, Y + K0, ld, sy, Y + k, ld, sy, make_double2(-1, 0),
+                    make_double2(1, 0), v.nbat};
+        feast::zgemm_launch(p, true, feast::ZG_SUB, v.sm);
+      }
       diag_apply(h, v, Y, sy, k, w, 1, true, m);   // (U_kk^H)^-1 = (U_kk^-1)^H
       const int64_t rest = K1 - k - w;
-      if (rest > 0) {   // Y[k+w:K1] -= (U[k:k+w, k+w:K1])^H Y[k:k+w]
+      if (!idot && rest > 0) {   // Y[k+w:K1] -= (U[k:k+w, k+w:K1])^H Y[k:k+w]
         ZgemmArgs p{rest, m, w, C + k + (k + w) * ld, ld, st, Y + k, ld, sy, Y + k + w, ld, sy,
                     make_double2(-1, 0), make_double2(1, 0), v.nbat};
         feast::zgemm_launch(p, true, feast::ZG_SUB, v.sm);
@@ -841,8 +885,13 @@ void solve_left(feast_ctx* h, const Lu& v, double2* Y) {
     else
     for (int64_t k = last; k >= K0; k -= h->nb) {
       const int w = (int)std::min<int64_t>(h->nb, K1 - k);
+      if (idot && k + w < K1) {   // Y[k:k+w] -= (L[k+w:K1, k:k+w])^H Y[k+w:K1]
+        ZgemmArgs p{w, m, K1 - k - w, C + (k + w) + k * ld, ld, st, Y + k + w, ld, sy, Y + k, ld, sy,
+                    make_double2(-1, 0), make_double2(1, 0), v.nbat};
+        feast::zgemm_launch(p, true, feast::ZG_SUB, v.sm);
+      }
       diag_apply(h, v, Y, sy, k, w, 0, true, m);   // (L_kk^H)^-1 = (L_kk^-1)^H
-      if (k > K0) {     // Y[K0:k] -= (L[k:k+w, K0:k])^H Y[k:k+w]
+      if (!idot && k > K0) {     // Y[K0:k] -= (L[k:k+w, K0:k])^H Y[k:k+w]
         ZgemmArgs p{k - K0, m, w, C + k + K0 * ld, ld, st, Y + k, ld, sy, Y + K0, ld, sy, make_double2(-1, 0),
                     make_double2(1, 0), v.nbat};
         feast::zgemm_launch(p, true, feast::ZG_SUB, v.sm);
@@ -1380,6 +1429,9 @@ int feast_init(feast_handle* out, int64_t n, int64_t m0, double c_re, double c_i
   h->subst_dot = n >= 8192;
   if (const char* e = getenv("FEAST_BTRSM")) h->btrsm = e[0] == '1';
   if (const char* e = getenv("FEAST_SUBST_DOT")) h->subst_dot = e[0] == '1';
+  h->u12_dot = n >= 8192 ? 1 : 0;
+  if (const char* e = getenv("FEAST_SUBST_INNER_DOT")) h->inner_dot = std::max(0, std::min(2, atoi(e)));
+  if (const char* e = getenv("FEAST_U12_DOT")) h->u12_dot = std::max(0, std::min(2, atoi(e)));
   if (const char* e = getenv("FEAST_SUBST_JOIN")) h->subst_join = e[0] == '1';
   if (const char* e = getenv("FEAST_PANEL_SWAP")) h->panel_swap = e[0] != '0';
   if (const char* e = getenv("FEAST_LSWAP_SIDE")) h->lswap_side = e[0] != '0';

@@ -664,3 +664,54 @@ def test_substitution_dot_form(monkeypatch, key, n, m0):
         assert rel(Q, Qo) <= TOL and rel(QL, QLo) <= TOL and rel(Qc, Qco) <= TOL
     for a, b in zip(out["0"], out["1"]):
         assert rel(a, b) <= 1e-12
+
+
+@pytest.mark.parametrize("key,n,m0", [("C2", 700, 24), ("C4", 600, 40)])
+def test_outer_u12_dot_form(monkeypatch, key, n, m0):
+    """FEAST_U12_DOT=2: the outer blocks' U12 = L11^-1 A12 in dot form (each 64-row block takes
+    the solved blocks' contribution in one GEMM with K = 64 i, then its 64x64 inverse) gives the
+    oracle's Q and Q_L on heights of several ragged outer blocks (augmented columns included),
+    and agrees with the right-looking form (FEAST_U12_DOT=0) to rounding."""
+    P = synth.make_pencil(key, n=n, m0=m0)
+    z, w = _oracle_nodes(P)
+    A, B, X = dev(P.A), dev(P.B), dev(P.X0)
+    out = {}
+    for v in ("0", "2"):
+        monkeypatch.setenv("FEAST_U12_DOT", v)
+        f = _handle(P, mode=fb.BI)
+        Q, QL = f.project_bi(A, B, X, X)
+        out[v] = (host(Q), host(QL))
+    Qo = oracle.project(P.A, P.B, P.X0, z, w)
+    QLo = oracle.project(P.A, P.B, P.X0, z, w, left=True)
+    for (Q, QL) in out.values():
+        assert rel(Q, Qo) <= TOL and rel(QL, QLo) <= TOL
+    for a, b in zip(out["0"], out["2"]):
+        assert rel(a, b) <= 1e-12
+
+
+@pytest.mark.parametrize("outer", ["0", "1"])
+def test_substitution_inner_dot_form(monkeypatch, outer):
+    """FEAST_SUBST_INNER_DOT=2: the 64-row blocks inside every substitution outer block (right
+    back, left U^H / L^H, the cached forward solve) in dot form, with right-looking (0) or dot-form
+    (1) outer blocks: the oracle's Q, Q_L and cached-factor Q on several ragged outer blocks, and
+    the right-looking inner form's results to rounding."""
+    P = synth.make_pencil("C4", n=600, m0=40)
+    z, w = _oracle_nodes(P)
+    A, B, X = dev(P.A), dev(P.B), dev(P.X0)
+    X2 = synth.random_block(P.n, P.m0, 7)
+    monkeypatch.setenv("FEAST_SUBST_DOT", outer)
+    out = {}
+    for v in ("0", "2"):
+        monkeypatch.setenv("FEAST_SUBST_INNER_DOT", v)
+        f = _handle(P, mode=fb.BI)
+        f.factor_cache(True)
+        Q, QL = f.project_bi(A, B, X, X)
+        Qc = f.project(A, B, dev(X2))
+        out[v] = (host(Q), host(QL), host(Qc))
+    Qo = oracle.project(P.A, P.B, P.X0, z, w)
+    QLo = oracle.project(P.A, P.B, P.X0, z, w, left=True)
+    Qco = oracle.project(P.A, P.B, X2, z, w)
+    for (Q, QL, Qc) in out.values():
+        assert rel(Q, Qo) <= TOL and rel(QL, QLo) <= TOL and rel(Qc, Qco) <= TOL
+    for a, b in zip(out["0"], out["2"]):
+        assert rel(a, b) <= 1e-12
